@@ -1,0 +1,379 @@
+"""B200-native MIDBF hot path: the butterfly apply (K1), the fused kernel-entry
+sampler that feeds the interpolative decompositions (K3) and the direct-sum
+oracle kernel (K4), all in hand-written sm_100a CUDA behind the C ABI of
+``include/midbf_b200.h``.
+
+This module is the Python mirror of the reference's C++ API
+(``proj/include/midbf/butterfly.hpp``): ``idbf_factorize`` / ``apply`` /
+``apply_transpose`` / ``save_factorization`` / ``load_factorization`` with the
+same argument meaning and error classes (``ValueError`` for the reference's
+``std::invalid_argument``, ``RuntimeError`` for ``std::runtime_error``).
+The shared library ``libmidbf_b200.so`` is built in-tree by
+``__graft_entry__.build()``; there is no CPU fallback — without it, or
+without an sm_100 device, every device call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+__all__ = [
+    "KIND_FIO2D", "KIND_FIO3D", "KIND_LOWRANK", "KIND_NUFFT", "KIND_CONST", "KIND_RANK1",
+    "Kernel", "Factorization", "DevicePlan", "idbf_factorize", "load_factorization", "save_factorization",
+    "apply", "apply_transpose", "random_coefficients", "chain", "device_count", "lib", "MidbfCudaError",
+    "LIB_PATH",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmidbf_b200.so")
+
+KIND_FIO2D, KIND_FIO3D, KIND_LOWRANK, KIND_NUFFT, KIND_CONST, KIND_RANK1 = range(6)
+MIDBF_OK, MIDBF_EINVAL, MIDBF_ELOGIC, MIDBF_ERUNTIME, MIDBF_ECUDA = 0, -1, -2, -3, -4
+
+i64, u64, dptr, iptr, vp = C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_void_p
+
+
+class MidbfCudaError(RuntimeError):
+    """CUDA failure or no sm_100 device (MIDBF_ECUDA)."""
+
+
+class _KernelDesc(C.Structure):  # midbf_kernel_desc
+    _fields_ = [
+        ("kind", C.c_int32), ("dim", C.c_int32), ("rank", C.c_int32),
+        ("nrows", i64), ("ncols", i64),
+        ("X", dptr), ("Omega", dptr), ("A", dptr), ("B", dptr),
+        ("u", dptr), ("v", dptr), ("cre", C.c_double), ("cim", C.c_double),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmidbf_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C paper_1908_09376_b200)")
+        L = C.CDLL(LIB_PATH)
+        L.midbf_last_error.restype = C.c_char_p
+        L.midbf_chain.restype = u64
+        L.midbf_chain.argtypes = [u64, u64]
+        L.midbf_factorize.argtypes = [C.POINTER(vp), C.POINTER(_KernelDesc), i64, i64, C.c_double, i64, u64,
+                                      C.c_int, C.c_int]
+        L.midbf_apply.argtypes = [vp, vp, vp, i64, C.c_int, vp]
+        L.midbf_fact_apply.argtypes = [vp, vp, vp, i64, C.c_int, vp]
+        L.midbf_plan_set_flags.argtypes = [vp, C.c_uint]
+        L.midbf_fact_plan.argtypes = [vp, C.c_uint, C.POINTER(vp)]
+        L.midbf_plan_load.argtypes = [C.POINTER(vp), C.c_char_p, C.c_uint]
+        L.midbf_plan_create.argtypes = [C.POINTER(vp), i64, i64, iptr, iptr, i64, iptr, iptr, iptr, dptr, C.c_uint]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc == MIDBF_OK:
+        return
+    msg = lib().midbf_last_error().decode()
+    if rc == MIDBF_EINVAL:
+        raise ValueError(msg)
+    if rc == MIDBF_ELOGIC:
+        raise AssertionError(msg)
+    if rc == MIDBF_ECUDA:
+        raise MidbfCudaError(msg)
+    raise RuntimeError(msg)
+
+
+def _p(a):
+    return a.ctypes.data_as(dptr)
+
+
+def _ip(a):
+    return a.ctypes.data_as(iptr)
+
+
+def chain(a, b):
+    """Stream derivation of the reference (src/butterfly.cpp:20-27)."""
+    return int(lib().midbf_chain(a, b))
+
+
+def device_count():
+    n = C.c_int()
+    _check(lib().midbf_device_count(C.byref(n)))
+    return n.value
+
+
+def random_coefficients(n, seed):
+    """Complex Gaussian f of the reference experiment (src/experiment.cpp:75-81)."""
+    out = np.empty(n, dtype=np.complex128)
+    _check(lib().midbf_random_coefficients(i64(n), u64(seed), _p(out.view(np.float64))))
+    return out
+
+
+class Kernel:
+    """Typed kernel K(x, xi) = exp(2*pi*i*Phi) (midbf_kernel_desc).
+
+    X, Omega: (N, dim) point sets (always required for factorization: they
+    build the trees); A, B: real (N, r) low-rank phase factors; u, v / const:
+    the reference's rank-one and constant test kernels.
+    """
+
+    def __init__(self, kind, X=None, Omega=None, A=None, B=None, u=None, v=None, const=0j):
+        self._keep = []
+        d = _KernelDesc()
+        d.kind = kind
+        nrows = ncols = 0
+        if X is not None:
+            X = np.ascontiguousarray(X, dtype=np.float64)
+            Omega = np.ascontiguousarray(Omega, dtype=np.float64)
+            self._keep += [X, Omega]
+            d.X, d.Omega, d.dim = _p(X), _p(Omega), X.shape[1]
+            nrows, ncols = X.shape[0], Omega.shape[0]
+        if A is not None:
+            A = np.ascontiguousarray(A, dtype=np.float64)
+            B = np.ascontiguousarray(B, dtype=np.float64)
+            self._keep += [A, B]
+            d.A, d.B, d.rank = _p(A), _p(B), A.shape[1]
+            nrows, ncols = A.shape[0], B.shape[0]
+        if u is not None:
+            u = np.ascontiguousarray(u, dtype=np.complex128)
+            v = np.ascontiguousarray(v, dtype=np.complex128)
+            self._keep += [u, v]
+            d.u, d.v = _p(u.view(np.float64)), _p(v.view(np.float64))
+            nrows, ncols = len(u), len(v)
+        d.cre, d.cim = complex(const).real, complex(const).imag
+        d.nrows, d.ncols = nrows, ncols
+        self.desc = d
+        self.kind, self.nrows, self.ncols = kind, nrows, ncols
+
+    def sample(self, rows_list, cols_list):
+        """K(rows_t, cols_t) for each task t in one fused GPU launch (K3)."""
+        tasks, rid, cid, off = [], [], [], 0
+        for r, c in zip(rows_list, cols_list):
+            tasks.append((len(rid), len(r), len(cid), len(c), off))
+            rid.extend(int(v) for v in r)
+            cid.extend(int(v) for v in c)
+            off += len(r) * len(c)
+        T = np.ascontiguousarray(np.array(tasks, dtype=np.int64).reshape(-1, 5))
+        R = np.ascontiguousarray(np.array(rid, dtype=np.int64))
+        Cc = np.ascontiguousarray(np.array(cid, dtype=np.int64))
+        out = np.empty(max(off, 1), dtype=np.complex128)
+        _check(lib().midbf_sample(C.byref(self.desc), i64(len(tasks)), _ip(T), _ip(R), i64(len(R)), _ip(Cc),
+                                  i64(len(Cc)), _p(out.view(np.float64)), i64(off)))
+        blocks, at = [], 0
+        for (_, nr, _, nc, _) in tasks:
+            blocks.append(out[at:at + nr * nc].reshape((nr, nc), order="F"))
+            at += nr * nc
+        return blocks
+
+    def direct_sum(self, f, rows=None):
+        """g(rows) = sum_j K(rows, j) f(j) on the GPU (K4)."""
+        f = np.ascontiguousarray(f, dtype=np.complex128)
+        if rows is None:
+            rp, n = None, self.nrows
+        else:
+            rows = np.ascontiguousarray(rows, dtype=np.int64)
+            rp, n = _ip(rows), len(rows)
+        g = np.empty(n, dtype=np.complex128)
+        _check(lib().midbf_direct_sum(C.byref(self.desc), _p(f.view(np.float64)), rp, i64(n), _p(g.view(np.float64))))
+        return g
+
+    def eps_b(self, g_b, f, nrows=256, seed=0):
+        """metrics::eps_b_of (src/metrics.cpp:26-48), direct sum on the GPU."""
+        N = len(g_b)
+        if nrows < 1:
+            raise ValueError("eps_b: need at least one sampled row")
+        if nrows >= N:
+            S = np.arange(N, dtype=np.int64)
+        else:
+            S = _rand_subset(N, nrows, seed)
+        gd = self.direct_sum(f, S)
+        num = float(np.sum(np.abs(np.asarray(g_b)[S] - gd) ** 2))
+        den = float(np.sum(np.abs(gd) ** 2))
+        return float(np.sqrt(num)) if den == 0 else float(np.sqrt(num / den))
+
+
+def _rand_subset(n, k, seed):
+    # std::mt19937_64 + uniform_int_distribution partial Fisher-Yates
+    # (src/linalg.cpp:390-400) is reproduced on the host side of the library.
+    out = np.empty(k, dtype=np.int64)
+    L = lib()
+    L.midbf_rand_subset.restype = i64
+    m = L.midbf_rand_subset(i64(n), i64(k), u64(seed), _ip(out))
+    return out[:m]
+
+
+class DevicePlan:
+    """Device arena of one factorization (K1).  apply() takes host numpy
+    arrays or device tensors (anything with data_ptr(); complex128)."""
+
+    def __init__(self, handle, owner=None, owned=True):
+        self._h = handle
+        self._owner = owner
+        self._owned = owned
+        info = np.empty(8, dtype=np.int64)
+        _check(lib().midbf_plan_info(handle, _ip(info)))
+        (self.nrows, self.ncols, self.nfactors, self.total_nnz, self.arena_bytes, self.nstrips, self.directions,
+         self.max_len) = (int(v) for v in info)
+
+    @classmethod
+    def load(cls, path, directions=1):
+        h = vp()
+        _check(lib().midbf_plan_load(C.byref(h), str(path).encode(), directions))
+        return cls(h)
+
+    @classmethod
+    def from_tables(cls, nrows, ncols, row_perm, col_perm, factors, directions=1):
+        """factors: list of (rows, cols, blocks[nb,4], groups[ng,2], [M_b ...]) in product order."""
+        shape = np.array([[f[0], f[1], len(f[2]), len(f[3])] for f in factors], dtype=np.int64).reshape(-1, 4)
+        blocks = np.ascontiguousarray(np.concatenate([np.asarray(f[2], np.int64).reshape(-1, 4) for f in factors]))
+        groups = np.ascontiguousarray(np.concatenate([np.asarray(f[3], np.int64).reshape(-1, 2) for f in factors]))
+        payload = np.concatenate([np.asarray(M, np.complex128).ravel(order="F") for f in factors for M in f[4]]
+                                 + [np.zeros(1, np.complex128)])
+        rp = np.ascontiguousarray(row_perm, dtype=np.int64)
+        cp = np.ascontiguousarray(col_perm, dtype=np.int64)
+        h = vp()
+        _check(lib().midbf_plan_create(C.byref(h), nrows, ncols, _ip(rp), _ip(cp), len(factors), _ip(shape),
+                                       _ip(blocks), _ip(groups), _p(payload.view(np.float64)), directions))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "_h", None):
+            lib().midbf_plan_destroy(self._h)
+            self._h = None
+
+    def set_flags(self, pdl=True, prefetch=True, graph=True):
+        _check(lib().midbf_plan_set_flags(self._h, (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0)))
+
+    def stages(self, transpose=False):
+        out = np.zeros((64, 4), dtype=np.int64)
+        _check(lib().midbf_plan_stages(self._h, 1 if transpose else 0, _ip(out), i64(64)))
+        return [tuple(int(v) for v in r) for r in out if r[2] or r[3]]
+
+    def apply_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
+        """Raw-pointer apply (device or host pointers, cudaStream_t as int)."""
+        _check(lib().midbf_apply(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))
+
+    def apply(self, f, transpose=False, out=None, stream=0):
+        if hasattr(f, "data_ptr"):  # device tensor
+            nrhs = 1 if f.dim() == 1 else f.shape[1]
+            self.apply_ptr(f.data_ptr(), out.data_ptr(), nrhs, transpose, stream)
+            return out
+        f = np.asarray(f, dtype=np.complex128)
+        vec = f.ndim == 1
+        F2 = np.asfortranarray(f.reshape(f.shape[0], -1))
+        nout = self.ncols if transpose else self.nrows
+        nin = self.nrows if transpose else self.ncols
+        if F2.shape[0] != nin:
+            raise ValueError("input length does not match the factorization")
+        g = np.empty((nout, F2.shape[1]), dtype=np.complex128, order="F")
+        self.apply_ptr(F2.ctypes.data, g.ctypes.data, F2.shape[1], transpose)
+        return g[:, 0] if vec else g
+
+
+class Factorization:
+    """Host bf::Factorization (include/midbf/butterfly.hpp:53-70) whose
+    apply runs on the GPU through a cached device plan."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = np.empty(12, dtype=np.int64)
+        eps = C.c_double()
+        _check(lib().midbf_fact_info(handle, _ip(info), C.byref(eps)))
+        (self.nrows, self.ncols, self.L, self.h, self.n0, self.nfactors, self.total_nnz, self.max_factor_nnz,
+         self.k_max, self.t, self.seed, self.exec) = (int(v) for v in info)
+        self.eps = eps.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().midbf_fact_destroy(self._h)
+            self._h = None
+
+    def factor_count(self):
+        return self.nfactors
+
+    def nnz_bound(self, c=4.0):
+        return c * self.k_max * self.k_max / max(self.n0, 1) * max(self.nrows, self.ncols)
+
+    def sample_stats(self):
+        o = np.zeros(2, dtype=np.int64)
+        _check(lib().midbf_fact_stats(self._h, _ip(o)))
+        return int(o[0]), int(o[1])
+
+    def perms(self):
+        rp = np.empty(self.nrows, dtype=np.int64)
+        cp = np.empty(self.ncols, dtype=np.int64)
+        _check(lib().midbf_fact_perms(self._h, _ip(rp), _ip(cp)))
+        return rp, cp
+
+    def factor(self, i):
+        o = np.empty(4, dtype=np.int64)
+        _check(lib().midbf_fact_factor(self._h, i64(i), _ip(o)))
+        rows, cols, nb, ng = (int(v) for v in o)
+        blocks = np.empty((nb, 4), dtype=np.int64)
+        groups = np.empty((ng, 2), dtype=np.int64)
+        _check(lib().midbf_fact_tables(self._h, i64(i), _ip(blocks), _ip(groups)))
+        return rows, cols, blocks, groups
+
+    def block(self, i, b):
+        _, _, blocks, _ = self.factor(i)
+        m, n = int(blocks[b, 2]), int(blocks[b, 3])
+        out = np.empty((m, n), dtype=np.complex128, order="F")
+        _check(lib().midbf_fact_block(self._h, i64(i), i64(b), out.ctypes.data_as(dptr)))
+        return out
+
+    def plan(self, directions=1):
+        h = vp()
+        _check(lib().midbf_fact_plan(self._h, directions, C.byref(h)))
+        return DevicePlan(h, owner=self, owned=False)
+
+    def apply(self, f, transpose=False):
+        f = np.asarray(f, dtype=np.complex128)
+        vec = f.ndim == 1
+        F2 = np.asfortranarray(f.reshape(f.shape[0], -1))
+        nin = self.nrows if transpose else self.ncols
+        if F2.shape[0] != nin:
+            raise ValueError("input length does not match the factorization")
+        g = np.empty((self.ncols if transpose else self.nrows, F2.shape[1]), dtype=np.complex128, order="F")
+        _check(lib().midbf_fact_apply(self._h, F2.ctypes.data, g.ctypes.data, F2.shape[1], 1 if transpose else 0,
+                                      None))
+        return g[:, 0] if vec else g
+
+    def apply_transpose(self, g):
+        return self.apply(g, transpose=True)
+
+    def dense(self):
+        return self.apply(np.eye(self.ncols, dtype=np.complex128))
+
+    def save(self, path):
+        _check(lib().midbf_fact_save(self._h, str(path).encode()))
+
+
+def idbf_factorize(kernel, n0, k=30, eps=1e-9, t=5, seed=0, parallel=True, sampler="device"):
+    """bf::idbf_factorize on trees built at a common depth from the kernel's
+    point sets.  sampler="device": every entry from the GPU sampler (K3);
+    "host": the same descriptor evaluated on the CPU (reference EntryFn path)."""
+    h = vp()
+    _check(lib().midbf_factorize(C.byref(h), C.byref(kernel.desc), n0, k, eps, t, seed, 1 if parallel else 0,
+                                 0 if sampler == "device" else 1))
+    return Factorization(h)
+
+
+def load_factorization(path):
+    h = vp()
+    _check(lib().midbf_fact_load(C.byref(h), str(path).encode()))
+    return Factorization(h)
+
+
+def save_factorization(path, F):
+    F.save(path)
+
+
+def apply(F, f):
+    return F.apply(f)
+
+
+def apply_transpose(F, g):
+    return F.apply(g, transpose=True)

@@ -1,0 +1,42 @@
+// Device-side helpers shared by the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../status.hpp"
+
+namespace midbf::dev {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw detail::CudaFailure(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// Fails loudly when no sm_100 device is present: there is no CPU fallback.
+int require_device();
+
+// Programmatic dependent launch (PTX griddepcontrol, sm_90+): a stage may
+// start its factor-data prefetch while the previous stage drains, and waits
+// here before touching the previous stage's output vector.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// One bulk L2 prefetch of a contiguous global range (TMA unit, no SM
+// registers or shared memory involved).  `bytes` must be a multiple of 16.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Streaming 128-bit load: read once, evict first (factor payload).
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v2.f64 {%0, %1}, [%2];"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p));
+  return v;
+}
+
+}  // namespace midbf::dev

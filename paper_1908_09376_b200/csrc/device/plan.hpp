@@ -1,0 +1,99 @@
+// Device plan of one factorization (K1 apply).  See plan.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace midbf::dev {
+
+// Output strip of <= 32 rows of one stage (one warp).
+struct Strip {
+  int32_t y0;    // first output row
+  int32_t h;     // rows in the strip
+  int32_t seg0;  // first panel in the segment table
+  int32_t nseg;  // panels accumulated in order
+};
+
+// One block panel feeding a strip: h x n, column-pair layout at arena + off.
+struct Seg {
+  int64_t off;    // complex-element offset in the arena (32-byte aligned)
+  int32_t x0;     // first input entry read
+  int32_t n;      // columns
+  int32_t elems;  // padded complex elements of the panel
+  int32_t pad_;
+};
+
+// Host-side view of one factor in MIDBF001 table form.
+struct FactorView {
+  int64_t rows = 0, cols = 0, nblocks = 0, ngroups = 0;
+  const int64_t* blocks = nullptr;   // nblocks x 4
+  const int64_t* groups = nullptr;   // ngroups x 2
+  const double* const* payload = nullptr;  // per block, column-major complex
+};
+
+struct PlanTables {
+  int64_t nrows = 0, ncols = 0, nfactors = 0, total_nnz = 0, total_blocks = 0;
+  const int64_t* row_perm = nullptr;
+  const int64_t* col_perm = nullptr;
+  std::vector<FactorView> factors;  // product order [U^1..U^T, S, V^T..V^1]
+};
+
+struct Stage {
+  int64_t in_len = 0, out_len = 0;
+  int32_t strip0 = 0, nstrips = 0;
+  int64_t arena0 = 0, payload_bytes = 0;
+};
+
+struct Direction {
+  bool built = false;
+  std::vector<Stage> stages;  // application order
+  Strip* d_strips = nullptr;
+  Seg* d_segs = nullptr;
+  double2* d_arena = nullptr;
+  int64_t nstrips = 0, nsegs = 0, arena_elems = 0;
+};
+
+struct GraphEntry {
+  int d;
+  const double2* in;
+  double2* out;
+  int64_t nrhs;
+  cudaGraphExec_t exec;
+};
+
+class Plan {
+ public:
+  Plan(const PlanTables& T, unsigned directions);
+  ~Plan();
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+
+  // f, g: host or device, column-major N x nrhs complex.
+  void apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t stream);
+  void apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+
+  int device = 0;
+  int64_t nrows = 0, ncols = 0, nfactors = 0, total_nnz = 0, max_len = 0;
+  Direction dir[2];
+  bool use_pdl = true, use_prefetch = true, use_graph = true;
+  std::vector<GraphEntry> graphs;
+
+ private:
+  void build_direction(int d, const PlanTables& T);
+  void ensure_buffers(int64_t nrhs);
+  void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+  int* d_row_perm = nullptr;
+  int* d_col_perm = nullptr;
+  double2* d_buf[2] = {nullptr, nullptr};
+  int64_t buf_elems = 0;
+  double2* d_io[2] = {nullptr, nullptr};
+  int64_t io_elems = 0;
+};
+
+std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions);
+
+}  // namespace midbf::dev

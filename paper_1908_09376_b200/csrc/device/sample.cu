@@ -1,0 +1,390 @@
+// K3 — fused batched kernel-entry sampler and K4 — direct O(N^2) sum, sm_100a.
+//
+// K3 replaces the EntryFn fills of shared_sweep (reference
+// src/butterfly.cpp:462-464, 512-514, 598-600) that call
+// polar(1, 2*pi*Phi(x_i, xi_j)) per entry (src/kernels.cpp:18-24, 242-245;
+// low-rank form src/metrics.cpp:18-24).  One launch fills every block of a
+// sweep pass: task t writes the nr x nc column-major block K(rows_t, cols_t).
+// Nothing N x N is materialised; entries are formed from the point sets (or
+// the low-rank factors A, B) on the fly.
+//
+// K4 replaces the direct summation of metrics::eps_b_of (src/metrics.cpp:40-45)
+// and tests/test_butterfly.cpp:29-37: g(i) = sum_j K(i,j) f(j) for selected
+// rows, column range split across CTAs, partial sums reduced in a fixed order.
+//
+// Arithmetic follows the reference expression by expression with
+// non-contracted multiplies/adds (__dmul_rn/__dadd_rn), so the phase Phi is
+// bitwise the x86 value; only the final sincos (CUDA libdevice vs glibc) may
+// differ in the last ulp.  The per-point coefficients c_k(x) are evaluated on
+// the host with glibc exactly as the reference does.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "common.cuh"
+#include "sample.hpp"
+
+namespace midbf::dev {
+
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+struct DevK {
+  int kind, dim, rank;
+  const double* X;     // nrows x dim
+  const double* Om;    // ncols x dim
+  const double* coef;  // nrows x 3, c_k(x) of the FIO phases
+  const double* A;     // nrows x rank
+  const double* B;     // ncols x rank
+  const double2* u;
+  const double2* v;
+  double cre, cim;
+};
+
+__device__ __forceinline__ double2 polar1(double phi) {
+  double s, c;
+  sincos(__dmul_rn(kTwoPi, phi), &s, &c);
+  return make_double2(c, s);
+}
+
+__device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
+  switch (k.kind) {
+    case MIDBF_KERNEL_FIO2D: {
+      const double x0 = k.X[2 * i], x1 = k.X[2 * i + 1];
+      const double c1 = k.coef[3 * i], c2 = k.coef[3 * i + 1];
+      const double w0 = k.Om[2 * j], w1 = k.Om[2 * j + 1];
+      const double lin = __dadd_rn(__dmul_rn(x0, w0), __dmul_rn(x1, w1));
+      const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(c1, c1), w0), w0),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(c2, c2), w1), w1));
+      return polar1(__dadd_rn(lin, __dsqrt_rn(q)));
+    }
+    case MIDBF_KERNEL_FIO3D: {
+      const double* x = k.X + 3 * i;
+      const double* w = k.Om + 3 * j;
+      const double* a = k.coef + 3 * i;
+      const double lin = __dadd_rn(__dadd_rn(__dmul_rn(x[0], w[0]), __dmul_rn(x[1], w[1])), __dmul_rn(x[2], w[2]));
+      const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(a[0], a[0]), w[0]), w[0]),
+                                           __dmul_rn(__dmul_rn(__dmul_rn(a[1], a[1]), w[1]), w[1])),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(a[2], a[2]), w[2]), w[2]));
+      return polar1(__dadd_rn(lin, __dsqrt_rn(q)));
+    }
+    case MIDBF_KERNEL_LOWRANK: {
+      double s = 0.0;
+      for (int q = 0; q < k.rank; ++q) s = __dadd_rn(s, __dmul_rn(k.A[i * k.rank + q], k.B[j * k.rank + q]));
+      return polar1(s);
+    }
+    case MIDBF_KERNEL_NUFFT: {
+      double s = 0.0;
+      for (int q = 0; q < k.dim; ++q) s = __dadd_rn(s, __dmul_rn(k.X[i * k.dim + q], k.Om[j * k.dim + q]));
+      return polar1(s);
+    }
+    case MIDBF_KERNEL_CONST:
+      return make_double2(k.cre, k.cim);
+    default: {  // RANK1
+      const double2 a = k.u[i], b = k.v[j];
+      return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                          __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+    }
+  }
+}
+
+// tasks: ntasks x 5 (row_off, nr, col_off, nc, out_off), out_off relative
+// to this chunk's output base.  One CTA per task, threads stride entries.
+__global__ void __launch_bounds__(256) k3_sample(DevK k, const int64_t* __restrict__ tasks,
+                                                 const int* __restrict__ rid, const int* __restrict__ cid,
+                                                 double2* __restrict__ out) {
+  const int64_t* tk = tasks + 5 * blockIdx.x;
+  const int64_t ro = tk[0], nr = tk[1], co = tk[2], nc = tk[3], oo = tk[4];
+  const int64_t total = nr * nc;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t c = e / nr, r = e - c * nr;
+    out[oo + e] = entry(k, rid[ro + r], cid[co + c]);
+  }
+}
+
+// Direct sum: blockIdx.x covers 256 selected rows (one per thread),
+// blockIdx.y a contiguous column split.  Column data staged in shared memory.
+constexpr int kTile = 256;
+__global__ void __launch_bounds__(256) k4_direct(DevK k, const int* __restrict__ rows, int nsel,
+                                                 const double2* __restrict__ f, int64_t ncols, int64_t cps,
+                                                 double2* __restrict__ partial) {
+  __shared__ double2 fs[kTile];
+  __shared__ int js[kTile];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c0 = blockIdx.y * cps, c1 = min(ncols, c0 + cps);
+  const int64_t i = r < nsel ? rows[r] : 0;
+  double ar = 0.0, ai = 0.0;
+  for (int64_t cb = c0; cb < c1; cb += kTile) {
+    const int cn = static_cast<int>(c1 - cb < kTile ? c1 - cb : kTile);
+    __syncthreads();
+    if (threadIdx.x < cn) {
+      fs[threadIdx.x] = f[cb + threadIdx.x];
+      js[threadIdx.x] = static_cast<int>(cb + threadIdx.x);
+    }
+    __syncthreads();
+    if (r < nsel) {
+      for (int q = 0; q < cn; ++q) {
+        const double2 e = entry(k, i, js[q]);
+        const double2 x = fs[q];
+        // acc += K * f, the same complex product as std::complex (no fma)
+        ar = __dadd_rn(ar, __dsub_rn(__dmul_rn(e.x, x.x), __dmul_rn(e.y, x.y)));
+        ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(e.x, x.y), __dmul_rn(e.y, x.x)));
+      }
+    }
+  }
+  if (r < nsel) partial[static_cast<int64_t>(blockIdx.y) * nsel + r] = make_double2(ar, ai);
+}
+
+__global__ void k4_reduce(const double2* __restrict__ partial, int nsel, int nsplit, double2* __restrict__ g) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nsel) return;
+  double ar = 0.0, ai = 0.0;
+  for (int s = 0; s < nsplit; ++s) {
+    const double2 p = partial[static_cast<int64_t>(s) * nsel + r];
+    ar += p.x;
+    ai += p.y;
+  }
+  g[r] = make_double2(ar, ai);
+}
+
+template <class T>
+T* upload(const T* h, size_t n, const char* what) {
+  if (!h || n == 0) return nullptr;
+  T* d = nullptr;
+  cuda_check(cudaMalloc(&d, n * sizeof(T)), what);
+  cuda_check(cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice), what);
+  return d;
+}
+
+}  // namespace
+
+struct EntrySampler::Impl {
+  DevK k{};
+  std::vector<void*> owned;
+  int64_t nrows = 0, ncols = 0;
+  int64_t launched_entries = 0;
+};
+
+EntrySampler::EntrySampler(const midbf_kernel_desc& kd) : impl_(new Impl) {
+  require_device();
+  Impl& I = *impl_;
+  I.nrows = kd.nrows;
+  I.ncols = kd.ncols;
+  if (kd.nrows < 0 || kd.ncols < 0 || kd.nrows > 0x7fffffff || kd.ncols > 0x7fffffff)
+    throw std::invalid_argument("kernel point counts out of range");
+  DevK& k = I.k;
+  k.kind = kd.kind;
+  k.dim = kd.dim;
+  k.rank = kd.rank;
+  k.cre = kd.cre;
+  k.cim = kd.cim;
+  auto own = [&](void* p) {
+    if (p) I.owned.push_back(p);
+    return p;
+  };
+  switch (kd.kind) {
+    case MIDBF_KERNEL_FIO2D:
+    case MIDBF_KERNEL_FIO3D: {
+      const int dim = kd.kind == MIDBF_KERNEL_FIO2D ? 2 : 3;
+      if (kd.dim != dim || !kd.X || !kd.Omega) throw std::invalid_argument("FIO kernel needs X and Omega of matching dim");
+      std::vector<double> coef(static_cast<size_t>(3 * kd.nrows), 0.0);
+      for (int64_t i = 0; i < kd.nrows; ++i) {
+        const double* x = kd.X + dim * i;
+        if (dim == 2) {  // src/kernels.cpp:20-21
+          coef[3 * i] = (2.0 + std::sin(kTwoPi * x[0]) * std::sin(kTwoPi * x[1])) / 16.0;
+          coef[3 * i + 1] = (2.0 + std::cos(kTwoPi * x[0]) * std::cos(kTwoPi * x[1])) / 16.0;
+        } else {  // BASELINE.json configs[3]
+          const double s0 = std::sin(kTwoPi * x[0]), s1 = std::sin(kTwoPi * x[1]), s2 = std::sin(kTwoPi * x[2]);
+          const double c0 = std::cos(kTwoPi * x[0]), c1 = std::cos(kTwoPi * x[1]), c2 = std::cos(kTwoPi * x[2]);
+          coef[3 * i] = (2.0 + s0 * s1 * s2) / 16.0;
+          coef[3 * i + 1] = (2.0 + c0 * c1 * c2) / 16.0;
+          coef[3 * i + 2] = (2.0 + s0 * c1 * s2) / 16.0;
+        }
+      }
+      k.X = static_cast<double*>(own(upload(kd.X, static_cast<size_t>(dim * kd.nrows), "upload X")));
+      k.Om = static_cast<double*>(own(upload(kd.Omega, static_cast<size_t>(dim * kd.ncols), "upload Omega")));
+      k.coef = static_cast<double*>(own(upload(coef.data(), coef.size(), "upload coef")));
+      break;
+    }
+    case MIDBF_KERNEL_NUFFT:
+      if (kd.dim < 1 || !kd.X || !kd.Omega) throw std::invalid_argument("x.xi kernel needs X and Omega");
+      k.X = static_cast<double*>(own(upload(kd.X, static_cast<size_t>(kd.dim * kd.nrows), "upload X")));
+      k.Om = static_cast<double*>(own(upload(kd.Omega, static_cast<size_t>(kd.dim * kd.ncols), "upload Omega")));
+      break;
+    case MIDBF_KERNEL_LOWRANK:
+      if (kd.rank < 1 || !kd.A || !kd.B) throw std::invalid_argument("low-rank kernel needs A and B");
+      k.A = static_cast<double*>(own(upload(kd.A, static_cast<size_t>(kd.rank * kd.nrows), "upload A")));
+      k.B = static_cast<double*>(own(upload(kd.B, static_cast<size_t>(kd.rank * kd.ncols), "upload B")));
+      break;
+    case MIDBF_KERNEL_CONST:
+      break;
+    case MIDBF_KERNEL_RANK1:
+      if (!kd.u || !kd.v) throw std::invalid_argument("rank-one kernel needs u and v");
+      k.u = static_cast<double2*>(own(upload(reinterpret_cast<const double2*>(kd.u), kd.nrows, "upload u")));
+      k.v = static_cast<double2*>(own(upload(reinterpret_cast<const double2*>(kd.v), kd.ncols, "upload v")));
+      break;
+    default:
+      throw std::invalid_argument("unknown kernel kind");
+  }
+}
+
+EntrySampler::~EntrySampler() {
+  for (void* p : impl_->owned) cudaFree(p);
+}
+
+int64_t EntrySampler::entries_evaluated() const { return impl_->launched_entries; }
+
+void EntrySampler::sample(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+                          const int64_t* col_ids, int64_t n_col_ids, double* out, int64_t out_len) {
+  Impl& I = *impl_;
+  if (ntasks == 0) return;
+  // validate and convert ids
+  std::vector<int> rid(static_cast<size_t>(n_row_ids)), cid(static_cast<size_t>(n_col_ids));
+  for (int64_t q = 0; q < n_row_ids; ++q) {
+    if (row_ids[q] < 0 || row_ids[q] >= I.nrows) throw std::invalid_argument("row id out of range");
+    rid[q] = static_cast<int>(row_ids[q]);
+  }
+  for (int64_t q = 0; q < n_col_ids; ++q) {
+    if (col_ids[q] < 0 || col_ids[q] >= I.ncols) throw std::invalid_argument("column id out of range");
+    cid[q] = static_cast<int>(col_ids[q]);
+  }
+  for (int64_t t = 0; t < ntasks; ++t) {
+    const int64_t* tk = tasks + 5 * t;
+    if (tk[1] < 0 || tk[3] < 0 || tk[0] < 0 || tk[2] < 0 || tk[0] + tk[1] > n_row_ids ||
+        tk[2] + tk[3] > n_col_ids || tk[4] < 0 || tk[4] + tk[1] * tk[3] > out_len)
+      throw std::invalid_argument("sample task outside its id lists or output");
+  }
+  int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
+  int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
+  // chunk the tasks so one device output buffer stays <= 256 MB
+  const int64_t kChunk = int64_t{16} << 20;  // complex entries
+  double2* d_out = nullptr;
+  double2* h_pin = nullptr;
+  int64_t cap = 0;
+  std::vector<int64_t> ctask;
+  int64_t t0 = 0;
+  try {
+    while (t0 < ntasks) {
+      int64_t t1 = t0, total = 0;
+      while (t1 < ntasks && (t1 == t0 || total + tasks[5 * t1 + 1] * tasks[5 * t1 + 3] <= kChunk)) {
+        total += tasks[5 * t1 + 1] * tasks[5 * t1 + 3];
+        ++t1;
+      }
+      if (total > cap) {
+        cudaFree(d_out);
+        cudaFreeHost(h_pin);
+        d_out = nullptr;
+        h_pin = nullptr;
+        cap = total;
+        cuda_check(cudaMalloc(&d_out, std::max<int64_t>(1, cap) * sizeof(double2)), "cudaMalloc sample out");
+        cuda_check(cudaMallocHost(&h_pin, std::max<int64_t>(1, cap) * sizeof(double2)), "cudaMallocHost");
+      }
+      ctask.assign(static_cast<size_t>(5 * (t1 - t0)), 0);
+      int64_t off = 0;
+      for (int64_t t = t0; t < t1; ++t) {
+        for (int q = 0; q < 4; ++q) ctask[5 * (t - t0) + q] = tasks[5 * t + q];
+        ctask[5 * (t - t0) + 4] = off;
+        off += tasks[5 * t + 1] * tasks[5 * t + 3];
+      }
+      int64_t* d_tasks = upload(ctask.data(), ctask.size(), "upload tasks");
+      if (total > 0) {
+        k3_sample<<<static_cast<unsigned>(t1 - t0), 256>>>(I.k, d_tasks, d_rid, d_cid, d_out);
+        cuda_check(cudaGetLastError(), "k3_sample launch");
+        cuda_check(cudaMemcpy(h_pin, d_out, total * sizeof(double2), cudaMemcpyDeviceToHost), "sample D2H");
+      }
+      cudaFree(d_tasks);
+      for (int64_t t = t0; t < t1; ++t) {
+        const int64_t n = tasks[5 * t + 1] * tasks[5 * t + 3];
+        std::memcpy(out + 2 * tasks[5 * t + 4], h_pin + ctask[5 * (t - t0) + 4], static_cast<size_t>(16 * n));
+      }
+      I.launched_entries += total;
+      t0 = t1;
+    }
+  } catch (...) {
+    cudaFree(d_out);
+    cudaFreeHost(h_pin);
+    cudaFree(d_rid);
+    cudaFree(d_cid);
+    throw;
+  }
+  cudaFree(d_out);
+  cudaFreeHost(h_pin);
+  cudaFree(d_rid);
+  cudaFree(d_cid);
+}
+
+void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g) {
+  Impl& I = *impl_;
+  if (nsel == 0) return;
+  std::vector<int> r(static_cast<size_t>(nsel));
+  for (int64_t q = 0; q < nsel; ++q) {
+    const int64_t v = rows ? rows[q] : q;
+    if (v < 0 || v >= I.nrows) throw std::invalid_argument("direct-sum row out of range");
+    r[q] = static_cast<int>(v);
+  }
+  if (nsel > 0x7fffffff) throw std::invalid_argument("too many rows");
+  int* d_rows = upload(r.data(), r.size(), "upload rows");
+  double2* d_f = upload(reinterpret_cast<const double2*>(f), static_cast<size_t>(I.ncols), "upload f");
+  const int rb = static_cast<int>((nsel + 255) / 256);
+  const int64_t target = 148 * 16;
+  int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>((I.ncols + kTile - 1) / kTile, (target + rb - 1) / rb));
+  nsplit = std::min<int64_t>(nsplit, 65535);
+  const int64_t cps = (I.ncols + nsplit - 1) / nsplit;
+  double2 *d_part = nullptr, *d_g = nullptr;
+  cuda_check(cudaMalloc(&d_part, nsplit * nsel * sizeof(double2)), "cudaMalloc partial");
+  cuda_check(cudaMalloc(&d_g, nsel * sizeof(double2)), "cudaMalloc g");
+  k4_direct<<<dim3(rb, static_cast<unsigned>(nsplit)), 256>>>(I.k, d_rows, static_cast<int>(nsel), d_f, I.ncols, cps,
+                                                              d_part);
+  cuda_check(cudaGetLastError(), "k4_direct launch");
+  k4_reduce<<<rb, 256>>>(d_part, static_cast<int>(nsel), static_cast<int>(nsplit), d_g);
+  cuda_check(cudaGetLastError(), "k4_reduce launch");
+  cuda_check(cudaMemcpy(g, d_g, nsel * sizeof(double2), cudaMemcpyDeviceToHost), "direct sum D2H");
+  cudaFree(d_part);
+  cudaFree(d_g);
+  cudaFree(d_rows);
+  cudaFree(d_f);
+}
+
+}  // namespace midbf::dev
+
+using midbf::detail::guard;
+
+extern "C" int midbf_sample(const midbf_kernel_desc* kernel, int64_t ntasks, const int64_t* tasks,
+                            const int64_t* row_ids, int64_t n_row_ids, const int64_t* col_ids, int64_t n_col_ids,
+                            double* out, int64_t out_len) {
+  return guard([&] {
+    if (!kernel) throw std::invalid_argument("null kernel");
+    midbf::dev::EntrySampler s(*kernel);
+    s.sample(ntasks, tasks, row_ids, n_row_ids, col_ids, n_col_ids, out, out_len);
+  });
+}
+
+extern "C" int midbf_direct_sum(const midbf_kernel_desc* kernel, const double* f, const int64_t* rows, int64_t nsel,
+                                double* g) {
+  return guard([&] {
+    if (!kernel || !f || !g) throw std::invalid_argument("null argument");
+    midbf::dev::EntrySampler s(*kernel);
+    s.direct_sum(f, rows, nsel, g);
+  });
+}
+
+extern "C" int midbf_device_count(int* out) {
+  return guard([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+      cudaDeviceProp p;
+      if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++good;
+    }
+    *out = good;
+  });
+}

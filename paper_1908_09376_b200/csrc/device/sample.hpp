@@ -1,0 +1,33 @@
+// K3 entry sampler / K4 direct sum (see sample.cu).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+
+extern "C" {
+#include "midbf_b200.h"
+}
+
+namespace midbf::dev {
+
+// Device copy of one kernel description (point sets / low-rank factors and
+// per-point phase coefficients), reused across the sweeps of a factorization.
+class EntrySampler {
+ public:
+  explicit EntrySampler(const midbf_kernel_desc& kd);
+  ~EntrySampler();
+  EntrySampler(const EntrySampler&) = delete;
+  EntrySampler& operator=(const EntrySampler&) = delete;
+
+  // tasks: ntasks x 5 (row_off, nr, col_off, nc, out_off); host in/out.
+  void sample(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+              const int64_t* col_ids, int64_t n_col_ids, double* out, int64_t out_len);
+  void direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g);
+  int64_t entries_evaluated() const;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace midbf::dev

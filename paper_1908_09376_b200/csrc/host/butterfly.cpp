@@ -1,0 +1,531 @@
+// MIDBF factorization on the host with batched entry sampling, and the
+// drop-in apply that forwards to the device plan.
+//
+// Follows reference src/butterfly.cpp:
+//   idbf_factorize :708-769, shared_sweep :413-622, split_side :380-408,
+//   sample_ids :360-369, leaf_side :279-293, check_inputs :295-305,
+//   stream derivation :18-27.
+// The one structural change is batching: the reference evaluates K inside
+// each (system, unit) OpenMP task; here every sweep pass first gathers all of
+// its (row ids x column ids) blocks and fills them in ONE call of a `Filler`
+// (the GPU sampler K3 for a KernelDesc, or a host EntryFn loop), then runs the
+// IDs on the host under OpenMP.  Draw order, stream seeds, block placement and
+// grouping are the reference's, so a host-filled factorization is identical to
+// the reference algorithm's.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <stdexcept>
+#include <utility>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "../device/sample.hpp"
+#include "../status.hpp"
+#include "midbf/butterfly.hpp"
+#include "midbf_internal.hpp"
+
+namespace midbf::bf {
+namespace {
+
+std::uint64_t mix(std::uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// A contiguous run of ids owned by one tree node at the current unit level;
+// `begin` is its offset inside its side.
+struct Cell {
+  Index node = 0;
+  Index begin = 0;
+  IndexVec ids;
+};
+struct Span {  // one side of a system
+  int level = 0;
+  std::vector<Cell> cells;
+  Index size = 0;
+  Index off = 0;
+};
+struct System {
+  Span row, col;
+};
+struct Skel {  // interpolation operator + kept global ids of one cell
+  MatXc M;
+  IndexVec keep;
+};
+
+struct FillJob {
+  const Index* rows;
+  Index nr;
+  const Index* cols;
+  Index nc;
+  MatXc* out;
+};
+using Filler = std::function<void(std::vector<FillJob>&)>;
+
+Index lift(const tree::ClusterTree& t, Index node, int from, int to) {
+  for (int l = from; l > to; --l) node = t.levels[static_cast<size_t>(l)][static_cast<size_t>(node)].parent;
+  return node;
+}
+
+Span leaves(const tree::ClusterTree& t) {
+  Span s;
+  s.level = t.depth;
+  const auto& lv = t.levels[static_cast<size_t>(t.depth)];
+  s.cells.resize(lv.size());
+  for (size_t q = 0; q < lv.size(); ++q) {
+    s.cells[q].node = static_cast<Index>(q);
+    s.cells[q].begin = s.size;
+    s.cells[q].ids.assign(t.perm.begin() + lv[q].begin, t.perm.begin() + lv[q].end);
+    s.size += lv[q].end - lv[q].begin;
+  }
+  return s;
+}
+
+IndexVec pick(const IndexVec& pool, const MatXd& P, Index want, std::mt19937_64& rng) {
+  const Index n = static_cast<Index>(pool.size());
+  if (n <= want) return pool;
+  MatXd C(n, P.cols());
+  for (Index i = 0; i < n; ++i)
+    for (Index a = 0; a < P.cols(); ++a) C(i, a) = P(pool[static_cast<size_t>(i)], a);
+  const IndexVec sel = la::mock_chebyshev_points(C, want, rng);
+  IndexVec out(sel.size());
+  for (size_t i = 0; i < sel.size(); ++i) out[i] = pool[static_cast<size_t>(sel[i])];
+  return out;
+}
+
+struct Piece {
+  Index anc = -1;
+  Span span;
+};
+
+// Regroup a compressed side one level up and cut it at `level` ancestors.
+std::vector<Piece> regroup(const tree::ClusterTree& tr, const Span& old, const std::vector<Skel>& sk, int level,
+                           Index base) {
+  std::vector<Piece> out;
+  Index used = 0;
+  for (size_t q = 0; q < old.cells.size(); ++q) {
+    const Cell& c = old.cells[q];
+    const Index anc = lift(tr, c.node, old.level, level);
+    if (out.empty() || out.back().anc != anc) {
+      out.emplace_back();
+      out.back().anc = anc;
+      out.back().span.level = old.level - 1;
+      out.back().span.off = base + used;
+    }
+    Span& s = out.back().span;
+    const Index par = tr.levels[static_cast<size_t>(old.level)][static_cast<size_t>(c.node)].parent;
+    if (s.cells.empty() || s.cells.back().node != par) {
+      s.cells.emplace_back();
+      s.cells.back().node = par;
+      s.cells.back().begin = s.size;
+    }
+    auto& ids = s.cells.back().ids;
+    ids.insert(ids.end(), sk[q].keep.begin(), sk[q].keep.end());
+    s.size += static_cast<Index>(sk[q].keep.size());
+    used += static_cast<Index>(sk[q].keep.size());
+  }
+  return out;
+}
+
+struct SweepOut {
+  Factor U, V, S;
+  Index mid_rows = 0, mid_cols = 0;
+  std::vector<System> next;
+};
+
+SweepOut sweep(const Filler& fill, const tree::ClusterTree& tx, const tree::ClusterTree& to, const MatXd& X,
+               const MatXd& Om, const Config& cfg, const std::vector<System>& sys, Index nB, int level, bool last,
+               std::uint64_t salt, Index stage_rows, Index stage_cols) {
+  const Index ns = static_cast<Index>(sys.size());
+  const Index nA = ns / std::max<Index>(nB, 1);
+  const Index want = cfg.rank.k_max * cfg.t;
+  const bool par = cfg.exec == Exec::Parallel;
+  for (Index a = 0; a < nA; ++a)
+    for (Index b = 1; b < nB; ++b)
+      if (sys[a * nB + b].row.cells.size() != sys[a * nB].row.cells.size())
+        throw std::logic_error("row unit layout differs between sibling systems");
+  for (Index b = 0; b < nB; ++b)
+    for (Index a = 1; a < nA; ++a)
+      if (sys[a * nB + b].col.cells.size() != sys[b].col.cells.size())
+        throw std::logic_error("column unit layout differs between sibling systems");
+
+  // column samples, one per system (:434-441)
+  std::vector<IndexVec> csamp(static_cast<size_t>(ns));
+  for (Index s = 0; s < ns; ++s) {
+    IndexVec pool;
+    pool.reserve(static_cast<size_t>(sys[s].col.size));
+    for (const Cell& c : sys[s].col.cells) pool.insert(pool.end(), c.ids.begin(), c.ids.end());
+    std::mt19937_64 rng(mix(mix(salt ^ mix(0x73636f6cull)) ^ mix(static_cast<std::uint64_t>(s))));
+    csamp[s] = pick(pool, Om, want, rng);
+  }
+
+  // row pass: fill all blocks K(cell ids, csamp[s]) at once, then the IDs
+  std::vector<std::vector<Skel>> rsk(static_cast<size_t>(ns));
+  std::vector<std::pair<Index, Index>> rjobs;
+  for (Index s = 0; s < ns; ++s) {
+    rsk[s].resize(sys[s].row.cells.size());
+    for (Index u = 0; u < static_cast<Index>(sys[s].row.cells.size()); ++u) rjobs.emplace_back(s, u);
+  }
+  {
+    std::vector<MatXc> blk(rjobs.size());
+    std::vector<FillJob> jobs;
+    for (size_t q = 0; q < rjobs.size(); ++q) {
+      const auto [s, u] = rjobs[q];
+      const Cell& c = sys[s].row.cells[u];
+      if (c.ids.empty() || csamp[s].empty()) continue;
+      jobs.push_back({c.ids.data(), static_cast<Index>(c.ids.size()), csamp[s].data(),
+                      static_cast<Index>(csamp[s].size()), &blk[q]});
+    }
+    fill(jobs);
+#pragma omp parallel for schedule(dynamic) if (par)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(rjobs.size()); ++q) {
+      const auto [s, u] = rjobs[q];
+      const Cell& c = sys[s].row.cells[u];
+      Skel& o = rsk[s][u];
+      if (c.ids.empty() || csamp[s].empty()) {
+        o.M = MatXc(static_cast<Index>(c.ids.size()), 0);
+        continue;
+      }
+      la::RowID id = la::rid_from_cols(blk[q], cfg.rank);
+      blk[q] = MatXc();
+      o.M = std::move(id.W);
+      for (Index p : id.skeleton) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
+    }
+  }
+
+  std::vector<IndexVec> rhat(static_cast<size_t>(ns));
+  std::vector<IndexVec> ruoff(static_cast<size_t>(ns));
+  std::vector<Index> orow(static_cast<size_t>(ns), 0);
+  Index mid_rows = 0;
+  for (Index s = 0; s < ns; ++s) {
+    orow[s] = mid_rows;
+    for (const Skel& k : rsk[s]) {
+      ruoff[s].push_back(static_cast<Index>(rhat[s].size()));
+      rhat[s].insert(rhat[s].end(), k.keep.begin(), k.keep.end());
+    }
+    mid_rows += static_cast<Index>(rhat[s].size());
+  }
+
+  // row samples for the column pass (:486-491)
+  std::vector<IndexVec> rsamp(static_cast<size_t>(ns));
+  for (Index s = 0; s < ns; ++s) {
+    std::mt19937_64 rng(mix(mix(salt ^ mix(0x73726f77ull)) ^ mix(static_cast<std::uint64_t>(s))));
+    rsamp[s] = pick(rhat[s], X, want, rng);
+  }
+
+  // column pass (:493-519)
+  std::vector<std::vector<Skel>> csk(static_cast<size_t>(ns));
+  std::vector<std::pair<Index, Index>> cjobs;
+  for (Index s = 0; s < ns; ++s) {
+    csk[s].resize(sys[s].col.cells.size());
+    for (Index w = 0; w < static_cast<Index>(sys[s].col.cells.size()); ++w) cjobs.emplace_back(s, w);
+  }
+  {
+    std::vector<MatXc> blk(cjobs.size());
+    std::vector<FillJob> jobs;
+    for (size_t q = 0; q < cjobs.size(); ++q) {
+      const auto [s, w] = cjobs[q];
+      const Cell& c = sys[s].col.cells[w];
+      if (c.ids.empty() || rsamp[s].empty()) continue;
+      jobs.push_back({rsamp[s].data(), static_cast<Index>(rsamp[s].size()), c.ids.data(),
+                      static_cast<Index>(c.ids.size()), &blk[q]});
+    }
+    fill(jobs);
+#pragma omp parallel for schedule(dynamic) if (par)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(cjobs.size()); ++q) {
+      const auto [s, w] = cjobs[q];
+      const Cell& c = sys[s].col.cells[w];
+      Skel& o = csk[s][w];
+      if (c.ids.empty() || rsamp[s].empty()) {
+        o.M = MatXc(0, static_cast<Index>(c.ids.size()));
+        continue;
+      }
+      la::ColumnID id = la::cid_from_rows(blk[q], cfg.rank);
+      blk[q] = MatXc();
+      o.M = std::move(id.V);
+      for (Index p : id.skeleton) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
+    }
+  }
+
+  std::vector<IndexVec> chat(static_cast<size_t>(ns));
+  std::vector<IndexVec> cuoff(static_cast<size_t>(ns));
+  std::vector<Index> ocol(static_cast<size_t>(ns), 0);
+  Index mid_cols = 0;
+  for (Index s = 0; s < ns; ++s) {
+    ocol[s] = mid_cols;
+    for (const Skel& k : csk[s]) {
+      cuoff[s].push_back(static_cast<Index>(chat[s].size()));
+      chat[s].insert(chat[s].end(), k.keep.begin(), k.keep.end());
+    }
+    mid_cols += static_cast<Index>(chat[s].size());
+  }
+
+  SweepOut R;
+  R.mid_rows = mid_rows;
+  R.mid_cols = mid_cols;
+  // U^t: blocks of sibling systems that write the same rows form a group (:539-563)
+  R.U.rows = stage_rows;
+  R.U.cols = mid_rows;
+  for (Index a = 0; a < nA; ++a) {
+    const Index nu = static_cast<Index>(sys[a * nB].row.cells.size());
+    for (Index u = 0; u < nu; ++u) {
+      Index g0 = static_cast<Index>(R.U.blocks.size()), prev = -1;
+      for (Index b = 0; b < nB; ++b) {
+        const Index s = a * nB + b;
+        MatXc& W = rsk[s][u].M;
+        if (W.rows() == 0 || W.cols() == 0) continue;
+        const Index ro = sys[s].row.off + sys[s].row.cells[u].begin;
+        if (prev >= 0 && ro != prev) {
+          R.U.groups.emplace_back(g0, static_cast<Index>(R.U.blocks.size()));
+          g0 = static_cast<Index>(R.U.blocks.size());
+        }
+        prev = ro;
+        R.U.blocks.push_back({ro, orow[s] + ruoff[s][u], std::move(W)});
+      }
+      if (g0 < static_cast<Index>(R.U.blocks.size())) R.U.groups.emplace_back(g0, static_cast<Index>(R.U.blocks.size()));
+    }
+  }
+  // V^t: mirrored (:565-588)
+  R.V.rows = mid_cols;
+  R.V.cols = stage_cols;
+  for (Index b = 0; b < nB; ++b) {
+    const Index nw = static_cast<Index>(sys[b].col.cells.size());
+    for (Index w = 0; w < nw; ++w) {
+      Index g0 = static_cast<Index>(R.V.blocks.size()), prev = -1;
+      for (Index a = 0; a < nA; ++a) {
+        const Index s = a * nB + b;
+        MatXc& V = csk[s][w].M;
+        if (V.rows() == 0 || V.cols() == 0) continue;
+        const Index co = sys[s].col.off + sys[s].col.cells[w].begin;
+        if (prev >= 0 && co != prev) {
+          R.V.groups.emplace_back(g0, static_cast<Index>(R.V.blocks.size()));
+          g0 = static_cast<Index>(R.V.blocks.size());
+        }
+        prev = co;
+        R.V.blocks.push_back({ocol[s] + cuoff[s][w], co, std::move(V)});
+      }
+      if (g0 < static_cast<Index>(R.V.blocks.size())) R.V.groups.emplace_back(g0, static_cast<Index>(R.V.blocks.size()));
+    }
+  }
+  if (last) {  // S: one dense skeleton block per system (:590-604)
+    R.S.rows = mid_rows;
+    R.S.cols = mid_cols;
+    std::vector<MatXc> blk(static_cast<size_t>(ns));
+    std::vector<FillJob> jobs;
+    for (Index s = 0; s < ns; ++s)
+      if (!rhat[s].empty() && !chat[s].empty())
+        jobs.push_back({rhat[s].data(), static_cast<Index>(rhat[s].size()), chat[s].data(),
+                        static_cast<Index>(chat[s].size()), &blk[s]});
+    fill(jobs);
+    for (Index s = 0; s < ns; ++s) {
+      if (rhat[s].empty() || chat[s].empty()) continue;
+      const Index g = static_cast<Index>(R.S.blocks.size());
+      R.S.blocks.push_back({orow[s], ocol[s], std::move(blk[s])});
+      R.S.groups.emplace_back(g, g + 1);
+    }
+  } else {  // child systems one level down (:605-620)
+    const Index na2 = static_cast<Index>(tx.levels[static_cast<size_t>(level)].size());
+    const Index nb2 = static_cast<Index>(to.levels[static_cast<size_t>(level)].size());
+    R.next.resize(static_cast<size_t>(na2 * nb2));
+    for (Index s = 0; s < ns; ++s) {
+      const auto rp = regroup(tx, sys[s].row, rsk[s], level, orow[s]);
+      const auto cp = regroup(to, sys[s].col, csk[s], level, ocol[s]);
+      for (const Piece& a : rp)
+        for (const Piece& b : cp) {
+          System& nx = R.next[static_cast<size_t>(a.anc * nb2 + b.anc)];
+          nx.row = a.span;
+          nx.col = b.span;
+        }
+    }
+  }
+  return R;
+}
+
+Factor eye(Index n) {
+  Factor f;
+  f.rows = f.cols = n;
+  f.blocks.push_back({0, 0, MatXc::Identity(n, n)});
+  f.groups.emplace_back(0, 1);
+  return f;
+}
+
+Factorization factorize(const Filler& fill, const tree::ClusterTree& tx, const tree::ClusterTree& to,
+                        const MatXd& X, const MatXd& Om, const Config& cfg) {
+  if (tx.dim != to.dim) throw std::invalid_argument("row and column trees have different dimensions");
+  if (X.rows() != tx.npoints() || Om.rows() != to.npoints())
+    throw std::invalid_argument("point set sizes do not match the trees");
+  if (X.cols() != tx.dim || Om.cols() != to.dim)
+    throw std::invalid_argument("point coordinates do not match the tree dimension");
+  if (cfg.rank.k_max < 1) throw std::invalid_argument("rank cap must be positive");
+  if (cfg.t < 1) throw std::invalid_argument("sampling oversize must be positive");
+  if (tx.depth != to.depth) throw std::invalid_argument("butterfly factorization requires trees of equal depth");
+  Factorization F;
+  F.nrows = tx.npoints();
+  F.ncols = to.npoints();
+  F.L = tx.depth;
+  F.h = (tx.depth + 1) / 2;
+  F.n0 = tx.n0;
+  F.cfg = cfg;
+  F.row_perm = tx.perm;
+  F.col_perm = to.perm;
+  if (F.L == 0) {  // [I, K, I] (:725-739)
+    Factor S;
+    S.rows = F.nrows;
+    S.cols = F.ncols;
+    MatXc Kd;
+    std::vector<FillJob> jobs{{F.row_perm.data(), F.nrows, F.col_perm.data(), F.ncols, &Kd}};
+    fill(jobs);
+    S.blocks.push_back({0, 0, std::move(Kd)});
+    S.groups.emplace_back(0, 1);
+    F.factors.push_back(eye(F.nrows));
+    F.factors.push_back(std::move(S));
+    F.factors.push_back(eye(F.ncols));
+    return F;
+  }
+  const int T = F.L - F.h + 1;
+  std::vector<System> sys(1);
+  sys[0].row = leaves(tx);
+  sys[0].col = leaves(to);
+  Index nB = 1, sr = F.nrows, sc = F.ncols;
+  std::vector<Factor> Us, Vs;
+  Factor S;
+  for (int t = 1; t <= T; ++t) {
+    SweepOut o = sweep(fill, tx, to, X, Om, cfg, sys, nB, t, t == T,
+                       mix(cfg.seed ^ mix(static_cast<std::uint64_t>(t))), sr, sc);
+    Us.push_back(std::move(o.U));
+    Vs.push_back(std::move(o.V));
+    if (t == T) {
+      S = std::move(o.S);
+    } else {
+      sys = std::move(o.next);
+      nB = static_cast<Index>(to.levels[static_cast<size_t>(t)].size());
+      sr = o.mid_rows;
+      sc = o.mid_cols;
+    }
+  }
+  for (Factor& f : Us) F.factors.push_back(std::move(f));
+  F.factors.push_back(std::move(S));
+  for (auto it = Vs.rbegin(); it != Vs.rend(); ++it) F.factors.push_back(std::move(*it));
+  return F;
+}
+
+Filler host_filler(const EntryFn& K, bool par) {
+  return [&K, par](std::vector<FillJob>& jobs) {
+#pragma omp parallel for schedule(dynamic) if (par)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(jobs.size()); ++q) {
+      FillJob& j = jobs[q];
+      j.out->resize(j.nr, j.nc);
+      for (Index c = 0; c < j.nc; ++c)
+        for (Index r = 0; r < j.nr; ++r) (*j.out)(r, c) = K(j.rows[r], j.cols[c]);
+    }
+  };
+}
+
+Filler device_filler(dev::EntrySampler& smp, FactorizeStats* stats) {
+  return [&smp, stats](std::vector<FillJob>& jobs) {
+    if (jobs.empty()) return;
+    std::vector<std::int64_t> tasks(5 * jobs.size());
+    IndexVec rid, cid;
+    Index total = 0;
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      const FillJob& j = jobs[q];
+      tasks[5 * q] = static_cast<std::int64_t>(rid.size());
+      tasks[5 * q + 1] = j.nr;
+      tasks[5 * q + 2] = static_cast<std::int64_t>(cid.size());
+      tasks[5 * q + 3] = j.nc;
+      tasks[5 * q + 4] = total;
+      rid.insert(rid.end(), j.rows, j.rows + j.nr);
+      cid.insert(cid.end(), j.cols, j.cols + j.nc);
+      total += j.nr * j.nc;
+    }
+    std::vector<double> buf(static_cast<size_t>(2 * total));
+    smp.sample(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(), static_cast<std::int64_t>(rid.size()),
+               cid.data(), static_cast<std::int64_t>(cid.size()), buf.data(), total);
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      FillJob& j = jobs[q];
+      j.out->resize(j.nr, j.nc);
+      std::memcpy(static_cast<void*>(j.out->data()), buf.data() + 2 * tasks[5 * q + 4],
+                  static_cast<size_t>(16 * j.nr * j.nc));
+    }
+    if (stats) {
+      stats->entries += total;
+      stats->launches += 1;
+    }
+  };
+}
+
+}  // namespace
+
+Index Factor::nnz() const {
+  Index n = 0;
+  for (const FactorBlock& b : blocks) n += b.M.size();
+  return n;
+}
+Index Factorization::total_nnz() const {
+  Index n = 0;
+  for (const Factor& f : factors) n += f.nnz();
+  return n;
+}
+Index Factorization::max_factor_nnz() const {
+  Index n = 0;
+  for (const Factor& f : factors) n = std::max(n, f.nnz());
+  return n;
+}
+double Factorization::nnz_bound(double c) const {
+  const double k = static_cast<double>(cfg.rank.k_max);
+  const double N = static_cast<double>(std::max(nrows, ncols));
+  return c * k * k / static_cast<double>(std::max<Index>(n0, 1)) * N;
+}
+
+Factorization idbf_factorize(const EntryFn& K, const tree::ClusterTree& tx, const tree::ClusterTree& to,
+                             const MatXd& X, const MatXd& Om, const Config& cfg) {
+  return factorize(host_filler(K, cfg.exec == Exec::Parallel), tx, to, X, Om, cfg);
+}
+
+Factorization idbf_factorize(const ker::KernelDesc& K, const tree::ClusterTree& tx, const tree::ClusterTree& to,
+                             const MatXd& X, const MatXd& Om, const Config& cfg) {
+  return idbf_factorize_stats(K, tx, to, X, Om, cfg, nullptr);
+}
+
+Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,
+                                   const tree::ClusterTree& to, const MatXd& X, const MatXd& Om, const Config& cfg,
+                                   FactorizeStats* stats) {
+  if (K.nrows != X.rows() || K.ncols != Om.rows())
+    throw std::invalid_argument("kernel description does not match the point sets");
+  dev::EntrySampler smp(K);
+  return factorize(device_filler(smp, stats), tx, to, X, Om, cfg);
+}
+
+MatXc factor_dense(const Factor& F) {
+  MatXc A(F.rows, F.cols);
+  for (const FactorBlock& b : F.blocks)
+    for (Index j = 0; j < b.M.cols(); ++j)
+      for (Index i = 0; i < b.M.rows(); ++i) A(b.row_off + i, b.col_off + j) += b.M(i, j);
+  return A;
+}
+
+// ------------------------------------------------------------------ apply
+MatXc apply_dir(const Factorization& F, const MatXc& in, bool transpose) {
+  const Index nin = transpose ? F.nrows : F.ncols;
+  const Index nout = transpose ? F.ncols : F.nrows;
+  if (in.rows() != nin) throw std::invalid_argument("input length does not match the factorization");
+  midbf_plan_t plan = device_plan(F, transpose ? 2u : 1u);
+  MatXc out(nout, in.cols());
+  if (in.cols() == 0) return out;
+  detail::rethrow(midbf_apply(plan, reinterpret_cast<const double*>(in.data()), reinterpret_cast<double*>(out.data()),
+                              in.cols(), transpose ? 1 : 0, nullptr));
+  return out;
+}
+
+MatXc apply(const Factorization& F, const MatXc& fs) { return apply_dir(F, fs, false); }
+MatXc apply_transpose(const Factorization& F, const MatXc& gs) { return apply_dir(F, gs, true); }
+
+MatXc dense(const Factorization& F) { return bf::apply(F, MatXc::Identity(F.ncols, F.ncols)); }
+
+}  // namespace midbf::bf

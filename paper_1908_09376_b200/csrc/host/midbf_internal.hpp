@@ -1,0 +1,29 @@
+// Internal glue between the C++ host API and the C ABI.
+#pragma once
+
+#include <cstdint>
+
+#include "midbf/butterfly.hpp"
+#include "midbf_b200.h"
+
+namespace midbf::bf {
+
+struct FactorizeStats {
+  std::int64_t entries = 0;   // kernel entries sampled on the device
+  std::int64_t launches = 0;  // sampler calls (one per sweep pass)
+};
+
+Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,
+                                   const tree::ClusterTree& to, const MatXd& X, const MatXd& Om, const Config& cfg,
+                                   FactorizeStats* stats);
+
+// Device plan cached inside the factorization; built (or rebuilt with the
+// union of directions) on demand.
+struct DevicePlanCache {
+  midbf_plan_t plan = nullptr;
+  unsigned directions = 0;
+  ~DevicePlanCache();
+};
+midbf_plan_t device_plan(const Factorization& F, unsigned directions);
+
+}  // namespace midbf::bf

@@ -1,0 +1,87 @@
+"""K3 (fused entry sampler) and K4 (direct sum) on the GPU against the oracle,
+and the device-sampled factorization against the direct sum."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1908_09376_b200 as M
+from helpers import cvec, integer_grid, rel, unit_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _kernels():
+    rng = np.random.default_rng(3)
+    X64 = O.grid2d(64)
+    yield "fio2d_intxi", O.KIND_FIO2D, dict(X=X64, Omega=integer_grid(64))
+    yield "fio2d_unit", O.KIND_FIO2D, dict(X=X64, Omega=X64)
+    yield "fio3d", O.KIND_FIO3D, dict(X=unit_grid(16, 3), Omega=integer_grid(16, 3))
+    A, B = rng.standard_normal((4096, 8)), rng.standard_normal((4096, 8)) * 8
+    yield "lowrank", O.KIND_LOWRANK, dict(A=A, B=B)
+    yield "nufft", O.KIND_NUFFT, dict(X=rng.random((4096, 3)), Omega=rng.random((4096, 3)) * 16)
+    u, v = cvec(4096, 1), cvec(4096, 2)
+    yield "rank1", O.KIND_RANK1, dict(u=u, v=v)
+
+
+@pytest.mark.parametrize("name,kind,kw", list(_kernels()), ids=lambda x: x if isinstance(x, str) else "")
+def test_sampler_matches_oracle_entries(gpu, name, kind, kw):
+    Ko, Km = O.Kernel(kind, **kw), M.Kernel(kind, **kw)
+    rng = np.random.default_rng(9)
+    rows = [rng.choice(Ko.nrows, size=s, replace=False) for s in (64, 7, 150)]
+    cols = [rng.choice(Ko.ncols, size=s, replace=False) for s in (150, 64, 1)]
+    blocks = Km.sample(rows, cols)
+    for r, c, B in zip(rows, cols, blocks):
+        rr, cc = np.meshgrid(r, c, indexing="ij")
+        ref = Ko.entries(rr.ravel(), cc.ravel()).reshape(len(r), len(c))
+        # Phi is evaluated with the reference's exact operation order; only
+        # sincos may differ (CUDA vs glibc) by a few ulp.
+        assert np.abs(B - ref).max() <= 4e-15, name
+
+
+@pytest.mark.parametrize("name,kind,kw", list(_kernels()), ids=lambda x: x if isinstance(x, str) else "")
+def test_direct_sum_matches_oracle(gpu, name, kind, kw):
+    Ko, Km = O.Kernel(kind, **kw), M.Kernel(kind, **kw)
+    f = cvec(Ko.ncols, 17)
+    rows = np.random.default_rng(4).choice(Ko.nrows, 256, replace=False)
+    assert rel(Km.direct_sum(f, rows), Ko.direct_sum(f, rows)) <= 1e-12
+
+
+def test_direct_sum_all_rows(gpu):
+    X = O.grid2d(32)
+    Ko, Km = O.Kernel(O.KIND_FIO2D, X=X, Omega=X), M.Kernel(M.KIND_FIO2D, X=X, Omega=X)
+    f = cvec(1024, 18)
+    assert rel(Km.direct_sum(f), Ko.direct_sum(f)) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [16, 32])
+def test_device_sampled_factorization_accuracy(gpu, n):
+    """tests/test_butterfly.cpp:187-206 with every entry sampled on the GPU."""
+    X = O.grid2d(n)
+    Km = M.Kernel(M.KIND_FIO2D, X=X, Omega=X)
+    F = M.idbf_factorize(Km, 64, k=30, eps=1e-9, sampler="device")
+    assert F.nfactors == 2 * (F.L - F.h + 1) + 1
+    assert F.nfactors == {16: 3, 32: 5}[n]
+    assert F.max_factor_nnz <= F.nnz_bound(4.0)
+    entries, calls = F.sample_stats()
+    assert entries > 0 and calls >= 3
+    f = cvec(n * n, 41 + n)
+    gd = Km.direct_sum(f)
+    assert rel(F.apply(f), gd) <= 1e-5
+    g = cvec(n * n, 43 + n)
+    Ko = O.Kernel(O.KIND_FIO2D, X=X, Omega=X)
+    assert rel(F.apply_transpose(g), Ko.dense().T @ g) <= 1e-5
+
+
+def test_device_and_host_sampling_agree_on_integer_xi(gpu):
+    """Every ID saturates for integer xi, so the
+    device-sampled and host-sampled factorizations have the same structure and
+    the same accuracy against the direct sum."""
+    X, Om = O.grid2d(64), integer_grid(64)
+    Km = M.Kernel(M.KIND_FIO2D, X=X, Omega=Om)
+    Fd = M.idbf_factorize(Km, 64, k=20, eps=1e-9, sampler="device")
+    Fh = M.idbf_factorize(Km, 64, k=20, eps=1e-9, sampler="host")
+    assert Fd.total_nnz == Fh.total_nnz == 471040
+    f = cvec(4096, 5)
+    gd = Km.direct_sum(f)
+    ed, eh = rel(Fd.apply(f), gd), rel(Fh.apply(f), gd)
+    assert abs(ed - eh) <= 0.05 * eh
