@@ -195,7 +195,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flags", type=int, default=7, help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph")
+    ap.add_argument("--flags", type=int, default=15,
+                    help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,7 +220,8 @@ def main():
     t_fac = time.perf_counter() - t0
     entries, sample_calls = F.sample_stats()
     plan = F.plan(1)
-    plan.set_flags(pdl=bool(args.flags & 1), prefetch=bool(args.flags & 2), graph=bool(args.flags & 4))
+    plan.set_flags(pdl=bool(args.flags & 1), prefetch=bool(args.flags & 2), graph=bool(args.flags & 4),
+                   flow=bool(args.flags & 8))
     N = F.ncols
     stages = plan.stages()
     alg_bytes = 16 * F.total_nnz + 16 * nrhs * (F.ncols + F.nrows)
@@ -303,11 +305,11 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_kind": peak_kind, "traffic": None,
                      "algorithmic_bytes_per_apply": alg_bytes,
-                     "note": "achieved = (16*total_nnz + 16*nrhs*(N_in+N_out)) / apply time; the apply is "
-                             f"{len(stages)} k1_stage launches in one graph"},
+                      "note": "achieved = (16*total_nnz + 16*nrhs*(N_in+N_out)) / apply time; one apply = "
+                             f"{plan.launches(nrhs)} kernel launch(es) in one CUDA graph"},
         "e2e": {"value": world * nrhs / e_s, "unit": "matvecs/s", "h2d_bytes_per_step": 16 * N * nrhs,
                 "d2h_bytes_per_step": 16 * F.nrows * nrhs},
-        "gpu_launches": len(stages) * args.steps,
+        "gpu_launches": plan.launches(nrhs) * args.steps,
         "factorize": {"seconds": t_fac, "entries_sampled_on_gpu": entries, "sampler_launch_batches": sample_calls,
                       "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L},
         "stages": [dict(strips=s[0], payload_mb=s[1] / 1e6, in_len=s[2], out_len=s[3]) for s in stages],

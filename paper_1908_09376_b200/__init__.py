@@ -244,8 +244,17 @@ class DevicePlan:
             lib().midbf_plan_destroy(self._h)
             self._h = None
 
-    def set_flags(self, pdl=True, prefetch=True, graph=True):
-        _check(lib().midbf_plan_set_flags(self._h, (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0)))
+    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True):
+        """Kernel-path switches: persistent dataflow kernel (flow) for single
+        RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs."""
+        f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
+        _check(lib().midbf_plan_set_flags(self._h, f))
+
+    def launches(self, nrhs=1, transpose=False):
+        """Kernel launches one apply issues."""
+        out = i64()
+        _check(lib().midbf_plan_launches(self._h, 1 if transpose else 0, i64(nrhs), C.byref(out)))
+        return out.value
 
     def stages(self, transpose=False):
         out = np.zeros((64, 4), dtype=np.int64)

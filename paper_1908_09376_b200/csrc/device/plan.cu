@@ -1,32 +1,40 @@
-// K1 — MIDBF apply on sm_100a: device plan (level-contiguous factor arena) and
-// the per-stage streaming ZGEMV kernel.
+// K1 — MIDBF apply on sm_100a: device plan (one contiguous factor arena) and
+// the apply kernels.
 //
 // Replaces bf::apply_impl / apply_factor (reference src/butterfly.cpp:624-667):
 //   v = f[col_perm];  for factor V^1 .. U^1: v = F_i v;  g[row_perm] = v.
-// In the reference every block is a separately heap-allocated Eigen matrix and
-// each group is an Eigen GEMV under OpenMP.  Here each applied factor (a
-// "stage") becomes a list of row *strips* of <= 32 output rows.  A strip owns
-// the ordered list of block panels that write those rows (the reference's
-// fixed in-group order), so no two warps ever write the same output and no
-// float atomics are used: results are run-to-run bitwise stable.
+// The reference keeps every block as a separately allocated Eigen matrix and
+// runs one OpenMP-parallel Eigen GEMV per group.  Here each applied factor (a
+// "stage") becomes a list of output *strips* of <= 32 rows; a strip owns the
+// ordered list of block panels that write its rows (the reference's fixed
+// in-group block order), so exactly one warp writes every output entry: no
+// atomics, no float reductions across warps, results bitwise reproducible.
 //
-// Arena layout (the whole factorization is one device allocation):
-//   strip panels in stage order, each panel = the strip's rows of one block,
-//   stored as column PAIRS: pair p holds (M(i,2p), M(i,2p+1)) for i = 0..h-1,
-//   so lane i of a warp fetches its row's two columns with one 256-bit
-//   LDG (LDG.E.256, sm_100), and a warp streams h*32 contiguous bytes per
-//   instruction.  An odd last column is stored as h plain complex values.
-//   Panels are padded to 32-byte multiples (<= 16 B each).
-// Perms are fused: stage 0 gathers f through col_perm while staging x into
-// shared memory, the last stage scatters through row_perm.
+// Arena: panel of (strip, block) = the strip's rows of that block, h x n
+// column-major, panels appended in strip order and strips in application
+// order, so one apply streams the arena once, front to back.
+//
+// k1_flow (single RHS, default): ONE persistent launch for all stages.
+//   * 1 CTA per SM, 4 warps; each warp is its own producer and consumer:
+//     lane 0 claims strips from a global counter (strips are numbered stage by
+//     stage, so claims run in dependency order) and streams their panels into
+//     the warp's ring of 3 x 16 KB shared-memory slots with cp.async.bulk
+//     (TMA bulk copy, mbarrier complete_tx), up to 48 KB in flight per warp;
+//   * before touching its input x a strip waits only for the few strips of the
+//     previous stage that produce that x range (per-strip release/acquire
+//     flags carrying the apply epoch) — there is no stage-wide barrier, so HBM
+//     streaming continues across stage boundaries;
+//   * x is staged in a per-warp shared window (stage 0 gathers f through
+//     col_perm), each lane owns one output row; the last stage scatters
+//     through row_perm.
+// k1_stage (multi-RHS fallback and A/B reference): one launch per stage,
+//   warp per strip, streaming 128-bit loads; chained with programmatic
+//   dependent launch inside a CUDA graph.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstring>
-#include <fstream>
-#include <map>
 #include <memory>
-#include <mutex>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -34,37 +42,66 @@
 
 #include "common.cuh"
 #include "plan.hpp"
+#include "flow.cuh"
 
 namespace midbf::dev {
 
 namespace {
 
-constexpr int kWarps = 4;    // warps per CTA (one strip per warp)
-constexpr int kXChunk = 256; // x entries staged per warp per chunk (4 KB)
 constexpr int kStripRows = 32;
 
-__device__ __forceinline__ double4 ld_stream4(const double2* p) {
-  double4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
-               : "l"(p));
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 x) {
+  ar = fma(m.x, x.x, ar);
+  ar = fma(-m.y, x.y, ar);
+  ai = fma(m.x, x.y, ai);
+  ai = fma(m.y, x.x, ai);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ double2 ld_stream2(const double2* p) {
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 
-__device__ __forceinline__ void cmac(double& ar, double& ai, double mr, double mi, double xr, double xi) {
-  ar = fma(mr, xr, ar);
-  ar = fma(-mi, xi, ar);
-  ai = fma(mr, xi, ai);
-  ai = fma(mi, xr, ai);
-}
+// ------------------------------------------------------------ k1_stage
+constexpr int kWarps = 4;
+constexpr int kXChunk = 256;
 
-// One warp per strip.  blockIdx.y selects the right-hand side (v1 multi-RHS:
-// the payload is re-streamed per column).
 template <bool kPrefetch>
 __global__ void __launch_bounds__(kWarps * 32) k1_stage(const Strip* __restrict__ strips, int nstrips,
                                                         const Seg* __restrict__ segs,
@@ -75,31 +112,26 @@ __global__ void __launch_bounds__(kWarps * 32) k1_stage(const Strip* __restrict_
   __shared__ __align__(16) double2 xs[kWarps][kXChunk];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int t = blockIdx.x * kWarps + wid;
-  Strip st = {0, 0, 0, 0};
+  Strip st = {0, 0, 0, 0, 0, 0, 0, 0};
   if (t < nstrips) st = strips[t];
   if (kPrefetch && t < nstrips && lane < st.nseg) {
-    // Factor payload does not depend on the previous stage: pull this
-    // strip's panels toward L2 before waiting on the dependency.
     const Seg s = segs[st.seg0 + lane];
-    bulk_prefetch_l2(arena + s.off, static_cast<uint32_t>(s.elems) * 16u);
+    bulk_prefetch_l2(arena + s.off, static_cast<uint32_t>(s.n) * static_cast<uint32_t>(st.h) * 16u);
   }
   pdl_wait();
   pdl_launch_dependents();
   if (t >= nstrips) return;
   x += blockIdx.y * xld;
   y += blockIdx.y * yld;
-
   const int h = st.h;
-  const bool row_live = lane < h;
+  const bool live = lane < h;
   double ar0 = 0, ai0 = 0, ar1 = 0, ai1 = 0;
   double2* xw = xs[wid];
   for (int si = 0; si < st.nseg; ++si) {
     const Seg s = segs[st.seg0 + si];
-    const double2* P = arena + s.off;
-    const int n = s.n;
-    const int npair = n >> 1;
-    for (int cb = 0; cb < n; cb += kXChunk) {
-      const int cn = min(kXChunk, n - cb);
+    const double2* P = arena + s.off + lane;
+    for (int cb = 0; cb < s.n; cb += kXChunk) {
+      const int cn = min(kXChunk, s.n - cb);
       __syncwarp();
       for (int j = lane; j < cn; j += 32) {
         int idx = s.x0 + cb + j;
@@ -107,39 +139,23 @@ __global__ void __launch_bounds__(kWarps * 32) k1_stage(const Strip* __restrict_
         xw[j] = x[idx];
       }
       __syncwarp();
-      // column pairs fully inside this chunk (cb is even: kXChunk is even)
-      const int p0 = cb >> 1;
-      const int p1 = min(npair, (cb + cn) >> 1);
-      int p = p0;
-      constexpr int U = 4;  // 4 x 256-bit loads in flight per lane per batch
-      for (; p + U <= p1; p += U) {
-        double4 m[U];
+      if (live) {
+        int c = 0;
+        for (; c + 8 <= cn; c += 8) {
+          double2 m[8];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          m[u] = row_live ? ld_stream4(P + 2 * ((int64_t)(p + u) * h + lane)) : make_double4(0, 0, 0, 0);
+          for (int u = 0; u < 8; ++u) m[u] = ld_stream(P + (int64_t)(cb + c + u) * h);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const double2 xa = xw[2 * (p + u) - cb];
-          const double2 xb = xw[2 * (p + u) + 1 - cb];
-          cmac(ar0, ai0, m[u].x, m[u].y, xa.x, xa.y);
-          cmac(ar1, ai1, m[u].z, m[u].w, xb.x, xb.y);
+          for (int u = 0; u < 8; u += 2) {
+            cmac(ar0, ai0, m[u], xw[c + u]);
+            cmac(ar1, ai1, m[u + 1], xw[c + u + 1]);
+          }
         }
-      }
-      for (; p < p1; ++p) {
-        const double4 m = row_live ? ld_stream4(P + 2 * ((int64_t)p * h + lane)) : make_double4(0, 0, 0, 0);
-        const double2 xa = xw[2 * p - cb];
-        const double2 xb = xw[2 * p + 1 - cb];
-        cmac(ar0, ai0, m.x, m.y, xa.x, xa.y);
-        cmac(ar1, ai1, m.z, m.w, xb.x, xb.y);
-      }
-      if ((n & 1) && cb + cn == n) {  // odd tail column, stored as h complex
-        const double2 m = row_live ? ld_stream2(P + 2 * (int64_t)npair * h + lane) : make_double2(0, 0);
-        const double2 xa = xw[n - 1 - cb];
-        cmac(ar0, ai0, m.x, m.y, xa.x, xa.y);
+        for (; c < cn; ++c) cmac(ar0, ai0, ld_stream(P + (int64_t)(cb + c) * h), xw[c]);
       }
     }
   }
-  if (row_live) {
+  if (live) {
     int idx = st.y0 + lane;
     if (yperm) idx = yperm[idx];
     y[idx] = make_double2(ar0 + ar1, ai0 + ai1);
@@ -154,25 +170,57 @@ struct EffBlock {
   int64_t order;
 };
 
-inline void get_entry(const EffBlock& b, int64_t i, int64_t c, double* dst) {
-  const double* src = b.tr ? b.data + 2 * (c + i * b.ld) : b.data + 2 * (i + c * b.ld);
-  dst[0] = src[0];
-  dst[1] = src[1];
+template <int FW, int FS, int SLOT>
+int flow_setup(int num_sms) {
+  const size_t smem = FlowCfg<FW, FS, SLOT>::kSmem;
+  cuda_check(cudaFuncSetAttribute(k1_flow<FW, FS, SLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "flow smem attribute");
+  int per_sm = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_flow<FW, FS, SLOT>, 2 * FW * 32, smem),
+             "occupancy");
+  if (per_sm < 1) throw detail::CudaFailure("k1_flow does not fit on an SM");
+  return std::min(per_sm * num_sms, kMaxFlowCtas);
+}
+
+template <int FW, int FS, int SLOT>
+void flow_launch(FlowParams& P, int grid, cudaStream_t stream, Direction& D, int& last_nwarps) {
+  P.nwarps = grid * FW;
+  if (last_nwarps != P.nwarps) {  // counters assume a fixed warp count
+    cuda_check(cudaMemsetAsync(D.d_sync, 0, (static_cast<size_t>(D.nstrips) + kMaxFlowCtas) * sizeof(unsigned),
+                               stream),
+               "reset flow counters");
+    last_nwarps = P.nwarps;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
+  cfg.blockDim = dim3(2 * FW * 32, 1, 1);
+  cfg.dynamicSmemBytes = FlowCfg<FW, FS, SLOT>::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT>, P), "k1_flow launch");
 }
 
 }  // namespace
 
 // Build one direction (forward or transpose) of the plan on the host and
-// upload it.  Task construction is general (ragged, overlapping, uncovered
-// rows): breakpoints at every block edge, active blocks in reference order.
+// upload it.  Strip construction is general (ragged, overlapping and
+// uncovered rows): breakpoints at every block edge, active blocks in the
+// reference's serial order (groups in order, blocks in group order).
 void Plan::build_direction(int d, const PlanTables& T) {
   Direction& D = dir[d];
   const int64_t nf = T.nfactors;
+  if (nf > kMaxStages) throw std::invalid_argument("too many factors for one device plan");
   D.stages.clear();
   std::vector<Strip> strips;
   std::vector<Seg> segs;
-  std::vector<double> arena;  // interleaved complex, grown per panel
-  arena.reserve(static_cast<size_t>(2 * T.total_nnz + 64 * T.total_blocks));
+  std::vector<double> arena;
+  arena.reserve(static_cast<size_t>(2 * T.total_nnz));
+  int64_t bufoff = 0;
 
   for (int64_t s = 0; s < nf; ++s) {
     const int64_t fi = d == 0 ? nf - 1 - s : s;
@@ -182,34 +230,28 @@ void Plan::build_direction(int d, const PlanTables& T) {
     stg.in_len = d == 0 ? F.cols : F.rows;
     stg.strip0 = static_cast<int32_t>(strips.size());
     stg.arena0 = static_cast<int64_t>(arena.size() / 2);
-    // effective blocks in the reference's serial order: groups, then blocks
+    stg.buf_off = bufoff;
+    if (s + 1 < nf) bufoff += std::max<int64_t>(stg.out_len, 1);
+    if (s > 0 && stg.in_len != D.stages.back().out_len)
+      throw std::invalid_argument("consecutive factors have mismatched inner dimensions");
     std::vector<EffBlock> eb;
     int64_t ord = 0;
     for (int64_t g = 0; g < F.ngroups; ++g) {
       for (int64_t b = F.groups[2 * g]; b < F.groups[2 * g + 1]; ++b) {
         const int64_t* bd = F.blocks + 4 * b;
+        if (bd[2] == 0 || bd[3] == 0) continue;
         EffBlock e;
         e.ld = bd[2];
         e.data = F.payload[static_cast<size_t>(b)];
         e.order = ord++;
-        if (bd[2] == 0 || bd[3] == 0) continue;
-        if (d == 0) {
-          e.yoff = bd[0];
-          e.xoff = bd[1];
-          e.m = bd[2];
-          e.n = bd[3];
-          e.tr = false;
-        } else {
-          e.yoff = bd[1];
-          e.xoff = bd[0];
-          e.m = bd[3];
-          e.n = bd[2];
-          e.tr = true;
-        }
+        e.tr = d != 0;
+        e.yoff = d == 0 ? bd[0] : bd[1];
+        e.xoff = d == 0 ? bd[1] : bd[0];
+        e.m = d == 0 ? bd[2] : bd[3];
+        e.n = d == 0 ? bd[3] : bd[2];
         eb.push_back(e);
       }
     }
-    // breakpoints
     std::vector<int64_t> bp{0, stg.out_len};
     for (const auto& e : eb) {
       bp.push_back(e.yoff);
@@ -217,12 +259,33 @@ void Plan::build_direction(int d, const PlanTables& T) {
     }
     std::sort(bp.begin(), bp.end());
     bp.erase(std::unique(bp.begin(), bp.end()), bp.end());
-    // blocks sorted by start for the active-set sweep
     std::vector<int64_t> by_start(eb.size());
     for (size_t i = 0; i < eb.size(); ++i) by_start[i] = static_cast<int64_t>(i);
     std::sort(by_start.begin(), by_start.end(), [&](int64_t a, int64_t b) { return eb[a].yoff < eb[b].yoff; });
     std::set<std::pair<int64_t, int64_t>> active;  // (order, index)
     size_t next = 0;
+    // producers of the previous stage, for dependency ranges
+    const int32_t prev0 = s > 0 ? D.stages.back().strip0 : 0;
+    const int32_t prev1 = s > 0 ? D.stages.back().strip0 + D.stages.back().nstrips : 0;
+    auto deps = [&](int64_t x0, int64_t n, int32_t& d0, int32_t& d1) {
+      if (s == 0) {
+        d0 = d1 = 0;
+        return;
+      }
+      // first strip with y0 + h > x0, one past the last strip with y0 < x0 + n
+      int32_t lo = prev0, hi = prev1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) / 2;
+        if (strips[mid].y0 + strips[mid].h > x0) hi = mid; else lo = mid + 1;
+      }
+      d0 = lo;
+      hi = prev1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi) / 2;
+        if (strips[mid].y0 < x0 + n) lo = mid + 1; else hi = mid;
+      }
+      d1 = lo;
+    };
     for (size_t q = 0; q + 1 < bp.size(); ++q) {
       const int64_t a = bp[q], b = bp[q + 1];
       if (a >= stg.out_len) break;
@@ -238,35 +301,34 @@ void Plan::build_direction(int d, const PlanTables& T) {
       }
       for (int64_t y = a; y < b; y += kStripRows) {
         const int h = static_cast<int>(std::min<int64_t>(kStripRows, b - y));
-        Strip st;
+        Strip st{};
         st.y0 = static_cast<int32_t>(y);
         st.h = h;
         st.seg0 = static_cast<int32_t>(segs.size());
-        st.nseg = 0;
+        st.stage = static_cast<int32_t>(s);
         for (const auto& pr : active) {
           const EffBlock& e = eb[pr.second];
-          Seg sg;
+          Seg sg{};
           sg.off = static_cast<int64_t>(arena.size() / 2);
           sg.x0 = static_cast<int32_t>(e.xoff);
           sg.n = static_cast<int32_t>(e.n);
+          deps(e.xoff, e.n, sg.dep0, sg.dep1);
           const int64_t r0 = y - e.yoff;
-          const int64_t npair = e.n / 2;
-          size_t base = arena.size();
-          int64_t elems = h * e.n;
-          if (elems & 1) ++elems;  // pad to 32 bytes
-          arena.resize(base + static_cast<size_t>(2 * elems), 0.0);
+          const size_t base = arena.size();
+          arena.resize(base + static_cast<size_t>(2 * h * e.n));
           double* dst = arena.data() + base;
-          for (int64_t p = 0; p < npair; ++p)
+          for (int64_t c = 0; c < e.n; ++c)
             for (int i = 0; i < h; ++i) {
-              get_entry(e, r0 + i, 2 * p, dst + 4 * (p * h + i));
-              get_entry(e, r0 + i, 2 * p + 1, dst + 4 * (p * h + i) + 2);
+              const int64_t r = r0 + i;
+              const double* src = e.tr ? e.data + 2 * (c + r * e.ld) : e.data + 2 * (r + c * e.ld);
+              dst[2 * (c * h + i)] = src[0];
+              dst[2 * (c * h + i) + 1] = src[1];
             }
-          if (e.n & 1)
-            for (int i = 0; i < h; ++i) get_entry(e, r0 + i, e.n - 1, dst + 2 * (2 * npair * h + i));
-          sg.elems = static_cast<int32_t>(elems);
           segs.push_back(sg);
           ++st.nseg;
+          st.xcols += sg.n;
         }
+        D.max_seg = std::max(D.max_seg, static_cast<int>(st.nseg));
         strips.push_back(st);
       }
     }
@@ -274,22 +336,29 @@ void Plan::build_direction(int d, const PlanTables& T) {
     stg.payload_bytes = 16 * (static_cast<int64_t>(arena.size() / 2) - stg.arena0);
     D.stages.push_back(stg);
   }
-  if (strips.size() > 0x7fffffff || segs.size() > 0x7fffffff)
+  if (strips.size() > 0x7ffffff0 || segs.size() > 0x7ffffff0)
     throw std::invalid_argument("factorization too large for one device plan");
   D.nstrips = static_cast<int64_t>(strips.size());
   D.nsegs = static_cast<int64_t>(segs.size());
   D.arena_elems = static_cast<int64_t>(arena.size() / 2);
-  cuda_check(cudaMalloc(&D.d_strips, std::max<size_t>(1, strips.size()) * sizeof(Strip)), "cudaMalloc strips");
-  cuda_check(cudaMalloc(&D.d_segs, std::max<size_t>(1, segs.size()) * sizeof(Seg)), "cudaMalloc segs");
-  cuda_check(cudaMalloc(&D.d_arena, std::max<size_t>(1, arena.size() / 2) * sizeof(double2)), "cudaMalloc arena");
-  cuda_check(cudaMemcpy(D.d_strips, strips.data(), strips.size() * sizeof(Strip), cudaMemcpyHostToDevice), "upload");
-  cuda_check(cudaMemcpy(D.d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice), "upload");
-  cuda_check(cudaMemcpy(D.d_arena, arena.data(), arena.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
+  D.stagebuf_elems = std::max<int64_t>(bufoff, 1);
+  auto up = [](void** dptr, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaMalloc(dptr, std::max<size_t>(bytes, 16)), what);
+    if (bytes) cuda_check(cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice), what);
+  };
+  up(reinterpret_cast<void**>(&D.d_strips), strips.data(), strips.size() * sizeof(Strip), "upload strips");
+  up(reinterpret_cast<void**>(&D.d_segs), segs.data(), segs.size() * sizeof(Seg), "upload segs");
+  up(reinterpret_cast<void**>(&D.d_arena), arena.data(), arena.size() * sizeof(double), "upload arena");
+  cuda_check(cudaMalloc(&D.d_stagebuf, D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
+  const size_t sync_words = static_cast<size_t>(D.nstrips) + kMaxFlowCtas;
+  cuda_check(cudaMalloc(&D.d_sync, sync_words * sizeof(unsigned)), "cudaMalloc sync");
+  cuda_check(cudaMemset(D.d_sync, 0, sync_words * sizeof(unsigned)), "memset sync");
   D.built = true;
 }
 
 Plan::Plan(const PlanTables& T, unsigned directions) {
   device = require_device();
+  cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
   nrows = T.nrows;
   ncols = T.ncols;
   nfactors = T.nfactors;
@@ -304,6 +373,10 @@ Plan::Plan(const PlanTables& T, unsigned directions) {
   cuda_check(cudaMemcpy(d_col_perm, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice), "upload perm");
   for (int d = 0; d < 2; ++d)
     if (directions & (1u << d)) build_direction(d, T);
+  flow_grid[0] = flow_setup<4, 3, 16384>(num_sms);
+  flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
+  flow_grid[2] = flow_setup<6, 4, 8192>(num_sms);
+  flow_grid[3] = flow_grid[0];
 }
 
 Plan::~Plan() {
@@ -311,6 +384,8 @@ Plan::~Plan() {
     cudaFree(D.d_strips);
     cudaFree(D.d_segs);
     cudaFree(D.d_arena);
+    cudaFree(D.d_stagebuf);
+    cudaFree(D.d_sync);
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   cudaFree(d_row_perm);
@@ -319,6 +394,15 @@ Plan::~Plan() {
   cudaFree(d_buf[1]);
   cudaFree(d_io[0]);
   cudaFree(d_io[1]);
+}
+
+bool Plan::flow_ok(int d, int64_t nrhs) const {
+  return nrhs == 1 && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
+}
+
+int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
+  if (flow_ok(d, nrhs)) return 1;
+  return static_cast<int64_t>(dir[d].stages.size());
 }
 
 void Plan::ensure_buffers(int64_t nrhs) {
@@ -332,6 +416,39 @@ void Plan::ensure_buffers(int64_t nrhs) {
     buf_elems = need;
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     graphs.clear();
+  }
+}
+
+void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stream) {
+  Direction& D = dir[d];
+  const int variant = static_cast<int>((flags >> 4) & 3u);
+  FlowParams P{};
+  P.strips = D.d_strips;
+  P.segs = D.d_segs;
+  P.arena = D.d_arena;
+  P.flags = D.d_sync;
+  P.epoch = D.d_sync + D.nstrips;
+  P.nstrips = static_cast<int>(D.nstrips);
+  P.nodeps = (flags & 64u) ? 1 : 0;
+  const int ns = static_cast<int>(D.stages.size());
+  for (int s = 0; s < ns; ++s) {
+    StageIO& io = P.st[s];
+    io.x = s == 0 ? in : D.d_stagebuf + D.stages[s - 1].buf_off;
+    io.y = s == ns - 1 ? out : D.d_stagebuf + D.stages[s].buf_off;
+    io.xperm = s == 0 ? (d == 0 ? d_col_perm : d_row_perm) : nullptr;
+    io.yperm = s == ns - 1 ? (d == 0 ? d_row_perm : d_col_perm) : nullptr;
+  }
+  // The done counter advances by nwarps per apply: keep the variant's warp
+  // count fixed for the plan's lifetime (reset the counters on a change).
+  switch (variant) {
+    case 1:
+      flow_launch<8, 2, 8192>(P, flow_grid[1], stream, D, last_nwarps[d]);
+      break;
+    case 2:
+      flow_launch<6, 4, 8192>(P, flow_grid[2], stream, D, last_nwarps[d]);
+      break;
+    default:
+      flow_launch<4, 3, 16384>(P, flow_grid[0], stream, D, last_nwarps[d]);
   }
 }
 
@@ -352,15 +469,14 @@ void Plan::launch_stages(int d, const double2* in, double2* out, int64_t nrhs, c
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(nblk), static_cast<unsigned>(nrhs), 1);
     cfg.blockDim = dim3(kWarps * 32, 1, 1);
-    cfg.dynamicSmemBytes = 0;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = use_pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = (flags & 1u) ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const Strip* sp = D.d_strips + st.strip0;
-    if (use_prefetch)
+    if (flags & 2u)
       cuda_check(cudaLaunchKernelEx(&cfg, k1_stage<true>, sp, st.nstrips, (const Seg*)D.d_segs,
                                     (const double2*)D.d_arena, x, xld, xp, y, yld, yp),
                  "k1_stage launch");
@@ -371,19 +487,26 @@ void Plan::launch_stages(int d, const double2* in, double2* out, int64_t nrhs, c
   }
 }
 
-// Device-operand apply; the stage chain is captured once per operand set into
-// a CUDA graph (7 launches at cfg1 become one graph launch).
+void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
+  if (flow_ok(d, nrhs))
+    launch_flow(d, in, out, stream);
+  else
+    launch_stages(d, in, out, nrhs, stream);
+}
+
+// Device-operand apply; the launch sequence is captured once per operand set
+// into a CUDA graph.
 void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
   ensure_buffers(nrhs);
   if (dir[d].stages.empty()) return;
-  if (!use_graph) {
-    launch_stages(d, in, out, nrhs, stream);
+  if (!(flags & 4u)) {
+    launch(d, in, out, nrhs, stream);
     cuda_check(cudaGetLastError(), "apply");
     return;
   }
   for (auto& g : graphs)
-    if (g.d == d && g.in == in && g.out == out && g.nrhs == nrhs) {
+    if (g.d == d && g.in == in && g.out == out && g.nrhs == nrhs && g.flags == flags) {
       cuda_check(cudaGraphLaunch(g.exec, stream), "cudaGraphLaunch");
       return;
     }
@@ -391,7 +514,7 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
   cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream create");
   cudaGraph_t graph;
   cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
-  launch_stages(d, in, out, nrhs, cap);
+  launch(d, in, out, nrhs, cap);
   cuda_check(cudaStreamEndCapture(cap, &graph), "end capture");
   cudaGraphExec_t exec;
   cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
@@ -401,7 +524,7 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
     cudaGraphExecDestroy(graphs.front().exec);
     graphs.erase(graphs.begin());
   }
-  graphs.push_back({d, in, out, nrhs, exec});
+  graphs.push_back({d, in, out, nrhs, flags, exec});
   cuda_check(cudaGraphLaunch(exec, stream), "cudaGraphLaunch");
 }
 
@@ -447,243 +570,4 @@ void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaS
   }
 }
 
-// ------------------------------------------------------------- MIDBF001 I/O
-// Container layout: reference include/midbf/butterfly_io.hpp:2-15; checks as
-// src/butterfly_io.cpp:103-167.
-std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions) {
-  std::ifstream f(path, std::ios::binary);
-  if (!f) throw std::runtime_error("cannot open for reading: " + path);
-  const auto need = [&](bool ok, const char* what) {
-    if (!ok) throw std::runtime_error(std::string(what) + " in " + path);
-  };
-  const auto raw = [&]() {
-    int64_t v = 0;
-    f.read(reinterpret_cast<char*>(&v), 8);
-    need(bool(f), "truncated container");
-    return v;
-  };
-  const int64_t big = int64_t{1} << 40;
-  const auto count = [&](const char* what, int64_t mx) {
-    const int64_t v = raw();
-    need(v >= 0 && v <= mx, what);
-    return v;
-  };
-  char magic[8];
-  f.read(magic, 8);
-  need(bool(f), "truncated container");
-  need(std::memcmp(magic, "MIDBF001", 8) == 0, "unrecognized container magic");
-  PlanTables T;
-  T.nrows = count("bad row count", big);
-  T.ncols = count("bad column count", big);
-  count("bad level count", 64);
-  count("bad stop level", 64);
-  count("bad leaf size", big);
-  count("bad rank cap", big);
-  count("bad sampling oversize", big);
-  raw();
-  raw();
-  raw();
-  T.nfactors = count("bad factor count", 4096);
-  std::vector<int64_t> rp(static_cast<size_t>(T.nrows)), cp(static_cast<size_t>(T.ncols));
-  for (auto& v : rp) {
-    v = count("bad row permutation entry", big);
-    need(v < T.nrows, "row permutation out of range");
-  }
-  for (auto& v : cp) {
-    v = count("bad column permutation entry", big);
-    need(v < T.ncols, "column permutation out of range");
-  }
-  std::vector<std::vector<int64_t>> blocks(static_cast<size_t>(T.nfactors)), groups(static_cast<size_t>(T.nfactors));
-  T.factors.resize(static_cast<size_t>(T.nfactors));
-  for (int64_t i = 0; i < T.nfactors; ++i) {
-    FactorView& F = T.factors[static_cast<size_t>(i)];
-    F.rows = count("bad factor rows", big);
-    F.cols = count("bad factor cols", big);
-    const int64_t nb = count("bad block count", big), ng = count("bad group count", big);
-    auto& bl = blocks[static_cast<size_t>(i)];
-    auto& gr = groups[static_cast<size_t>(i)];
-    bl.resize(static_cast<size_t>(4 * nb));
-    gr.resize(static_cast<size_t>(2 * ng));
-    for (int64_t b = 0; b < nb; ++b) {
-      for (int q = 0; q < 4; ++q) bl[4 * b + q] = count(q == 0   ? "bad block row offset"
-                                                        : q == 1 ? "bad block column offset"
-                                                        : q == 2 ? "bad block height"
-                                                                 : "bad block width",
-                                                        big);
-      need(bl[4 * b] + bl[4 * b + 2] <= F.rows && bl[4 * b + 1] + bl[4 * b + 3] <= F.cols,
-           "block outside its factor");
-    }
-    for (int64_t g = 0; g < ng; ++g) {
-      gr[2 * g] = count("bad group begin", big);
-      gr[2 * g + 1] = count("bad group end", big);
-      need(gr[2 * g] <= gr[2 * g + 1] && gr[2 * g + 1] <= nb, "group outside block table");
-    }
-    F.nblocks = nb;
-    F.ngroups = ng;
-  }
-  int64_t total = 0, nblocks_all = 0;
-  for (int64_t i = 0; i < T.nfactors; ++i)
-    for (int64_t b = 0; b < T.factors[i].nblocks; ++b) {
-      total += blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
-      ++nblocks_all;
-    }
-  std::vector<double> payload(static_cast<size_t>(2 * total));
-  f.read(reinterpret_cast<char*>(payload.data()), static_cast<std::streamsize>(16 * total));
-  need(bool(f), "truncated payload");
-  f.peek();
-  need(f.eof(), "trailing bytes after payload");
-  const double* p = payload.data();
-  std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(T.nfactors));
-  for (int64_t i = 0; i < T.nfactors; ++i) {
-    FactorView& F = T.factors[static_cast<size_t>(i)];
-    F.blocks = blocks[i].data();
-    F.groups = groups[i].data();
-    for (int64_t b = 0; b < F.nblocks; ++b) {
-      ptrs[i].push_back(p);
-      p += 2 * blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
-    }
-    F.payload = ptrs[i].data();
-  }
-  T.row_perm = rp.data();
-  T.col_perm = cp.data();
-  T.total_nnz = total;
-  T.total_blocks = nblocks_all;
-  return std::make_unique<Plan>(T, directions);
-}
-
-int require_device() {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
-    cudaGetLastError();
-    throw detail::CudaFailure("no CUDA device visible: the MIDBF B200 path has no CPU fallback");
-  }
-  int dev = 0;
-  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  cudaDeviceProp prop;
-  cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
-  if (prop.major != 10)
-    throw detail::CudaFailure("device " + std::string(prop.name) + " is not sm_100 (this build targets sm_100a)");
-  return dev;
-}
-
 }  // namespace midbf::dev
-
-// ------------------------------------------------------------------ C ABI
-using midbf::detail::guard;
-using midbf::dev::Plan;
-
-struct midbf_plan_s {
-  std::unique_ptr<Plan> p;
-};
-
-extern "C" int midbf_plan_create(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int64_t* row_perm,
-                                 const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
-                                 const int64_t* blocks, const int64_t* groups, const double* payload,
-                                 unsigned directions) {
-  return guard([&] {
-    if (!out) throw std::invalid_argument("null output handle");
-    midbf::dev::PlanTables T;
-    T.nrows = nrows;
-    T.ncols = ncols;
-    T.row_perm = row_perm;
-    T.col_perm = col_perm;
-    T.nfactors = nfactors;
-    T.factors.resize(static_cast<size_t>(nfactors));
-    std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(nfactors));
-    const int64_t* bp = blocks;
-    const int64_t* gp = groups;
-    const double* pp = payload;
-    for (int64_t i = 0; i < nfactors; ++i) {
-      auto& F = T.factors[static_cast<size_t>(i)];
-      F.rows = factor_shape[4 * i];
-      F.cols = factor_shape[4 * i + 1];
-      F.nblocks = factor_shape[4 * i + 2];
-      F.ngroups = factor_shape[4 * i + 3];
-      F.blocks = bp;
-      F.groups = gp;
-      for (int64_t b = 0; b < F.nblocks; ++b) {
-        const int64_t m = bp[4 * b + 2], n = bp[4 * b + 3];
-        if (m < 0 || n < 0 || bp[4 * b] < 0 || bp[4 * b + 1] < 0 || bp[4 * b] + m > F.rows ||
-            bp[4 * b + 1] + n > F.cols)
-          throw std::invalid_argument("block outside its factor");
-        ptrs[i].push_back(pp);
-        pp += 2 * m * n;
-        T.total_nnz += m * n;
-        ++T.total_blocks;
-      }
-      for (int64_t g = 0; g < F.ngroups; ++g)
-        if (gp[2 * g] < 0 || gp[2 * g] > gp[2 * g + 1] || gp[2 * g + 1] > F.nblocks)
-          throw std::invalid_argument("group outside block table");
-      F.payload = ptrs[i].data();
-      bp += 4 * F.nblocks;
-      gp += 2 * F.ngroups;
-    }
-    *out = new midbf_plan_s{std::make_unique<Plan>(T, directions)};
-  });
-}
-
-extern "C" int midbf_plan_load(midbf_plan_t* out, const char* path, unsigned directions) {
-  return guard([&] { *out = new midbf_plan_s{midbf::dev::load_plan(path, directions)}; });
-}
-
-extern "C" int midbf_plan_destroy(midbf_plan_t plan) {
-  return guard([&] { delete plan; });
-}
-
-extern "C" int midbf_plan_info(midbf_plan_t plan, int64_t* out) {
-  return guard([&] {
-    const Plan& p = *plan->p;
-    out[0] = p.nrows;
-    out[1] = p.ncols;
-    out[2] = p.nfactors;
-    out[3] = p.total_nnz;
-    int64_t bytes = 0, tasks = 0;
-    unsigned dirs = 0;
-    for (int d = 0; d < 2; ++d)
-      if (p.dir[d].built) {
-        bytes += p.dir[d].arena_elems * 16;
-        tasks += p.dir[d].nstrips;
-        dirs |= 1u << d;
-      }
-    out[4] = bytes;
-    out[5] = tasks;
-    out[6] = dirs;
-    out[7] = p.max_len;
-  });
-}
-
-extern "C" int midbf_apply(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose, void* stream) {
-  return guard([&] {
-    if (!plan || !f || !g) throw std::invalid_argument("null argument");
-    plan->p->apply(f, g, nrhs, transpose != 0, static_cast<cudaStream_t>(stream));
-  });
-}
-
-// Stage table for benchmarks / roofline accounting:
-// out[s*4 + 0..3] = strips, payload bytes, in_len, out_len of stage s.
-extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap) {
-  return guard([&] {
-    const auto& D = plan->p->dir[transpose ? 1 : 0];
-    int64_t s = 0;
-    for (const auto& st : D.stages) {
-      if (s >= cap) break;
-      out[4 * s] = st.nstrips;
-      out[4 * s + 1] = st.payload_bytes;
-      out[4 * s + 2] = st.in_len;
-      out[4 * s + 3] = st.out_len;
-      ++s;
-    }
-  });
-}
-
-// Tuning switches (bench / profiling): bit0 PDL, bit1 L2 bulk prefetch, bit2 graphs.
-extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
-  return guard([&] {
-    Plan& p = *plan->p;
-    p.use_pdl = flags & 1u;
-    p.use_prefetch = flags & 2u;
-    p.use_graph = flags & 4u;
-    for (auto& g : p.graphs) cudaGraphExecDestroy(g.exec);
-    p.graphs.clear();
-  });
-}

@@ -10,28 +10,35 @@
 
 namespace midbf::dev {
 
-// Output strip of <= 32 rows of one stage (one warp).
+constexpr int kMaxStages = 64;
+constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words after the strip flags
+
+// Output strip of <= 32 rows of one stage; one warp computes it.
 struct Strip {
-  int32_t y0;    // first output row
-  int32_t h;     // rows in the strip
-  int32_t seg0;  // first panel in the segment table
-  int32_t nseg;  // panels accumulated in order
+  int32_t y0;     // first output row (stage-local)
+  int32_t h;      // rows
+  int32_t seg0;   // first panel in the segment table
+  int32_t nseg;   // panels accumulated in the reference's block order
+  int32_t stage;  // application stage
+  int32_t xcols;  // sum of the panel widths (staged x entries)
+  int32_t pad_[2];
 };
 
-// One block panel feeding a strip: h x n, column-pair layout at arena + off.
+// One block panel feeding a strip: h x n complex, column-major, at arena+off.
 struct Seg {
-  int64_t off;    // complex-element offset in the arena (32-byte aligned)
-  int32_t x0;     // first input entry read
-  int32_t n;      // columns
-  int32_t elems;  // padded complex elements of the panel
-  int32_t pad_;
+  int64_t off;   // complex-element offset in the arena
+  int32_t x0;    // first input entry read (stage-local)
+  int32_t n;     // columns
+  int32_t dep0;  // producer strips [dep0, dep1) of the previous stage (global ids)
+  int32_t dep1;
+  int32_t pad_[2];
 };
 
 // Host-side view of one factor in MIDBF001 table form.
 struct FactorView {
   int64_t rows = 0, cols = 0, nblocks = 0, ngroups = 0;
-  const int64_t* blocks = nullptr;   // nblocks x 4
-  const int64_t* groups = nullptr;   // ngroups x 2
+  const int64_t* blocks = nullptr;         // nblocks x 4
+  const int64_t* groups = nullptr;         // ngroups x 2
   const double* const* payload = nullptr;  // per block, column-major complex
 };
 
@@ -46,6 +53,7 @@ struct Stage {
   int64_t in_len = 0, out_len = 0;
   int32_t strip0 = 0, nstrips = 0;
   int64_t arena0 = 0, payload_bytes = 0;
+  int64_t buf_off = 0;  // offset of this stage's output in the stage buffer
 };
 
 struct Direction {
@@ -54,7 +62,10 @@ struct Direction {
   Strip* d_strips = nullptr;
   Seg* d_segs = nullptr;
   double2* d_arena = nullptr;
-  int64_t nstrips = 0, nsegs = 0, arena_elems = 0;
+  double2* d_stagebuf = nullptr;  // outputs of every stage but the last
+  unsigned* d_sync = nullptr;     // [strip flags (nstrips) | per-CTA epochs (kMaxFlowCtas)]
+  int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
+  int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
 };
 
 struct GraphEntry {
@@ -62,6 +73,7 @@ struct GraphEntry {
   const double2* in;
   double2* out;
   int64_t nrhs;
+  unsigned flags;
   cudaGraphExec_t exec;
 };
 
@@ -77,15 +89,25 @@ class Plan {
   void apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
 
   int device = 0;
+  int num_sms = 0;
   int64_t nrows = 0, ncols = 0, nfactors = 0, total_nnz = 0, max_len = 0;
   Direction dir[2];
-  bool use_pdl = true, use_prefetch = true, use_graph = true;
+  // bit0 PDL + bit1 L2 prefetch (stage kernels), bit2 CUDA graphs,
+  // bit3 persistent dataflow kernel for single-RHS applies,
+  // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size).
+  unsigned flags = 0xF;
   std::vector<GraphEntry> graphs;
+  int flow_grid[4] = {0, 0, 0, 0};
+  int64_t launches_per_apply(int d, int64_t nrhs) const;
+  bool flow_ok(int d, int64_t nrhs) const;
+  int last_nwarps[2] = {0, 0};
 
  private:
   void build_direction(int d, const PlanTables& T);
   void ensure_buffers(int64_t nrhs);
+  void launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+  void launch_flow(int d, const double2* in, double2* out, cudaStream_t stream);
   int* d_row_perm = nullptr;
   int* d_col_perm = nullptr;
   double2* d_buf[2] = {nullptr, nullptr};

@@ -1,0 +1,256 @@
+// MIDBF001 container -> device plan, device checks, and the plan C ABI
+// (include/midbf_b200.h "plan" section).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "plan.hpp"
+
+namespace midbf::dev {
+
+// ------------------------------------------------------------- MIDBF001 I/O
+// Container layout: reference include/midbf/butterfly_io.hpp:2-15; checks as
+// src/butterfly_io.cpp:103-167.
+std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot open for reading: " + path);
+  const auto need = [&](bool ok, const char* what) {
+    if (!ok) throw std::runtime_error(std::string(what) + " in " + path);
+  };
+  const auto raw = [&]() {
+    int64_t v = 0;
+    f.read(reinterpret_cast<char*>(&v), 8);
+    need(bool(f), "truncated container");
+    return v;
+  };
+  const int64_t big = int64_t{1} << 40;
+  const auto count = [&](const char* what, int64_t mx) {
+    const int64_t v = raw();
+    need(v >= 0 && v <= mx, what);
+    return v;
+  };
+  char magic[8];
+  f.read(magic, 8);
+  need(bool(f), "truncated container");
+  need(std::memcmp(magic, "MIDBF001", 8) == 0, "unrecognized container magic");
+  PlanTables T;
+  T.nrows = count("bad row count", big);
+  T.ncols = count("bad column count", big);
+  count("bad level count", 64);
+  count("bad stop level", 64);
+  count("bad leaf size", big);
+  count("bad rank cap", big);
+  count("bad sampling oversize", big);
+  raw();
+  raw();
+  raw();
+  T.nfactors = count("bad factor count", 4096);
+  std::vector<int64_t> rp(static_cast<size_t>(T.nrows)), cp(static_cast<size_t>(T.ncols));
+  for (auto& v : rp) {
+    v = count("bad row permutation entry", big);
+    need(v < T.nrows, "row permutation out of range");
+  }
+  for (auto& v : cp) {
+    v = count("bad column permutation entry", big);
+    need(v < T.ncols, "column permutation out of range");
+  }
+  std::vector<std::vector<int64_t>> blocks(static_cast<size_t>(T.nfactors)), groups(static_cast<size_t>(T.nfactors));
+  T.factors.resize(static_cast<size_t>(T.nfactors));
+  for (int64_t i = 0; i < T.nfactors; ++i) {
+    FactorView& F = T.factors[static_cast<size_t>(i)];
+    F.rows = count("bad factor rows", big);
+    F.cols = count("bad factor cols", big);
+    const int64_t nb = count("bad block count", big), ng = count("bad group count", big);
+    auto& bl = blocks[static_cast<size_t>(i)];
+    auto& gr = groups[static_cast<size_t>(i)];
+    bl.resize(static_cast<size_t>(4 * nb));
+    gr.resize(static_cast<size_t>(2 * ng));
+    for (int64_t b = 0; b < nb; ++b) {
+      for (int q = 0; q < 4; ++q) bl[4 * b + q] = count(q == 0   ? "bad block row offset"
+                                                        : q == 1 ? "bad block column offset"
+                                                        : q == 2 ? "bad block height"
+                                                                 : "bad block width",
+                                                        big);
+      need(bl[4 * b] + bl[4 * b + 2] <= F.rows && bl[4 * b + 1] + bl[4 * b + 3] <= F.cols,
+           "block outside its factor");
+    }
+    for (int64_t g = 0; g < ng; ++g) {
+      gr[2 * g] = count("bad group begin", big);
+      gr[2 * g + 1] = count("bad group end", big);
+      need(gr[2 * g] <= gr[2 * g + 1] && gr[2 * g + 1] <= nb, "group outside block table");
+    }
+    F.nblocks = nb;
+    F.ngroups = ng;
+  }
+  int64_t total = 0, nblocks_all = 0;
+  for (int64_t i = 0; i < T.nfactors; ++i)
+    for (int64_t b = 0; b < T.factors[i].nblocks; ++b) {
+      total += blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
+      ++nblocks_all;
+    }
+  std::vector<double> payload(static_cast<size_t>(2 * total));
+  f.read(reinterpret_cast<char*>(payload.data()), static_cast<std::streamsize>(16 * total));
+  need(bool(f), "truncated payload");
+  f.peek();
+  need(f.eof(), "trailing bytes after payload");
+  const double* p = payload.data();
+  std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(T.nfactors));
+  for (int64_t i = 0; i < T.nfactors; ++i) {
+    FactorView& F = T.factors[static_cast<size_t>(i)];
+    F.blocks = blocks[i].data();
+    F.groups = groups[i].data();
+    for (int64_t b = 0; b < F.nblocks; ++b) {
+      ptrs[i].push_back(p);
+      p += 2 * blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
+    }
+    F.payload = ptrs[i].data();
+  }
+  T.row_perm = rp.data();
+  T.col_perm = cp.data();
+  T.total_nnz = total;
+  T.total_blocks = nblocks_all;
+  return std::make_unique<Plan>(T, directions);
+}
+
+int require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw detail::CudaFailure("no CUDA device visible: the MIDBF B200 path has no CPU fallback");
+  }
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaDeviceProp prop;
+  cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    throw detail::CudaFailure("device " + std::string(prop.name) + " is not sm_100 (this build targets sm_100a)");
+  return dev;
+}
+
+}  // namespace midbf::dev
+
+// ------------------------------------------------------------------ C ABI
+using midbf::detail::guard;
+using midbf::dev::Plan;
+
+struct midbf_plan_s {
+  std::unique_ptr<Plan> p;
+};
+
+extern "C" int midbf_plan_create(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int64_t* row_perm,
+                                 const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
+                                 const int64_t* blocks, const int64_t* groups, const double* payload,
+                                 unsigned directions) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output handle");
+    midbf::dev::PlanTables T;
+    T.nrows = nrows;
+    T.ncols = ncols;
+    T.row_perm = row_perm;
+    T.col_perm = col_perm;
+    T.nfactors = nfactors;
+    T.factors.resize(static_cast<size_t>(nfactors));
+    std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(nfactors));
+    const int64_t* bp = blocks;
+    const int64_t* gp = groups;
+    const double* pp = payload;
+    for (int64_t i = 0; i < nfactors; ++i) {
+      auto& F = T.factors[static_cast<size_t>(i)];
+      F.rows = factor_shape[4 * i];
+      F.cols = factor_shape[4 * i + 1];
+      F.nblocks = factor_shape[4 * i + 2];
+      F.ngroups = factor_shape[4 * i + 3];
+      F.blocks = bp;
+      F.groups = gp;
+      for (int64_t b = 0; b < F.nblocks; ++b) {
+        const int64_t m = bp[4 * b + 2], n = bp[4 * b + 3];
+        if (m < 0 || n < 0 || bp[4 * b] < 0 || bp[4 * b + 1] < 0 || bp[4 * b] + m > F.rows ||
+            bp[4 * b + 1] + n > F.cols)
+          throw std::invalid_argument("block outside its factor");
+        ptrs[i].push_back(pp);
+        pp += 2 * m * n;
+        T.total_nnz += m * n;
+        ++T.total_blocks;
+      }
+      for (int64_t g = 0; g < F.ngroups; ++g)
+        if (gp[2 * g] < 0 || gp[2 * g] > gp[2 * g + 1] || gp[2 * g + 1] > F.nblocks)
+          throw std::invalid_argument("group outside block table");
+      F.payload = ptrs[i].data();
+      bp += 4 * F.nblocks;
+      gp += 2 * F.ngroups;
+    }
+    *out = new midbf_plan_s{std::make_unique<Plan>(T, directions)};
+  });
+}
+
+extern "C" int midbf_plan_load(midbf_plan_t* out, const char* path, unsigned directions) {
+  return guard([&] { *out = new midbf_plan_s{midbf::dev::load_plan(path, directions)}; });
+}
+
+extern "C" int midbf_plan_destroy(midbf_plan_t plan) {
+  return guard([&] { delete plan; });
+}
+
+extern "C" int midbf_plan_info(midbf_plan_t plan, int64_t* out) {
+  return guard([&] {
+    const Plan& p = *plan->p;
+    out[0] = p.nrows;
+    out[1] = p.ncols;
+    out[2] = p.nfactors;
+    out[3] = p.total_nnz;
+    int64_t bytes = 0, tasks = 0;
+    unsigned dirs = 0;
+    for (int d = 0; d < 2; ++d)
+      if (p.dir[d].built) {
+        bytes += p.dir[d].arena_elems * 16;
+        tasks += p.dir[d].nstrips;
+        dirs |= 1u << d;
+      }
+    out[4] = bytes;
+    out[5] = tasks;
+    out[6] = dirs;
+    out[7] = p.max_len;
+  });
+}
+
+extern "C" int midbf_apply(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose, void* stream) {
+  return guard([&] {
+    if (!plan || !f || !g) throw std::invalid_argument("null argument");
+    plan->p->apply(f, g, nrhs, transpose != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// Stage table for benchmarks / roofline accounting:
+// out[s*4 + 0..3] = strips, payload bytes, in_len, out_len of stage s.
+extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap) {
+  return guard([&] {
+    const auto& D = plan->p->dir[transpose ? 1 : 0];
+    int64_t s = 0;
+    for (const auto& st : D.stages) {
+      if (s >= cap) break;
+      out[4 * s] = st.nstrips;
+      out[4 * s + 1] = st.payload_bytes;
+      out[4 * s + 2] = st.in_len;
+      out[4 * s + 3] = st.out_len;
+      ++s;
+    }
+  });
+}
+
+// Tuning switches (bench / profiling): bit0 PDL, bit1 L2 bulk prefetch
+// (stage kernels), bit2 CUDA graphs, bit3 persistent dataflow kernel.
+extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
+  return guard([&] { plan->p->flags = flags; });
+}
+
+// Kernel launches of one apply (evidence for bench.py's gpu_launches).
+extern "C" int midbf_plan_launches(midbf_plan_t plan, int transpose, int64_t nrhs, int64_t* out) {
+  return guard([&] { *out = plan->p->launches_per_apply(transpose ? 1 : 0, nrhs); });
+}
