@@ -195,7 +195,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flags", type=int, default=15,
+    ap.add_argument("--flags", type=int, default=31,
                     help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel")
     args = ap.parse_args()
 
@@ -220,8 +220,7 @@ def main():
     t_fac = time.perf_counter() - t0
     entries, sample_calls = F.sample_stats()
     plan = F.plan(1)
-    plan.set_flags(pdl=bool(args.flags & 1), prefetch=bool(args.flags & 2), graph=bool(args.flags & 4),
-                   flow=bool(args.flags & 8))
+    M.lib().midbf_plan_set_flags(plan._h, args.flags)
     N = F.ncols
     stages = plan.stages()
     alg_bytes = 16 * F.total_nnz + 16 * nrhs * (F.ncols + F.nrows)
@@ -245,8 +244,10 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(args.steps):
             step()
+        host_issue_us = (time.perf_counter() - h0) / args.steps * 1e6
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -314,6 +315,7 @@ def main():
                       "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L},
         "stages": [dict(strips=s[0], payload_mb=s[1] / 1e6, in_len=s[2], out_len=s[3]) for s in stages],
         "clocks": clk.summary(),
+        "host_issue_us_per_step": host_issue_us,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         fd_, path = tempfile.mkstemp(suffix=".midbf")

@@ -46,7 +46,9 @@ struct StageIO {
   const int* yperm;
 };
 
+struct StripCtx;
 struct FlowParams {
+  const StripCtx* ctxs;  // per strip: metadata record (strip id in s.seg0)
   const Strip* strips;
   const Seg* segs;
   const double2* arena;
@@ -54,7 +56,11 @@ struct FlowParams {
   unsigned* epoch;   // per CTA: applies completed (all CTAs run every apply)
   int nstrips;
   int nwarps;
-  int nodeps;  // timing experiment only: skip dependency waits (results invalid)
+  // Timing experiments only (results invalid): 1 skip dependency waits,
+  // 2 stream the payload only, 3 compute on resident slots without
+  // streaming, 4 everything but the FMA loop.
+  int nodeps;
+  int pubmode;  // 0 publish after the x prefetch, 1 before it, 2 no fence (timing only)
   StageIO st[kMaxStages];
 };
 
@@ -75,13 +81,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// Blocking wait.  The suspend-time hint lets the hardware park the thread
+// until the phase completes instead of re-polling: with 8 waiting warps per
+// SM, back-to-back polls otherwise contend with the TMA complete_tx updates.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -115,13 +124,15 @@ __device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 
   ai = fma(m.y, x.x, ai);
 }
 
-// Lane-0 dependency check (relaxed loads); the caller fences on success.
-__device__ __forceinline__ bool deps_done(const FlowParams& P, const StripCtx& c, unsigned e) {
+// Warp-wide dependency check: every producer flag of the strip is loaded in
+// parallel (lane-strided per panel, no early exit, so all loads are in flight
+// together) and voted; the caller issues one acquire fence on success.
+__device__ __forceinline__ bool deps_done(const FlowParams& P, const StripCtx& c, unsigned e, int lane) {
   if (P.nodeps) return true;
+  bool ok = true;
   for (int j = 0; j < c.s.nseg; ++j)
-    for (int p = c.g[j].dep0; p < c.g[j].dep1; ++p)
-      if (ld_relaxed(P.flags + p) < e) return false;
-  return true;
+    for (int p = c.g[j].dep0 + lane; p < c.g[j].dep1; p += 32) ok &= ld_relaxed(P.flags + p) >= e;
+  return __all_sync(0xffffffffu, ok);
 }
 
 // Gather a strip's x entries (sum of panel widths <= kXWin) with cp.async.
@@ -209,22 +220,40 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
 
   if (producer) {
     if (lane == 0) {
-      unsigned q = 0;
-      for (int k = 0;; ++k) {
-        const int t = gw + k * P.nwarps;
-        const int sc = k % kQN;
-        mbar_wait(&cempty[sc], ((k / kQN) & 1) ^ 1);
-        StripCtx& C = ctx[sc];
-        if (t >= P.nstrips) {
-          C.s.y0 = -1;  // terminator
-          mbar_arrive(&cfull[sc]);
-          break;
+      // Strips owned by this pair: gw, gw + NW, ...; context k == nmine is
+      // the terminator.  Contexts are prefetched with bulk copies as soon as
+      // their ring entry is released, so reading a strip's metadata never
+      // waits on a plain global load.
+      const int nmine = gw < P.nstrips ? (P.nstrips - 1 - gw) / P.nwarps + 1 : 0;
+      int kf = 0;  // next context to request
+      auto prefetch = [&](bool block) {
+        while (kf <= nmine) {
+          const int sc = kf % kQN;
+          const unsigned par = ((kf / kQN) & 1) ^ 1;
+          if (block) {
+            mbar_wait(&cempty[sc], par);
+            block = false;
+          } else if (!mbar_test(&cempty[sc], par)) {
+            break;
+          }
+          if (kf == nmine) {
+            ctx[sc].s.y0 = -1;
+            mbar_arrive(&cfull[sc]);
+          } else {
+            fence_proxy_async();
+            mbar_expect_tx(&cfull[sc], sizeof(StripCtx));
+            bulk_g2s(&ctx[sc], P.ctxs + gw + static_cast<int64_t>(kf) * P.nwarps, sizeof(StripCtx), &cfull[sc]);
+          }
+          ++kf;
         }
-        C.s = P.strips[t];
+      };
+      unsigned q = 0;
+      for (int k = 0; k < nmine; ++k) {
+        prefetch(kf <= k);
+        const int sc = k % kQN;
+        mbar_wait(&cfull[sc], (k / kQN) & 1);
+        const StripCtx& C = ctx[sc];
         const int nseg = C.s.nseg, h = C.s.h;
-        for (int j = 0; j < nseg; ++j) C.g[j] = P.segs[C.s.seg0 + j];
-        C.s.seg0 = t;  // the context keeps the strip id here
-        mbar_arrive(&cfull[sc]);  // release: metadata visible to the consumer
         const int cpc = chunk_cols_for(h, SLOT);
         for (int j = 0; j < nseg; ++j) {
           const int n = C.g[j].n;
@@ -232,36 +261,63 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
           for (int col = 0; col < n; col += cpc, ++q) {
             const int ncol = min(cpc, n - col);
             const unsigned slot = q % FS;
+            if (P.nodeps == 3 && q >= FS) continue;  // timing experiment: compute on resident data
             mbar_wait(&empty[slot], ((q / FS) & 1) ^ 1);
             fence_proxy_async();
             const unsigned bytes = static_cast<unsigned>(h * ncol * 16);
             mbar_expect_tx(&full[slot], bytes);
             bulk_g2s(slots + size_t(slot) * SLOT, src + static_cast<int64_t>(col) * h, bytes, &full[slot]);
+            prefetch(false);
           }
         }
       }
+      while (kf <= nmine) prefetch(true);
     }
     __syncwarp();
   } else {
     unsigned q = 0;
     int xsel = 0;
     bool have_x = false;
+    int pending = -1;  // finished strip whose flag is not yet published
+    // Release: the strip's row stores (all lanes, ordered by the warp
+    // barrier) before its flag.  Deferred by one strip so the fence finds the
+    // stores already drained instead of waiting for them.
+    auto publish = [&]() {
+      if (pending >= 0) {
+        if (lane == 0) {
+          if (P.pubmode != 2) fence_acq_rel();
+          st_relaxed(P.flags + pending, e);
+        }
+        pending = -1;
+      }
+    };
     for (int k = 0;; ++k) {
       const int sc = k % kQN;
       mbar_wait(&cfull[sc], (k / kQN) & 1);
       const StripCtx& C = ctx[sc];
       if (C.s.y0 < 0) break;
+      if (P.nodeps == 2) {  // timing experiment: stream the payload only
+        const int cpc = chunk_cols_for(C.s.h, SLOT);
+        for (int j = 0; j < C.s.nseg; ++j)
+          for (int col0 = 0; col0 < C.g[j].n; col0 += cpc, ++q) {
+            mbar_wait(&full[q % FS], (q / FS) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q % FS]);
+          }
+        if (lane == 0) mbar_arrive(&cempty[sc]);
+        continue;
+      }
       const int t = C.s.seg0;
-      const int h = C.s.h, nseg = C.s.nseg;
+      const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + xsel * kXWin;
+      if (P.pubmode == 1) publish();
       if (fast && !have_x) {
-        if (lane == 0) {
-          while (!deps_done(P, C, e)) {
-          }
-          fence_acq_rel();
+        publish();  // before any blocking dependency wait (deadlock freedom)
+        while (!deps_done(P, C, e, lane)) {
         }
+        if (lane == 0) fence_acq_rel();
         __syncwarp();
         issue_x(P, C, xcur, lane);
       }
@@ -271,20 +327,15 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
         const int sn = (k + 1) % kQN;
         if (mbar_test(&cfull[sn], ((k + 1) / kQN) & 1)) {
           const StripCtx& Cn = ctx[sn];
-          if (Cn.s.y0 >= 0 && Cn.s.xcols <= kXWin) {
-            int ok = 0;
-            if (lane == 0) {
-              ok = deps_done(P, Cn, e);
-              if (ok) fence_acq_rel();
-            }
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            if (ok) {
-              issue_x(P, Cn, xb + (xsel ^ 1) * kXWin, lane);
-              pref = true;
-            }
+          if (Cn.s.y0 >= 0 && Cn.s.xcols <= kXWin && deps_done(P, Cn, e, lane)) {
+            if (lane == 0) fence_acq_rel();
+            __syncwarp();
+            issue_x(P, Cn, xb + (xsel ^ 1) * kXWin, lane);
+            pref = true;
           }
         }
       }
+      publish();
       if (fast) {
         if (pref)
           cp_async_wait<1>();
@@ -329,9 +380,9 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
             xv = xcur + (col0 - w0 * kXWin);
           }
           const unsigned slot = q % FS;
-          mbar_wait(&full[slot], (q / FS) & 1);
+          if (P.nodeps != 3 || q < FS) mbar_wait(&full[slot], (q / FS) & 1);
           const double2* M = reinterpret_cast<const double2*>(slots + size_t(slot) * SLOT);
-          if (live) {
+          if (live && P.nodeps != 4) {
             int cc = 0;
             for (; cc + 4 <= ncol; cc += 4) {
               const double2 m0 = M[(cc + 0) * h + lane], m1 = M[(cc + 1) * h + lane];
@@ -344,24 +395,23 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
             for (; cc < ncol; ++cc) cmac(ar0, ai0, M[cc * h + lane], xv[cc]);
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);  // slot back to the producer
+          if (lane == 0 && P.nodeps != 3) mbar_arrive(&empty[slot]);  // slot back to the producer
         }
         cb += n;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cempty[sc]);  // context no longer read
       if (live) {
-        int idx = C.s.y0 + lane;
+        int idx = y0 + lane;
         if (io.yperm) idx = io.yperm[idx];
         io.y[idx] = make_double2(ar0 + ar1, ai0 + ai1);
       }
       __syncwarp();
-      if (lane == 0) {
-        fence_acq_rel();  // the warp's row writes before the flag (cumulative via the warp barrier)
-        st_relaxed(P.flags + t, e);
-        mbar_arrive(&cempty[sc]);
-      }
+      pending = t;  // flag published at the next strip, once the stores drained
       if (pref) xsel ^= 1;
       have_x = pref;
     }
+    publish();
     cp_async_wait<0>();
   }
   __syncthreads();

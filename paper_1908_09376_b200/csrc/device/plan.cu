@@ -309,6 +309,10 @@ void Plan::build_direction(int d, const PlanTables& T) {
         for (const auto& pr : active) {
           const EffBlock& e = eb[pr.second];
           Seg sg{};
+          // 128-byte aligned panels: every full TMA chunk (h x 32 columns)
+          // then starts on a cache-line boundary (unaligned bulk copies
+          // stream at a fraction of the rate, tools/bw_probe.cu)
+          arena.resize((arena.size() + 15) & ~size_t(15), 0.0);
           sg.off = static_cast<int64_t>(arena.size() / 2);
           sg.x0 = static_cast<int32_t>(e.xoff);
           sg.n = static_cast<int32_t>(e.n);
@@ -349,6 +353,17 @@ void Plan::build_direction(int d, const PlanTables& T) {
   up(reinterpret_cast<void**>(&D.d_strips), strips.data(), strips.size() * sizeof(Strip), "upload strips");
   up(reinterpret_cast<void**>(&D.d_segs), segs.data(), segs.size() * sizeof(Seg), "upload segs");
   up(reinterpret_cast<void**>(&D.d_arena), arena.data(), arena.size() * sizeof(double), "upload arena");
+  if (D.max_seg <= kMaxSeg) {  // one self-contained metadata record per strip for k1_flow
+    std::vector<StripCtx> ctxs(strips.size());
+    for (size_t t = 0; t < strips.size(); ++t) {
+      StripCtx& c = ctxs[t];
+      std::memset(static_cast<void*>(&c), 0, sizeof(c));
+      c.s = strips[t];
+      c.s.seg0 = static_cast<int32_t>(t);
+      for (int j = 0; j < strips[t].nseg; ++j) c.g[j] = segs[static_cast<size_t>(strips[t].seg0 + j)];
+    }
+    up(reinterpret_cast<void**>(&D.d_ctx), ctxs.data(), ctxs.size() * sizeof(StripCtx), "upload strip records");
+  }
   cuda_check(cudaMalloc(&D.d_stagebuf, D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
   const size_t sync_words = static_cast<size_t>(D.nstrips) + kMaxFlowCtas;
   cuda_check(cudaMalloc(&D.d_sync, sync_words * sizeof(unsigned)), "cudaMalloc sync");
@@ -384,6 +399,7 @@ Plan::~Plan() {
     cudaFree(D.d_strips);
     cudaFree(D.d_segs);
     cudaFree(D.d_arena);
+    cudaFree(D.d_ctx);
     cudaFree(D.d_stagebuf);
     cudaFree(D.d_sync);
   }
@@ -423,13 +439,15 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   Direction& D = dir[d];
   const int variant = static_cast<int>((flags >> 4) & 3u);
   FlowParams P{};
+  P.ctxs = static_cast<const StripCtx*>(D.d_ctx);
   P.strips = D.d_strips;
   P.segs = D.d_segs;
   P.arena = D.d_arena;
   P.flags = D.d_sync;
   P.epoch = D.d_sync + D.nstrips;
   P.nstrips = static_cast<int>(D.nstrips);
-  P.nodeps = (flags & 64u) ? 1 : 0;
+  P.nodeps = static_cast<int>((flags >> 6) & 7u);  // bits 6-8: timing experiments
+  P.pubmode = static_cast<int>((flags >> 9) & 3u);  // bits 9-10: flag publish policy
   const int ns = static_cast<int>(D.stages.size());
   for (int s = 0; s < ns; ++s) {
     StageIO& io = P.st[s];

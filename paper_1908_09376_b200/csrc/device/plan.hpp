@@ -62,6 +62,7 @@ struct Direction {
   Strip* d_strips = nullptr;
   Seg* d_segs = nullptr;
   double2* d_arena = nullptr;
+  void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh)
   double2* d_stagebuf = nullptr;  // outputs of every stage but the last
   unsigned* d_sync = nullptr;     // [strip flags (nstrips) | per-CTA epochs (kMaxFlowCtas)]
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
@@ -95,7 +96,7 @@ class Plan {
   // bit0 PDL + bit1 L2 prefetch (stage kernels), bit2 CUDA graphs,
   // bit3 persistent dataflow kernel for single-RHS applies,
   // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size).
-  unsigned flags = 0xF;
+  unsigned flags = 0x1F;  // default: k1_flow variant 1 (8 pairs x 2 x 8 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
   int64_t launches_per_apply(int d, int64_t nrhs) const;
