@@ -32,6 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_SM = 148
+# FP64 tensor (DMMA m8n8k4) peak measured on this pool's B200 by tools/fp64_probe.cu
+# (MEASURED_PEAKS.json records HBM and bf16 only); DFMA measured 36.7.
+FP64_DMMA_TFLOPS = 36.8
 
 
 def peaks():
@@ -287,6 +290,20 @@ def main():
 
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
+    launches = plan.launches(nrhs)
+    if nrhs == 1:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes_per_apply": alg_bytes,
+                    "note": "achieved = (16*total_nnz + 16*(N_in+N_out)) / apply time; one apply = "
+                            f"{launches} k1_flow launch in one CUDA graph"}
+    else:
+        flops = 8.0 * F.total_nnz * nrhs
+        tf = flops / (ms_step * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                    "frac": tf / FP64_DMMA_TFLOPS, "peak_kind": "measured (tools/fp64_probe.cu, DMMA m8n8k4)",
+                    "traffic": None, "algorithmic_flops_per_apply": flops, "hbm_gbs": achieved,
+                    "hbm_frac": achieved / hbm,
+                    "note": f"FP64 tensor-core (DMMA) K2 path, {launches} stage launches per apply in one graph"}
     line = {
         "metric": "MIDBF matvecs/s at 2D N=256^2 (HBM roofline fraction); rel-L2 err vs ref",
         "value": world * nrhs / (ms_step * 1e-3),
@@ -303,14 +320,10 @@ def main():
         "config": dict(workload=args.config, nrhs=nrhs, parallelism=f"replicas x{world}",
                        l2="factor payload %.1f MB > 126 MB L2 (no flush needed; vectors L2-resident)"
                           % (16 * F.total_nnz / 1e6), **desc),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_kind": peak_kind, "traffic": None,
-                     "algorithmic_bytes_per_apply": alg_bytes,
-                      "note": "achieved = (16*total_nnz + 16*nrhs*(N_in+N_out)) / apply time; one apply = "
-                             f"{plan.launches(nrhs)} kernel launch(es) in one CUDA graph"},
+        "roofline": roofline,
         "e2e": {"value": world * nrhs / e_s, "unit": "matvecs/s", "h2d_bytes_per_step": 16 * N * nrhs,
                 "d2h_bytes_per_step": 16 * F.nrows * nrhs},
-        "gpu_launches": plan.launches(nrhs) * args.steps,
+        "gpu_launches": launches * args.steps,
         "factorize": {"seconds": t_fac, "entries_sampled_on_gpu": entries, "sampler_launch_batches": sample_calls,
                       "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L},
         "stages": [dict(strips=s[0], payload_mb=s[1] / 1e6, in_len=s[2], out_len=s[3]) for s in stages],

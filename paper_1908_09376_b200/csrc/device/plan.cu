@@ -43,6 +43,7 @@
 #include "common.cuh"
 #include "plan.hpp"
 #include "flow.cuh"
+#include "k2.cuh"
 
 namespace midbf::dev {
 
@@ -392,6 +393,8 @@ Plan::Plan(const PlanTables& T, unsigned directions) {
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
   flow_grid[2] = flow_setup<6, 4, 8192>(num_sms);
   flow_grid[3] = flow_grid[0];
+  cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
+             "k2 smem attribute");
 }
 
 Plan::~Plan() {
@@ -418,6 +421,11 @@ bool Plan::flow_ok(int d, int64_t nrhs) const {
 
 int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
   if (flow_ok(d, nrhs)) return 1;
+  if (k2_ok(nrhs)) {
+    int64_t n = 0;
+    for (const auto& st : dir[d].stages) n += st.nstrips > 0;
+    return n;
+  }
   return static_cast<int64_t>(dir[d].stages.size());
 }
 
@@ -505,9 +513,43 @@ void Plan::launch_stages(int d, const double2* in, double2* out, int64_t nrhs, c
   }
 }
 
+// K2: one DMMA launch per stage, chained with programmatic dependent launch.
+void Plan::launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
+  const Direction& D = dir[d];
+  const int ns = static_cast<int>(D.stages.size());
+  const int* in_perm = d == 0 ? d_col_perm : d_row_perm;
+  const int* out_perm = d == 0 ? d_row_perm : d_col_perm;
+  for (int s = 0; s < ns; ++s) {
+    const Stage& st = D.stages[s];
+    if (st.nstrips == 0) continue;
+    const double2* x = s == 0 ? in : d_buf[(s - 1) & 1];
+    double2* y = s == ns - 1 ? out : d_buf[s & 1];
+    const int64_t xld = s == 0 ? (d == 0 ? ncols : nrows) : max_len;
+    const int64_t yld = s == ns - 1 ? (d == 0 ? nrows : ncols) : max_len;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(st.nstrips), static_cast<unsigned>((nrhs + kK2Rhs - 1) / kK2Rhs), 1);
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.dynamicSmemBytes = kK2Smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, k2_stage, (const Strip*)(D.d_strips + st.strip0), (const Seg*)D.d_segs,
+                                  (const double2*)D.d_arena, x, xld, s == 0 ? in_perm : nullptr, y, yld,
+                                  s == ns - 1 ? out_perm : nullptr, static_cast<int>(nrhs)),
+               "k2_stage launch");
+  }
+}
+
+bool Plan::k2_ok(int64_t nrhs) const { return nrhs > 1 && !(flags & 2048u); }
+
 void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   if (flow_ok(d, nrhs))
     launch_flow(d, in, out, stream);
+  else if (k2_ok(nrhs))
+    launch_k2(d, in, out, nrhs, stream);
   else
     launch_stages(d, in, out, nrhs, stream);
 }

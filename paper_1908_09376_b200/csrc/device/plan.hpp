@@ -95,12 +95,14 @@ class Plan {
   Direction dir[2];
   // bit0 PDL + bit1 L2 prefetch (stage kernels), bit2 CUDA graphs,
   // bit3 persistent dataflow kernel for single-RHS applies,
-  // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size).
+  // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size),
+  // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS).
   unsigned flags = 0x1F;  // default: k1_flow variant 1 (8 pairs x 2 x 8 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
+  bool k2_ok(int64_t nrhs) const;
   int last_nwarps[2] = {0, 0};
 
  private:
@@ -109,6 +111,7 @@ class Plan {
   void launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_flow(int d, const double2* in, double2* out, cudaStream_t stream);
+  void launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   int* d_row_perm = nullptr;
   int* d_col_perm = nullptr;
   double2* d_buf[2] = {nullptr, nullptr};

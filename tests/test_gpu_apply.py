@@ -52,6 +52,16 @@ def test_multi_rhs_matches_oracle_and_columns(pair):
         assert np.abs(G[:, c] - plan.apply(F3[:, c])).max() <= 1e-12 * max(1.0, np.abs(G).max())
 
 
+@pytest.mark.parametrize("nrhs", [64, 70])
+def test_dmma_multi_rhs_matches_oracle(pair, nrhs):
+    """K2 (FP64 tensor cores) over full and ragged 64-RHS tiles, both directions."""
+    name, K, Fo, Fm, plan = pair
+    X = cvec(Fo.ncols, 16, cols=nrhs)
+    assert rel(plan.apply(X), Fo.apply(X)) <= TOL
+    Y = cvec(Fo.nrows, 17, cols=nrhs)
+    assert rel(plan.apply(Y, transpose=True), Fo.apply_transpose(Y)) <= TOL
+
+
 def test_runs_are_bitwise_identical(pair):
     name, K, Fo, Fm, plan = pair
     f = cvec(Fo.ncols, 14)
