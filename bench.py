@@ -240,7 +240,7 @@ def main():
     t0 = time.perf_counter()
     F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="device")
     t_fac = time.perf_counter() - t0
-    entries, sample_calls = F.sample_stats()
+    entries, sample_calls, sample_s = F.sample_stats()
     plan = F.plan(1)
     M.lib().midbf_plan_set_flags(plan._h, args.flags)
     N = F.ncols
@@ -336,6 +336,7 @@ def main():
                 "d2h_bytes_per_step": 16 * F.nrows * nrhs},
         "gpu_launches": launches * args.steps,
         "factorize": {"seconds": t_fac, "entries_sampled_on_gpu": entries, "sampler_launch_batches": sample_calls,
+                      "sampler_seconds": sample_s, "sampled_entries_per_s": entries / max(sample_s, 1e-9),
                       "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L},
         "stages": [dict(strips=s[0], payload_mb=s[1] / 1e6, in_len=s[2], out_len=s[3]) for s in stages],
         "clocks": clk.summary(),

@@ -138,7 +138,8 @@ int midbf_fact_plan(midbf_fact_t fact, unsigned directions, midbf_plan_t* out);
 /* bf::apply on the factorization's cached device plan (host or device operands). */
 int midbf_fact_apply(midbf_fact_t fact, const double* f, double* g, int64_t nrhs, int transpose, void* stream);
 
-/* Statistics of a device-sampled factorize: out[0] entries, out[1] sampler calls. */
+/* Statistics of a device-sampled factorize: out[0] entries, out[1] sampler calls,
+ * out[2] nanoseconds spent in the device sampler (kernel + copies). */
 int midbf_fact_stats(midbf_fact_t fact, int64_t* out);
 
 /* Plan introspection / tuning (benchmarks, profiling):

@@ -307,9 +307,10 @@ class Factorization:
         return c * self.k_max * self.k_max / max(self.n0, 1) * max(self.nrows, self.ncols)
 
     def sample_stats(self):
-        o = np.zeros(2, dtype=np.int64)
+        """(entries sampled on the GPU, sampler calls, seconds in the sampler)."""
+        o = np.zeros(3, dtype=np.int64)
         _check(lib().midbf_fact_stats(self._h, _ip(o)))
-        return int(o[0]), int(o[1])
+        return int(o[0]), int(o[1]), o[2] * 1e-9
 
     def perms(self):
         rp = np.empty(self.nrows, dtype=np.int64)

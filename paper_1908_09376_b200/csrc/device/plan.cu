@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -49,7 +50,6 @@ namespace midbf::dev {
 
 namespace {
 
-constexpr int kStripRows = 32;
 
 // ---------------------------------------------------------------- helpers
 __device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 x) {
@@ -300,8 +300,8 @@ void Plan::build_direction(int d, const PlanTables& T) {
         else
           ++it;
       }
-      for (int64_t y = a; y < b; y += kStripRows) {
-        const int h = static_cast<int>(std::min<int64_t>(kStripRows, b - y));
+      for (int64_t y = a; y < b; y += strip_rows) {
+        const int h = static_cast<int>(std::min<int64_t>(strip_rows, b - y));
         Strip st{};
         st.y0 = static_cast<int32_t>(y);
         st.h = h;
@@ -374,6 +374,10 @@ void Plan::build_direction(int d, const PlanTables& T) {
 
 Plan::Plan(const PlanTables& T, unsigned directions) {
   device = require_device();
+  if (const char* e = std::getenv("MIDBF_STRIP_ROWS")) {  // experiments: strip height 1..32
+    const int v = std::atoi(e);
+    if (v >= 1 && v <= 32) strip_rows = v;
+  }
   cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
   nrows = T.nrows;
   ncols = T.ncols;

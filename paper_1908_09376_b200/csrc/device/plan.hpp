@@ -100,6 +100,7 @@ class Plan {
   unsigned flags = 0x1F;  // default: k1_flow variant 1 (8 pairs x 2 x 8 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
+  int strip_rows = 32;  // output rows per strip (one warp's lanes)
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
   bool k2_ok(int64_t nrhs) const;

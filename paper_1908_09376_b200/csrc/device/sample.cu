@@ -93,16 +93,17 @@ __device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
   }
 }
 
-// tasks: ntasks x 5 (row_off, nr, col_off, nc, out_off), out_off relative
-// to this chunk's output base.  One CTA per task, threads stride entries.
-__global__ void __launch_bounds__(256) k3_sample(DevK k, const int64_t* __restrict__ tasks,
+// tasks: ntasks x 5 (row_off, nr, col_off, nc, out_off) as int32, out_off
+// relative to this chunk's output base.  One CTA per task, threads stride
+// the task's entries in output (column-major) order: coalesced stores.
+__global__ void __launch_bounds__(256) k3_sample(DevK k, const int* __restrict__ tasks,
                                                  const int* __restrict__ rid, const int* __restrict__ cid,
                                                  double2* __restrict__ out) {
-  const int64_t* tk = tasks + 5 * blockIdx.x;
-  const int64_t ro = tk[0], nr = tk[1], co = tk[2], nc = tk[3], oo = tk[4];
-  const int64_t total = nr * nc;
-  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-    const int64_t c = e / nr, r = e - c * nr;
+  const int* tk = tasks + 5 * blockIdx.x;
+  const int ro = tk[0], nr = tk[1], co = tk[2], nc = tk[3], oo = tk[4];
+  const int total = nr * nc;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int c = e / nr, r = e - c * nr;
     out[oo + e] = entry(k, rid[ro + r], cid[co + c]);
   }
 }
@@ -168,6 +169,29 @@ struct EntrySampler::Impl {
   std::vector<void*> owned;
   int64_t nrows = 0, ncols = 0;
   int64_t launched_entries = 0;
+  // double-buffered device output / pinned staging, allocated on first use
+  static constexpr int64_t kChunk = int64_t{4} << 20;  // complex entries per chunk (64 MB)
+  double2* d_out[2] = {nullptr, nullptr};
+  double2* h_pin[2] = {nullptr, nullptr};
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  void ensure_buffers() {
+    if (d_out[0]) return;
+    for (int b = 0; b < 2; ++b) {
+      cuda_check(cudaMalloc(&d_out[b], kChunk * sizeof(double2)), "cudaMalloc sample buffer");
+      cuda_check(cudaMallocHost(&h_pin[b], kChunk * sizeof(double2)), "cudaMallocHost sample buffer");
+      cuda_check(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
+    }
+    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  }
+  ~Impl() {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(d_out[b]);
+      cudaFreeHost(h_pin[b]);
+      if (done[b]) cudaEventDestroy(done[b]);
+    }
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
 
 EntrySampler::EntrySampler(const midbf_kernel_desc& kd) : impl_(new Impl) {
@@ -241,9 +265,24 @@ int64_t EntrySampler::entries_evaluated() const { return impl_->launched_entries
 
 void EntrySampler::sample(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
                           const int64_t* col_ids, int64_t n_col_ids, double* out, int64_t out_len) {
+  std::vector<double*> outs(static_cast<size_t>(ntasks));
+  for (int64_t t = 0; t < ntasks; ++t) {
+    const int64_t* tk = tasks + 5 * t;
+    if (tk[4] < 0 || tk[1] < 0 || tk[3] < 0 || tk[4] + tk[1] * tk[3] > out_len)
+      throw std::invalid_argument("sample task outside its output");
+    outs[static_cast<size_t>(t)] = out + 2 * tk[4];
+  }
+  sample_blocks(ntasks, tasks, row_ids, n_row_ids, col_ids, n_col_ids, outs.data());
+}
+
+// Pipeline: chunk i's kernel and D2H copy run on the sampler's stream while
+// the host scatters chunk i-1 from pinned memory into the destination blocks
+// (OpenMP over tasks).
+void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+                                 const int64_t* col_ids, int64_t n_col_ids, double* const* outs) {
   Impl& I = *impl_;
-  if (ntasks == 0) return;
-  // validate and convert ids
+  if (ntasks <= 0) return;
+  if (n_row_ids > 0x7fffffff || n_col_ids > 0x7fffffff) throw std::invalid_argument("too many sample ids");
   std::vector<int> rid(static_cast<size_t>(n_row_ids)), cid(static_cast<size_t>(n_col_ids));
   for (int64_t q = 0; q < n_row_ids; ++q) {
     if (row_ids[q] < 0 || row_ids[q] >= I.nrows) throw std::invalid_argument("row id out of range");
@@ -253,69 +292,92 @@ void EntrySampler::sample(int64_t ntasks, const int64_t* tasks, const int64_t* r
     if (col_ids[q] < 0 || col_ids[q] >= I.ncols) throw std::invalid_argument("column id out of range");
     cid[q] = static_cast<int>(col_ids[q]);
   }
+  // Sub-tasks: a block larger than one chunk is split into column ranges;
+  // chunks = consecutive sub-tasks with <= kChunk entries.
+  struct Sub {
+    int ro, nr, co, nc;
+    double* dst;
+  };
+  std::vector<Sub> subs;
+  subs.reserve(static_cast<size_t>(ntasks));
   for (int64_t t = 0; t < ntasks; ++t) {
     const int64_t* tk = tasks + 5 * t;
-    if (tk[1] < 0 || tk[3] < 0 || tk[0] < 0 || tk[2] < 0 || tk[0] + tk[1] > n_row_ids ||
-        tk[2] + tk[3] > n_col_ids || tk[4] < 0 || tk[4] + tk[1] * tk[3] > out_len)
-      throw std::invalid_argument("sample task outside its id lists or output");
+    if (tk[1] < 0 || tk[3] < 0 || tk[0] < 0 || tk[2] < 0 || tk[0] + tk[1] > n_row_ids || tk[2] + tk[3] > n_col_ids)
+      throw std::invalid_argument("sample task outside its id lists");
+    if (tk[1] == 0 || tk[3] == 0) continue;
+    const int64_t cols_per = std::max<int64_t>(1, Impl::kChunk / tk[1]);
+    if (tk[1] > Impl::kChunk) throw std::invalid_argument("sample block taller than the sampler chunk");
+    for (int64_t c0 = 0; c0 < tk[3]; c0 += cols_per)
+      subs.push_back({static_cast<int>(tk[0]), static_cast<int>(tk[1]), static_cast<int>(tk[2] + c0),
+                      static_cast<int>(std::min<int64_t>(cols_per, tk[3] - c0)), outs[t] + 2 * c0 * tk[1]});
   }
+  const int64_t nsub = static_cast<int64_t>(subs.size());
+  if (nsub == 0) return;
+  std::vector<int> dt(static_cast<size_t>(5 * nsub));
+  std::vector<int64_t> chunk_begin{0}, chunk_entries;
+  int64_t acc = 0;
+  for (int64_t t = 0; t < nsub; ++t) {
+    const Sub& u = subs[static_cast<size_t>(t)];
+    const int64_t n = static_cast<int64_t>(u.nr) * u.nc;
+    if (acc + n > Impl::kChunk) {
+      chunk_entries.push_back(acc);
+      chunk_begin.push_back(t);
+      acc = 0;
+    }
+    int* d = &dt[static_cast<size_t>(5 * t)];
+    d[0] = u.ro;
+    d[1] = u.nr;
+    d[2] = u.co;
+    d[3] = u.nc;
+    d[4] = static_cast<int>(acc);
+    acc += n;
+  }
+  chunk_entries.push_back(acc);
+  chunk_begin.push_back(nsub);
+  I.ensure_buffers();
   int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
   int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
-  // chunk the tasks so one device output buffer stays <= 256 MB
-  const int64_t kChunk = int64_t{16} << 20;  // complex entries
-  double2* d_out = nullptr;
-  double2* h_pin = nullptr;
-  int64_t cap = 0;
-  std::vector<int64_t> ctask;
-  int64_t t0 = 0;
-  try {
-    while (t0 < ntasks) {
-      int64_t t1 = t0, total = 0;
-      while (t1 < ntasks && (t1 == t0 || total + tasks[5 * t1 + 1] * tasks[5 * t1 + 3] <= kChunk)) {
-        total += tasks[5 * t1 + 1] * tasks[5 * t1 + 3];
-        ++t1;
-      }
-      if (total > cap) {
-        cudaFree(d_out);
-        cudaFreeHost(h_pin);
-        d_out = nullptr;
-        h_pin = nullptr;
-        cap = total;
-        cuda_check(cudaMalloc(&d_out, std::max<int64_t>(1, cap) * sizeof(double2)), "cudaMalloc sample out");
-        cuda_check(cudaMallocHost(&h_pin, std::max<int64_t>(1, cap) * sizeof(double2)), "cudaMallocHost");
-      }
-      ctask.assign(static_cast<size_t>(5 * (t1 - t0)), 0);
-      int64_t off = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        for (int q = 0; q < 4; ++q) ctask[5 * (t - t0) + q] = tasks[5 * t + q];
-        ctask[5 * (t - t0) + 4] = off;
-        off += tasks[5 * t + 1] * tasks[5 * t + 3];
-      }
-      int64_t* d_tasks = upload(ctask.data(), ctask.size(), "upload tasks");
-      if (total > 0) {
-        k3_sample<<<static_cast<unsigned>(t1 - t0), 256>>>(I.k, d_tasks, d_rid, d_cid, d_out);
-        cuda_check(cudaGetLastError(), "k3_sample launch");
-        cuda_check(cudaMemcpy(h_pin, d_out, total * sizeof(double2), cudaMemcpyDeviceToHost), "sample D2H");
-      }
-      cudaFree(d_tasks);
-      for (int64_t t = t0; t < t1; ++t) {
-        const int64_t n = tasks[5 * t + 1] * tasks[5 * t + 3];
-        std::memcpy(out + 2 * tasks[5 * t + 4], h_pin + ctask[5 * (t - t0) + 4], static_cast<size_t>(16 * n));
-      }
-      I.launched_entries += total;
-      t0 = t1;
+  int* d_tasks = upload(dt.data(), dt.size(), "upload tasks");
+  const int64_t nchunks = static_cast<int64_t>(chunk_entries.size());
+  auto scatter = [&](int64_t c) {
+    const int b = static_cast<int>(c & 1);
+    cuda_check(cudaEventSynchronize(I.done[b]), "sample chunk");
+    const double2* src = I.h_pin[b];
+    const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t t = t0; t < t1; ++t) {
+      const Sub& u = subs[static_cast<size_t>(t)];
+      std::memcpy(u.dst, src + dt[static_cast<size_t>(5 * t + 4)], static_cast<size_t>(16) * u.nr * u.nc);
     }
+  };
+  try {
+    for (int64_t c = 0; c < nchunks; ++c) {
+      const int b = static_cast<int>(c & 1);
+      if (c >= 2) cuda_check(cudaEventSynchronize(I.done[b]), "sample buffer reuse");
+      const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
+      if (chunk_entries[static_cast<size_t>(c)] > 0) {
+        k3_sample<<<static_cast<unsigned>(t1 - t0), 256, 0, I.stream>>>(I.k, d_tasks + 5 * t0, d_rid, d_cid,
+                                                                         I.d_out[b]);
+        cuda_check(cudaGetLastError(), "k3_sample launch");
+        cuda_check(cudaMemcpyAsync(I.h_pin[b], I.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, I.stream),
+                   "sample D2H");
+      }
+      cuda_check(cudaEventRecord(I.done[b], I.stream), "event record");
+      if (c >= 1) scatter(c - 1);
+      I.launched_entries += chunk_entries[static_cast<size_t>(c)];
+    }
+    scatter(nchunks - 1);
   } catch (...) {
-    cudaFree(d_out);
-    cudaFreeHost(h_pin);
+    cudaStreamSynchronize(I.stream);
     cudaFree(d_rid);
     cudaFree(d_cid);
+    cudaFree(d_tasks);
     throw;
   }
-  cudaFree(d_out);
-  cudaFreeHost(h_pin);
   cudaFree(d_rid);
   cudaFree(d_cid);
+  cudaFree(d_tasks);
 }
 
 void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g) {

@@ -22,6 +22,9 @@ class EntrySampler {
   // tasks: ntasks x 5 (row_off, nr, col_off, nc, out_off); host in/out.
   void sample(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
               const int64_t* col_ids, int64_t n_col_ids, double* out, int64_t out_len);
+  // Same, each task's block written to its own destination outs[t].
+  void sample_blocks(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+                     const int64_t* col_ids, int64_t n_col_ids, double* const* outs);
   void direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g);
   int64_t entries_evaluated() const;
 

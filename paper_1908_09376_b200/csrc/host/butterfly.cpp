@@ -13,6 +13,7 @@
 // grouping are the reference's, so a host-filled factorization is identical to
 // the reference algorithm's.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -431,31 +432,30 @@ Filler device_filler(dev::EntrySampler& smp, FactorizeStats* stats) {
   return [&smp, stats](std::vector<FillJob>& jobs) {
     if (jobs.empty()) return;
     std::vector<std::int64_t> tasks(5 * jobs.size());
+    std::vector<double*> outs(jobs.size());
     IndexVec rid, cid;
     Index total = 0;
     for (size_t q = 0; q < jobs.size(); ++q) {
-      const FillJob& j = jobs[q];
+      FillJob& j = jobs[q];
       tasks[5 * q] = static_cast<std::int64_t>(rid.size());
       tasks[5 * q + 1] = j.nr;
       tasks[5 * q + 2] = static_cast<std::int64_t>(cid.size());
       tasks[5 * q + 3] = j.nc;
-      tasks[5 * q + 4] = total;
+      tasks[5 * q + 4] = 0;
       rid.insert(rid.end(), j.rows, j.rows + j.nr);
       cid.insert(cid.end(), j.cols, j.cols + j.nc);
+      j.out->resize(j.nr, j.nc);
+      outs[q] = reinterpret_cast<double*>(j.out->data());
       total += j.nr * j.nc;
     }
-    std::vector<double> buf(static_cast<size_t>(2 * total));
-    smp.sample(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(), static_cast<std::int64_t>(rid.size()),
-               cid.data(), static_cast<std::int64_t>(cid.size()), buf.data(), total);
-    for (size_t q = 0; q < jobs.size(); ++q) {
-      FillJob& j = jobs[q];
-      j.out->resize(j.nr, j.nc);
-      std::memcpy(static_cast<void*>(j.out->data()), buf.data() + 2 * tasks[5 * q + 4],
-                  static_cast<size_t>(16 * j.nr * j.nc));
-    }
+    const auto t0 = std::chrono::steady_clock::now();
+    smp.sample_blocks(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(),
+                      static_cast<std::int64_t>(rid.size()), cid.data(), static_cast<std::int64_t>(cid.size()),
+                      outs.data());
     if (stats) {
       stats->entries += total;
       stats->launches += 1;
+      stats->sample_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   };
 }

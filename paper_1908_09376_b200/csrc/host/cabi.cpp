@@ -156,6 +156,7 @@ int midbf_fact_stats(midbf_fact_t fact, int64_t* o) {
   return guard([&] {
     o[0] = fact->stats.entries;
     o[1] = fact->stats.launches;
+    o[2] = static_cast<int64_t>(fact->stats.sample_seconds * 1e9);  // ns
   });
 }
 

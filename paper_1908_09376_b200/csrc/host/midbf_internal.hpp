@@ -11,6 +11,7 @@ namespace midbf::bf {
 struct FactorizeStats {
   std::int64_t entries = 0;   // kernel entries sampled on the device
   std::int64_t launches = 0;  // sampler calls (one per sweep pass)
+  double sample_seconds = 0;  // wall time inside the device sampler (kernel + copies)
 };
 
 Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,

@@ -62,7 +62,7 @@ def test_device_sampled_factorization_accuracy(gpu, n):
     assert F.nfactors == 2 * (F.L - F.h + 1) + 1
     assert F.nfactors == {16: 3, 32: 5}[n]
     assert F.max_factor_nnz <= F.nnz_bound(4.0)
-    entries, calls = F.sample_stats()
+    entries, calls, _ = F.sample_stats()
     assert entries > 0 and calls >= 3
     f = cvec(n * n, 41 + n)
     gd = Km.direct_sum(f)
@@ -85,3 +85,19 @@ def test_device_and_host_sampling_agree_on_integer_xi(gpu):
     gd = Km.direct_sum(f)
     ed, eh = rel(Fd.apply(f), gd), rel(Fh.apply(f), gd)
     assert abs(ed - eh) <= 0.05 * eh
+
+
+def test_sampler_splits_blocks_larger_than_a_chunk(gpu):
+    """A 64 x 66000 block exceeds the sampler's 4M-entry chunk and is split
+    into column ranges; every entry must still land in place."""
+    rng = np.random.default_rng(8)
+    A, B = rng.standard_normal((128, 4)), rng.standard_normal((70000, 4))
+    Ko, Km = O.Kernel(O.KIND_LOWRANK, A=A, B=B), M.Kernel(M.KIND_LOWRANK, A=A, B=B)
+    rows = rng.choice(128, 64, replace=False)
+    cols = rng.choice(70000, 66000, replace=False)
+    small_r, small_c = rng.choice(128, 5, replace=False), rng.choice(70000, 7, replace=False)
+    big, small = Km.sample([rows, small_r], [cols, small_c])
+    for r, c, Bk in ((rows, cols, big), (small_r, small_c, small)):
+        rr, cc = np.meshgrid(r, c, indexing="ij")
+        ref = Ko.entries(rr.ravel(), cc.ravel()).reshape(len(r), len(c))
+        assert np.abs(Bk - ref).max() <= 4e-15
