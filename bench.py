@@ -217,7 +217,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--flags", type=int, default=31,
+    ap.add_argument("--flags", type=int, default=15,
                     help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel")
     args = ap.parse_args()
 

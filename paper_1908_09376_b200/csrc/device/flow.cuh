@@ -16,12 +16,13 @@
 //     derived arithmetically from the strip's cached metadata;
 //   consumer (32 lanes, lane = output row): waits on the slot's mbarrier,
 //     multiplies the panel columns with the staged x entries (fp64 FMA), and
-//     after the last panel writes its row and publishes the strip's flag.
-// Dependencies: a strip reads x[x0, x0+n) of each panel; the previous
-// stage's strips producing that range are [dep0, dep1).  Lane 0 polls their
-// flags (relaxed loads of the apply epoch) and issues one acquire fence; x
-// is then gathered asynchronously with cp.async into a double-buffered
-// window, one strip ahead when the next strip's producers are already done.
+//     after the last panel writes its row (the row value is the ready signal).
+// Dependencies: a strip reads x[x0, x0+n) of each panel from the previous
+// stage's output buffer, which is armed with a sentinel bit pattern before the
+// apply; the consumer polls exactly the entries it needs until none is a
+// sentinel (the data is its own ready signal: no flags, no fences).  The next
+// strip's entries are loaded into registers before the current strip is
+// computed and validated after it, so x usually arrives for free.
 // Strip metadata (strip + up to kMaxSeg panels) is loaded once per claim into
 // a per-warp shared-memory context ring, so the hot loop issues no
 // dependent global loads besides x.
@@ -40,10 +41,11 @@ constexpr int kQN = 4;      // claimed-strip context ring per warp
 constexpr int kXWin = 128;  // staged x entries per buffer (two per warp)
 
 struct StageIO {
-  const double2* x;
+  const double2* x;  // parity-0 address for stage buffers
   double2* y;
   const int* xperm;
   const int* yperm;
+  int x_par, y_par;  // 1: stage buffer, add FlowParams::par_elems on odd applies
 };
 
 struct StripCtx;
@@ -52,15 +54,16 @@ struct FlowParams {
   const Strip* strips;
   const Seg* segs;
   const double2* arena;
-  unsigned* flags;   // per strip: epoch of its last completion
   unsigned* epoch;   // per CTA: applies completed (all CTAs run every apply)
+  double2* stagebuf;  // both parity sets of intermediate stage buffers
+  int64_t par_elems;  // complex entries per parity set
   int nstrips;
   int nwarps;
-  // Timing experiments only (results invalid): 1 skip dependency waits,
-  // 2 stream the payload only, 3 compute on resident slots without
-  // streaming, 4 everything but the FMA loop.
+  // Timing experiments only (results invalid): 2 stream the payload only,
+  // 3 compute on resident slots without streaming, 4 everything but the
+  // FMA loop.
   int nodeps;
-  int pubmode;  // 0 publish after the x prefetch, 1 before it, 2 no fence (timing only)
+  long long* prof;  // phase timers of the PROF instantiation
   StageIO st[kMaxStages];
 };
 
@@ -100,23 +103,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 x) {
   ar = fma(m.x, x.x, ar);
   ar = fma(-m.y, x.y, ar);
@@ -124,31 +110,94 @@ __device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 
   ai = fma(m.y, x.x, ai);
 }
 
-// Warp-wide dependency check: every producer flag of the strip is loaded in
-// parallel (lane-strided per panel, no early exit, so all loads are in flight
-// together) and voted; the caller issues one acquire fence on success.
-__device__ __forceinline__ bool deps_done(const FlowParams& P, const StripCtx& c, unsigned e, int lane) {
-  if (P.nodeps) return true;
-  bool ok = true;
-  for (int j = 0; j < c.s.nseg; ++j)
-    for (int p = c.g[j].dep0 + lane; p < c.g[j].dep1; p += 32) ok &= ld_relaxed(P.flags + p) >= e;
-  return __all_sync(0xffffffffu, ok);
+// ---- data-as-signal dependencies -------------------------------------------
+// Intermediate stage buffers are armed with an all-ones bit pattern before an
+// apply uses them; a consumer polls the entries it reads (L2, .cg) until none
+// carries the sentinel.  An entry is written exactly once per apply by the
+// warp owning its strip, and 8-byte aligned stores are single-copy atomic,
+// so "re and im both differ from the sentinel" means the final value is
+// visible: no flags, no fences on the critical path.
+constexpr int kXPerLane = kXWin / 32;
+__device__ __forceinline__ bool is_sentinel(const double2& v) {
+  return __double_as_longlong(v.x) == -1ll || __double_as_longlong(v.y) == -1ll;
 }
-
-// Gather a strip's x entries (sum of panel widths <= kXWin) with cp.async.
-__device__ __forceinline__ void issue_x(const FlowParams& P, const StripCtx& c, double2* dst, int lane) {
-  const StageIO io = P.st[c.s.stage];
+__device__ __forceinline__ double unsentinel(double v) {
+  return __double_as_longlong(v) == -1ll ? __longlong_as_double(0x7ff8000000000000ll) : v;
+}
+__device__ __forceinline__ double2 ld_cg(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+// input index of the strip's flattened staged column kk
+__device__ __forceinline__ int x_index(const StripCtx& c, int kk) {
+  int j = 0;
+  while (kk >= c.g[j].n) kk -= c.g[j++].n;
+  return c.g[j].x0 + kk;
+}
+// Gather cnt entries from x0 (stage 0 through xperm, never polled: user f),
+// polling intermediate buffers until every loaded entry is valid.
+__device__ __forceinline__ void gather_range(const double2* x, const int* xperm, int x0, int cnt, double2* dst,
+                                             int lane) {
+  for (int base = 0; base < cnt; base += 32 * 4) {
+    double2 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = base + lane + 32 * i;
+      if (kk < cnt) v[i] = xperm ? __ldg(x + __ldg(xperm + x0 + kk)) : ld_cg(x + x0 + kk);
+    }
+    if (!xperm) {
+      bool ok;
+      do {
+        ok = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int kk = base + lane + 32 * i;
+          if (kk < cnt && is_sentinel(v[i])) {
+            v[i] = ld_cg(x + x0 + kk);
+            ok = false;
+          }
+        }
+      } while (!ok);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = base + lane + 32 * i;
+      if (kk < cnt) dst[kk] = v[i];
+    }
+  }
+}
+__device__ __forceinline__ void gather_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst,
+                                         int lane) {
   int cb = 0;
   for (int j = 0; j < c.s.nseg; ++j) {
-    const int n = c.g[j].n, x0 = c.g[j].x0;
-    for (int k = lane; k < n; k += 32) {
-      int idx = x0 + k;
-      if (io.xperm) idx = __ldg(io.xperm + idx);
-      cp_async16(dst + cb + k, io.x + idx);
-    }
-    cb += n;
+    gather_range(x, xperm, c.g[j].x0, c.g[j].n, dst + cb, lane);
+    cb += c.g[j].n;
   }
-  cp_async_commit();
+  __syncwarp();
+}
+__device__ __forceinline__ void load_x_regs(const StripCtx& c, const double2* x, const int* xperm, double2* v,
+                                            int lane) {
+#pragma unroll
+  for (int i = 0; i < kXPerLane; ++i) {
+    const int kk = lane + 32 * i;
+    if (kk < c.s.xcols) {
+      const int idx = x_index(c, kk);
+      v[i] = xperm ? __ldg(x + __ldg(xperm + idx)) : ld_cg(x + idx);
+    }
+  }
+}
+__device__ __forceinline__ bool x_regs_ready(const StripCtx& c, const double2* v, int lane) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < kXPerLane; ++i)
+    if (lane + 32 * i < c.s.xcols && is_sentinel(v[i])) ok = false;
+  return __all_sync(0xffffffffu, ok);
+}
+__device__ __forceinline__ void store_x_regs(const StripCtx& c, const double2* v, double2* dst, int lane) {
+#pragma unroll
+  for (int i = 0; i < kXPerLane; ++i)
+    if (lane + 32 * i < c.s.xcols) dst[lane + 32 * i] = v[i];
 }
 
 __host__ __device__ constexpr int chunk_cols_for(int h, int slot_bytes) {
@@ -192,7 +241,9 @@ struct FlowCfg {
 // issues one cp.async.bulk into it.  It never waits on the consumer's
 // dependency polls, x gathers or completion fences, so the slot ring stays
 // full and HBM keeps streaming while the consumer is stalled.
-template <int FW, int FS, int SLOT>
+// PROF: per-warp clock64 phase timers (experiment builds only), written to
+// P.prof[(blockIdx.x * 2*FW + warp) * 16 + phase].
+template <int FW, int FS, int SLOT, bool PROF = false>
 __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant__ FlowParams P) {
   using namespace flowdev;
   using Cfg = FlowCfg<FW, FS, SLOT>;
@@ -217,6 +268,27 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
 
   const unsigned e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
+  {  // re-arm the other parity set for the next apply (nobody reads it now)
+    long long* other = reinterpret_cast<long long*>(P.stagebuf + ((e & 1u) ? 0 : P.par_elems));
+    const int64_t n = 2 * P.par_elems;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      other[i] = -1ll;
+  }
+  long long tm[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tm[i] = 0;
+  long long t_start = PROF ? clock64() : 0;
+#define FLOW_T(i, ...)                          \
+  do {                                          \
+    if (PROF) {                                 \
+      const long long t0_ = clock64();          \
+      __VA_ARGS__;                              \
+      tm[i] += clock64() - t0_;                 \
+    } else {                                    \
+      __VA_ARGS__;                              \
+    }                                           \
+  } while (0)
 
   if (producer) {
     if (lane == 0) {
@@ -251,7 +323,7 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
       for (int k = 0; k < nmine; ++k) {
         prefetch(kf <= k);
         const int sc = k % kQN;
-        mbar_wait(&cfull[sc], (k / kQN) & 1);
+        FLOW_T(0, mbar_wait(&cfull[sc], (k / kQN) & 1));
         const StripCtx& C = ctx[sc];
         const int nseg = C.s.nseg, h = C.s.h;
         const int cpc = chunk_cols_for(h, SLOT);
@@ -262,7 +334,7 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
             const int ncol = min(cpc, n - col);
             const unsigned slot = q % FS;
             if (P.nodeps == 3 && q >= FS) continue;  // timing experiment: compute on resident data
-            mbar_wait(&empty[slot], ((q / FS) & 1) ^ 1);
+            FLOW_T(1, mbar_wait(&empty[slot], ((q / FS) & 1) ^ 1));
             fence_proxy_async();
             const unsigned bytes = static_cast<unsigned>(h * ncol * 16);
             mbar_expect_tx(&full[slot], bytes);
@@ -278,22 +350,10 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
     unsigned q = 0;
     int xsel = 0;
     bool have_x = false;
-    int pending = -1;  // finished strip whose flag is not yet published
-    // Release: the strip's row stores (all lanes, ordered by the warp
-    // barrier) before its flag.  Deferred by one strip so the fence finds the
-    // stores already drained instead of waiting for them.
-    auto publish = [&]() {
-      if (pending >= 0) {
-        if (lane == 0) {
-          if (P.pubmode != 2) fence_acq_rel();
-          st_relaxed(P.flags + pending, e);
-        }
-        pending = -1;
-      }
-    };
+    const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
     for (int k = 0;; ++k) {
       const int sc = k % kQN;
-      mbar_wait(&cfull[sc], (k / kQN) & 1);
+      FLOW_T(2, mbar_wait(&cfull[sc], (k / kQN) & 1));
       const StripCtx& C = ctx[sc];
       if (C.s.y0 < 0) break;
       if (P.nodeps == 2) {  // timing experiment: stream the payload only
@@ -307,115 +367,115 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
         if (lane == 0) mbar_arrive(&cempty[sc]);
         continue;
       }
-      const int t = C.s.seg0;
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
+      const double2* xin = io.x + (io.x_par ? par_off : 0);
+      double2* yout = io.y + (io.y_par ? par_off : 0);
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + xsel * kXWin;
-      if (P.pubmode == 1) publish();
       if (fast && !have_x) {
-        publish();  // before any blocking dependency wait (deadlock freedom)
-        while (!deps_done(P, C, e, lane)) {
-        }
-        if (lane == 0) fence_acq_rel();
-        __syncwarp();
-        issue_x(P, C, xcur, lane);
+        FLOW_T(4, gather_x(C, xin, io.xperm, xcur, lane));
+        if (PROF) tm[11] += 1;  // strips whose x was not prefetched
       }
-      // x of the next strip, if its metadata is in and its producers are done
-      bool pref = false;
+      // The next strip's x: loads issued now, validated after this strip.
+      double2 nx[kXPerLane];
+      const StripCtx* Cn = nullptr;
+      const double2* nxin = nullptr;
       {
         const int sn = (k + 1) % kQN;
-        if (mbar_test(&cfull[sn], ((k + 1) / kQN) & 1)) {
-          const StripCtx& Cn = ctx[sn];
-          if (Cn.s.y0 >= 0 && Cn.s.xcols <= kXWin && deps_done(P, Cn, e, lane)) {
-            if (lane == 0) fence_acq_rel();
-            __syncwarp();
-            issue_x(P, Cn, xb + (xsel ^ 1) * kXWin, lane);
-            pref = true;
-          }
+        if (mbar_test(&cfull[sn], ((k + 1) / kQN) & 1) && ctx[sn].s.y0 >= 0 && ctx[sn].s.xcols <= kXWin) {
+          Cn = &ctx[sn];
+          const StageIO nio = P.st[Cn->s.stage];
+          nxin = nio.x + (nio.x_par ? par_off : 0);
+          load_x_regs(*Cn, nxin, nio.xperm, nx, lane);
         }
       }
-      publish();
-      if (fast) {
-        if (pref)
-          cp_async_wait<1>();
-        else
-          cp_async_wait<0>();
-        __syncwarp();
-      }
-      const bool live = lane < h;
+      // Lane mapping: strips of <= 16 rows use both half-warps (row = lane&15,
+      // column parity = lane>>4, combined by one shuffle at the end), wider
+      // strips one lane per row.
+      const bool halves = h <= 16;
+      const int row = halves ? (lane & 15) : lane;
+      const int cpar = halves ? (lane >> 4) : 0;
+      const int cstep = halves ? 2 : 1;
+      const bool live = row < h;
       const int cpc = chunk_cols_for(h, SLOT);
       double ar0 = 0, ai0 = 0, ar1 = 0, ai1 = 0;
       int cb = 0;
       for (int j = 0; j < nseg; ++j) {
         const int n = C.g[j].n;
         int win = -1;
-        if (!fast) {
-          if (lane == 0) {
-            for (int p = C.g[j].dep0; p < C.g[j].dep1 && !P.nodeps; ++p)
-              while (ld_relaxed(P.flags + p) < e) {
-              }
-            fence_acq_rel();
-          }
-          __syncwarp();
-        }
         for (int col0 = 0; col0 < n; col0 += cpc, ++q) {
           const int ncol = min(cpc, n - col0);
           const double2* xv;
           if (fast) {
             xv = xcur + cb + col0;
-          } else {  // wide strip: synchronous windows of kXWin columns
+          } else {  // wide strip: windows of kXWin columns, polled synchronously
             const int w0 = col0 / kXWin;
             if (w0 != win) {
               __syncwarp();
               const int cnt = min(kXWin, n - w0 * kXWin);
-              for (int kk = lane; kk < cnt; kk += 32) {
-                int idx = C.g[j].x0 + w0 * kXWin + kk;
-                if (io.xperm) idx = __ldg(io.xperm + idx);
-                xcur[kk] = __ldcg(io.x + idx);
-              }
+              gather_range(xin, io.xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
               __syncwarp();
               win = w0;
             }
             xv = xcur + (col0 - w0 * kXWin);
           }
           const unsigned slot = q % FS;
-          if (P.nodeps != 3 || q < FS) mbar_wait(&full[slot], (q / FS) & 1);
+          if (P.nodeps != 3 || q < FS) FLOW_T(8, mbar_wait(&full[slot], (q / FS) & 1));
           const double2* M = reinterpret_cast<const double2*>(slots + size_t(slot) * SLOT);
+          const long long tc0 = PROF ? clock64() : 0;
           if (live && P.nodeps != 4) {
-            int cc = 0;
-            for (; cc + 4 <= ncol; cc += 4) {
-              const double2 m0 = M[(cc + 0) * h + lane], m1 = M[(cc + 1) * h + lane];
-              const double2 m2 = M[(cc + 2) * h + lane], m3 = M[(cc + 3) * h + lane];
-              cmac(ar0, ai0, m0, xv[cc + 0]);
-              cmac(ar1, ai1, m1, xv[cc + 1]);
-              cmac(ar0, ai0, m2, xv[cc + 2]);
-              cmac(ar1, ai1, m3, xv[cc + 3]);
+            int cc = cpar;
+            for (; cc + 3 * cstep < ncol; cc += 4 * cstep) {
+              const double2 m0 = M[cc * h + row], m1 = M[(cc + cstep) * h + row];
+              const double2 m2 = M[(cc + 2 * cstep) * h + row], m3 = M[(cc + 3 * cstep) * h + row];
+              cmac(ar0, ai0, m0, xv[cc]);
+              cmac(ar1, ai1, m1, xv[cc + cstep]);
+              cmac(ar0, ai0, m2, xv[cc + 2 * cstep]);
+              cmac(ar1, ai1, m3, xv[cc + 3 * cstep]);
             }
-            for (; cc < ncol; ++cc) cmac(ar0, ai0, M[cc * h + lane], xv[cc]);
+            for (; cc < ncol; cc += cstep) cmac(ar0, ai0, M[cc * h + row], xv[cc]);
           }
+          if (PROF) tm[9] += clock64() - tc0;
           __syncwarp();
           if (lane == 0 && P.nodeps != 3) mbar_arrive(&empty[slot]);  // slot back to the producer
         }
         cb += n;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&cempty[sc]);  // context no longer read
-      if (live) {
-        int idx = y0 + lane;
+      double yr = ar0 + ar1, yi = ai0 + ai1;
+      if (halves) {  // odd-column half-warp adds into the even one (fixed order)
+        yr += __shfl_down_sync(0xffffffffu, yr, 16);
+        yi += __shfl_down_sync(0xffffffffu, yi, 16);
+      }
+      if (live && cpar == 0) {
+        int idx = y0 + row;
         if (io.yperm) idx = io.yperm[idx];
-        io.y[idx] = make_double2(ar0 + ar1, ai0 + ai1);
+        // The stored value is the readiness signal of this row: never let a
+        // result alias the "not yet written" sentinel.
+        yout[idx] = make_double2(unsentinel(yr), unsentinel(yi));
+      }
+      bool pref = false;
+      if (Cn) {
+        FLOW_T(5, pref = x_regs_ready(*Cn, nx, lane));
+        if (pref) {
+          store_x_regs(*Cn, nx, xb + (xsel ^ 1) * kXWin, lane);
+          __syncwarp();
+        }
       }
       __syncwarp();
-      pending = t;  // flag published at the next strip, once the stores drained
+      if (lane == 0) mbar_arrive(&cempty[sc]);  // context no longer read
       if (pref) xsel ^= 1;
       have_x = pref;
     }
-    publish();
-    cp_async_wait<0>();
+  }
+  if (PROF) {
+    tm[10] = clock64() - t_start;  // until this warp is done
+    if (lane == 0)
+      for (int i = 0; i < 16; ++i) P.prof[(static_cast<int64_t>(blockIdx.x) * 2 * FW + warp) * 16 + i] = tm[i];
   }
   __syncthreads();
   if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) = e;
 }
+#undef FLOW_T
 
 }  // namespace midbf::dev

@@ -177,6 +177,9 @@ int flow_setup(int num_sms) {
   cuda_check(cudaFuncSetAttribute(k1_flow<FW, FS, SLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)),
              "flow smem attribute");
+  cuda_check(cudaFuncSetAttribute(k1_flow<FW, FS, SLOT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "flow smem attribute");
   int per_sm = 0;
   cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_flow<FW, FS, SLOT>, 2 * FW * 32, smem),
              "occupancy");
@@ -185,14 +188,8 @@ int flow_setup(int num_sms) {
 }
 
 template <int FW, int FS, int SLOT>
-void flow_launch(FlowParams& P, int grid, cudaStream_t stream, Direction& D, int& last_nwarps) {
+void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
   P.nwarps = grid * FW;
-  if (last_nwarps != P.nwarps) {  // counters assume a fixed warp count
-    cuda_check(cudaMemsetAsync(D.d_sync, 0, (static_cast<size_t>(D.nstrips) + kMaxFlowCtas) * sizeof(unsigned),
-                               stream),
-               "reset flow counters");
-    last_nwarps = P.nwarps;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
   cfg.blockDim = dim3(2 * FW * 32, 1, 1);
@@ -203,7 +200,10 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream, Direction& D, int
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT>, P), "k1_flow launch");
+  if (P.prof)
+    cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT, true>, P), "k1_flow launch");
+  else
+    cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT>, P), "k1_flow launch");
 }
 
 }  // namespace
@@ -365,10 +365,11 @@ void Plan::build_direction(int d, const PlanTables& T) {
     }
     up(reinterpret_cast<void**>(&D.d_ctx), ctxs.data(), ctxs.size() * sizeof(StripCtx), "upload strip records");
   }
-  cuda_check(cudaMalloc(&D.d_stagebuf, D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
-  const size_t sync_words = static_cast<size_t>(D.nstrips) + kMaxFlowCtas;
-  cuda_check(cudaMalloc(&D.d_sync, sync_words * sizeof(unsigned)), "cudaMalloc sync");
-  cuda_check(cudaMemset(D.d_sync, 0, sync_words * sizeof(unsigned)), "memset sync");
+  // two parity sets, armed with the all-ones sentinel (k1_flow's ready signal)
+  cuda_check(cudaMalloc(&D.d_stagebuf, 2 * D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
+  cuda_check(cudaMemset(D.d_stagebuf, 0xff, 2 * D.stagebuf_elems * sizeof(double2)), "arm stage buffers");
+  cuda_check(cudaMalloc(&D.d_sync, kMaxFlowCtas * sizeof(unsigned)), "cudaMalloc sync");
+  cuda_check(cudaMemset(D.d_sync, 0, kMaxFlowCtas * sizeof(unsigned)), "memset sync");
   D.built = true;
 }
 
@@ -411,6 +412,7 @@ Plan::~Plan() {
     cudaFree(D.d_sync);
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  cudaFree(d_prof);
   cudaFree(d_row_perm);
   cudaFree(d_col_perm);
   cudaFree(d_buf[0]);
@@ -455,11 +457,12 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.strips = D.d_strips;
   P.segs = D.d_segs;
   P.arena = D.d_arena;
-  P.flags = D.d_sync;
-  P.epoch = D.d_sync + D.nstrips;
+  P.epoch = D.d_sync;
+  P.stagebuf = D.d_stagebuf;
+  P.par_elems = D.stagebuf_elems;
   P.nstrips = static_cast<int>(D.nstrips);
   P.nodeps = static_cast<int>((flags >> 6) & 7u);  // bits 6-8: timing experiments
-  P.pubmode = static_cast<int>((flags >> 9) & 3u);  // bits 9-10: flag publish policy
+  if ((flags & 4096u) && d_prof) P.prof = d_prof;  // bit 12: phase timers (experiments)
   const int ns = static_cast<int>(D.stages.size());
   for (int s = 0; s < ns; ++s) {
     StageIO& io = P.st[s];
@@ -467,18 +470,18 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
     io.y = s == ns - 1 ? out : D.d_stagebuf + D.stages[s].buf_off;
     io.xperm = s == 0 ? (d == 0 ? d_col_perm : d_row_perm) : nullptr;
     io.yperm = s == ns - 1 ? (d == 0 ? d_row_perm : d_col_perm) : nullptr;
+    io.x_par = s == 0 ? 0 : 1;
+    io.y_par = s == ns - 1 ? 0 : 1;
   }
-  // The done counter advances by nwarps per apply: keep the variant's warp
-  // count fixed for the plan's lifetime (reset the counters on a change).
   switch (variant) {
     case 1:
-      flow_launch<8, 2, 8192>(P, flow_grid[1], stream, D, last_nwarps[d]);
+      flow_launch<8, 2, 8192>(P, flow_grid[1], stream);
       break;
     case 2:
-      flow_launch<6, 4, 8192>(P, flow_grid[2], stream, D, last_nwarps[d]);
+      flow_launch<6, 4, 8192>(P, flow_grid[2], stream);
       break;
     default:
-      flow_launch<4, 3, 16384>(P, flow_grid[0], stream, D, last_nwarps[d]);
+      flow_launch<4, 3, 16384>(P, flow_grid[0], stream);
   }
 }
 
@@ -560,9 +563,23 @@ void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStre
 
 // Device-operand apply; the launch sequence is captured once per operand set
 // into a CUDA graph.
+// k1_flow keeps per-CTA apply epochs (parity of the stage-buffer set) that
+// assume one grid size; a variant switch re-initialises them, outside any
+// stream capture and after all earlier work.
+void Plan::prepare_flow(int d) {
+  const int grid = flow_grid[(flags >> 4) & 3u];
+  if (last_grid[d] == grid) return;
+  Direction& D = dir[d];
+  cuda_check(cudaDeviceSynchronize(), "flow reset sync");
+  cuda_check(cudaMemset(D.d_sync, 0, kMaxFlowCtas * sizeof(unsigned)), "reset flow epochs");
+  cuda_check(cudaMemset(D.d_stagebuf, 0xff, 2 * D.stagebuf_elems * sizeof(double2)), "arm stage buffers");
+  last_grid[d] = grid;
+}
+
 void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
   ensure_buffers(nrhs);
+  if (flow_ok(d, nrhs)) prepare_flow(d);
   if (dir[d].stages.empty()) return;
   if (!(flags & 4u)) {
     launch(d, in, out, nrhs, stream);

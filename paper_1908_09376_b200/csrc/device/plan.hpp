@@ -11,7 +11,7 @@
 namespace midbf::dev {
 
 constexpr int kMaxStages = 64;
-constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words after the strip flags
+constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 
 // Output strip of <= 32 rows of one stage; one warp computes it.
 struct Strip {
@@ -63,8 +63,8 @@ struct Direction {
   Seg* d_segs = nullptr;
   double2* d_arena = nullptr;
   void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh)
-  double2* d_stagebuf = nullptr;  // outputs of every stage but the last
-  unsigned* d_sync = nullptr;     // [strip flags (nstrips) | per-CTA epochs (kMaxFlowCtas)]
+  double2* d_stagebuf = nullptr;  // outputs of every stage but the last, two parity sets
+  unsigned* d_sync = nullptr;     // per-CTA apply epochs (kMaxFlowCtas)
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
   int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
 };
@@ -97,14 +97,16 @@ class Plan {
   // bit3 persistent dataflow kernel for single-RHS applies,
   // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size),
   // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS).
-  unsigned flags = 0x1F;  // default: k1_flow variant 1 (8 pairs x 2 x 8 KB), fastest measured at cfg1
+  unsigned flags = 0xF;  // default: k1_flow variant 0 (4 pairs x 3 x 16 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
   int strip_rows = 32;  // output rows per strip (one warp's lanes)
+  long long* d_prof = nullptr;  // k1_flow phase timers (flag bit 12)
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
   bool k2_ok(int64_t nrhs) const;
-  int last_nwarps[2] = {0, 0};
+  int last_grid[2] = {-1, -1};
+  void prepare_flow(int d);
 
  private:
   void build_direction(int d, const PlanTables& T);

@@ -247,10 +247,27 @@ extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out,
 // Tuning switches (bench / profiling): bit0 PDL, bit1 L2 bulk prefetch
 // (stage kernels), bit2 CUDA graphs, bit3 persistent dataflow kernel.
 extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
-  return guard([&] { plan->p->flags = flags; });
+  return guard([&] {
+    Plan& p = *plan->p;
+    p.flags = flags;
+    if ((flags & 4096u) && !p.d_prof)  // phase-timer buffer, allocated outside any capture
+      midbf::dev::cuda_check(cudaMalloc(&p.d_prof, size_t(1024) * 64 * 16 * sizeof(long long)), "prof buffer");
+  });
 }
 
 // Kernel launches of one apply (evidence for bench.py's gpu_launches).
 extern "C" int midbf_plan_launches(midbf_plan_t plan, int transpose, int64_t nrhs, int64_t* out) {
   return guard([&] { *out = plan->p->launches_per_apply(transpose ? 1 : 0, nrhs); });
+}
+
+// Phase timers of the last k1_flow launch made with flag bit 12: per warp
+// 16 counters (cycles); out must hold grid * 2 * warps_per_cta * 16 values.
+extern "C" int midbf_plan_flow_profile(midbf_plan_t plan, int64_t* out, int64_t n) {
+  return guard([&] {
+    Plan& p = *plan->p;
+    if (!p.d_prof) throw std::logic_error("no profiled k1_flow launch");
+    midbf::dev::cuda_check(cudaDeviceSynchronize(), "sync");
+    const size_t bytes = std::min<size_t>(static_cast<size_t>(n), size_t(1024) * 64 * 16) * sizeof(long long);
+    midbf::dev::cuda_check(cudaMemcpy(out, p.d_prof, bytes, cudaMemcpyDeviceToHost), "prof D2H");
+  });
 }

@@ -1,0 +1,49 @@
+"""Phase breakdown of k1_flow at cfg1 (flag bit 12 phase timers).
+
+    python tools/flow_phases.py [flags]
+Prints, per warp role, the mean cycles per apply spent in each phase.
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_1908_09376_b200 as M  # noqa: E402
+
+NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "-", "C: x gather+poll (not prefetched)",
+         "C: next-x validate", "-", "-", "C: wait full slot", "C: FMA loop", "total", "strips w/o prefetched x"]
+
+
+def main():
+    flags = int(sys.argv[1]) if len(sys.argv) > 1 else 31
+    K, X, Om, fk, nrhs, desc = bench.workload("cfg1")
+    F = M.idbf_factorize(K, 64, k=30, eps=1e-9, seed=M.chain(0, 0x666163))
+    plan = F.plan(1)
+    M.lib().midbf_plan_set_flags(plan._h, flags | 4096)
+    f = torch.randn(F.ncols, dtype=torch.complex128, device="cuda")
+    g = torch.empty(F.nrows, dtype=torch.complex128, device="cuda")
+    for _ in range(5):
+        plan.apply_ptr(f.data_ptr(), g.data_ptr(), 1, False, 0)
+    torch.cuda.synchronize()
+    fw = {15: 4, 31: 8, 47: 6}[flags & 63]
+    grid = 148
+    n = grid * 2 * fw * 16
+    out = np.zeros(n, dtype=np.int64)
+    M.lib().midbf_plan_flow_profile(plan._h, out.ctypes.data_as(C.POINTER(C.c_int64)), C.c_int64(n))
+    t = out.reshape(grid, 2 * fw, 16)
+    cons, prod = t[:, :fw, :].reshape(-1, 16), t[:, fw:, :].reshape(-1, 16)
+    clk = 1.965e3  # cycles per us
+    for role, arr in (("consumer", cons), ("producer", prod)):
+        print(f"== {role} warps ({len(arr)}), mean over warps, us")
+        for i, name in enumerate(NAMES):
+            if arr[:, i].any():
+                v = arr[:, i].mean()
+                print(f"  {name:28s} {v / clk if i != 11 else v:9.2f}   (max {arr[:, i].max() / (clk if i != 11 else 1):.2f})")
+
+
+if __name__ == "__main__":
+    main()
