@@ -57,6 +57,9 @@ struct FlowParams {
   unsigned* epoch;   // per CTA: applies completed (all CTAs run every apply)
   double2* stagebuf;  // both parity sets of intermediate stage buffers
   int64_t par_elems;  // complex entries per parity set
+  const double2* in;  // user input (read once by the permutation prologue)
+  const int* in_perm;
+  int64_t in_len;
   int nstrips;
   int nwarps;
   // Timing experiments only (results invalid): 2 stream the payload only,
@@ -126,7 +129,7 @@ __device__ __forceinline__ double unsentinel(double v) {
 }
 __device__ __forceinline__ double2 ld_cg(const double2* p) {
   double2 v;
-  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 // input index of the strip's flattened staged column kk
@@ -178,14 +181,23 @@ __device__ __forceinline__ void gather_x(const StripCtx& c, const double2* x, co
 }
 __device__ __forceinline__ void load_x_regs(const StripCtx& c, const double2* x, const int* xperm, double2* v,
                                             int lane) {
+  // input index of each of this lane's staged columns, one pass over the panels
+  int idx[kXPerLane];
 #pragma unroll
-  for (int i = 0; i < kXPerLane; ++i) {
-    const int kk = lane + 32 * i;
-    if (kk < c.s.xcols) {
-      const int idx = x_index(c, kk);
-      v[i] = xperm ? __ldg(x + __ldg(xperm + idx)) : ld_cg(x + idx);
+  for (int i = 0; i < kXPerLane; ++i) idx[i] = -1;
+  int cb = 0;
+  for (int j = 0; j < c.s.nseg; ++j) {
+    const int n = c.g[j].n, x0 = c.g[j].x0;
+#pragma unroll
+    for (int i = 0; i < kXPerLane; ++i) {
+      const int kk = lane + 32 * i - cb;
+      if (kk >= 0 && kk < n) idx[i] = x0 + kk;
     }
+    cb += n;
   }
+#pragma unroll
+  for (int i = 0; i < kXPerLane; ++i)
+    if (idx[i] >= 0) v[i] = xperm ? __ldg(x + __ldg(xperm + idx[i])) : ld_cg(x + idx[i]);
 }
 __device__ __forceinline__ bool x_regs_ready(const StripCtx& c, const double2* v, int lane) {
   bool ok = true;
@@ -268,12 +280,20 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
 
   const unsigned e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
-  {  // re-arm the other parity set for the next apply (nobody reads it now)
+  const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
+  {
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t di = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    // stage -1: the input permutation, gathered once into the head of this
+    // apply's set (sentinel-armed; stage 0 polls it like any other stage)
+    double2* x0 = P.stagebuf + par_off;
+    for (int64_t i = i0; i < P.in_len; i += di) {
+      const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
+      x0[i] = make_double2(unsentinel(v.x), unsentinel(v.y));
+    }
+    // re-arm the other set for the next apply (nobody reads it now)
     long long* other = reinterpret_cast<long long*>(P.stagebuf + ((e & 1u) ? 0 : P.par_elems));
-    const int64_t n = 2 * P.par_elems;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      other[i] = -1ll;
+    for (int64_t i = i0; i < 2 * P.par_elems; i += di) other[i] = -1ll;
   }
   long long tm[16];
 #pragma unroll
@@ -350,7 +370,6 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
     unsigned q = 0;
     int xsel = 0;
     bool have_x = false;
-    const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
     for (int k = 0;; ++k) {
       const int sc = k % kQN;
       FLOW_T(2, mbar_wait(&cfull[sc], (k / kQN) & 1));
@@ -387,7 +406,7 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
           Cn = &ctx[sn];
           const StageIO nio = P.st[Cn->s.stage];
           nxin = nio.x + (nio.x_par ? par_off : 0);
-          load_x_regs(*Cn, nxin, nio.xperm, nx, lane);
+          FLOW_T(6, load_x_regs(*Cn, nxin, nio.xperm, nx, lane));
         }
       }
       // Lane mapping: strips of <= 16 rows use both half-warps (row = lane&15,
@@ -399,7 +418,9 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
       const int cstep = halves ? 2 : 1;
       const bool live = row < h;
       const int cpc = chunk_cols_for(h, SLOT);
-      double ar0 = 0, ai0 = 0, ar1 = 0, ai1 = 0;
+      int yidx = y0 + row;  // output permutation looked up now, used after the compute
+      if (io.yperm && live && cpar == 0) yidx = io.yperm[yidx];
+      double ar0 = 0, ai0 = 0, ar1 = 0, ai1 = 0, ar2 = 0, ai2 = 0, ar3 = 0, ai3 = 0;
       int cb = 0;
       for (int j = 0; j < nseg; ++j) {
         const int n = C.g[j].n;
@@ -425,16 +446,38 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
           const double2* M = reinterpret_cast<const double2*>(slots + size_t(slot) * SLOT);
           const long long tc0 = PROF ? clock64() : 0;
           if (live && P.nodeps != 4) {
+            // one consumer warp per SM sub-partition: 4 independent
+            // accumulators keep the DFMA chains short (latency 8 cycles)
             int cc = cpar;
-            for (; cc + 3 * cstep < ncol; cc += 4 * cstep) {
-              const double2 m0 = M[cc * h + row], m1 = M[(cc + cstep) * h + row];
-              const double2 m2 = M[(cc + 2 * cstep) * h + row], m3 = M[(cc + 3 * cstep) * h + row];
-              cmac(ar0, ai0, m0, xv[cc]);
-              cmac(ar1, ai1, m1, xv[cc + cstep]);
-              cmac(ar0, ai0, m2, xv[cc + 2 * cstep]);
-              cmac(ar1, ai1, m3, xv[cc + 3 * cstep]);
+            for (; cc + 7 * cstep < ncol; cc += 8 * cstep) {
+              double2 m[8], xr[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                m[i] = M[(cc + i * cstep) * h + row];
+                xr[i] = xv[cc + i * cstep];
+              }
+              cmac(ar0, ai0, m[0], xr[0]);
+              cmac(ar1, ai1, m[1], xr[1]);
+              cmac(ar2, ai2, m[2], xr[2]);
+              cmac(ar3, ai3, m[3], xr[3]);
+              cmac(ar0, ai0, m[4], xr[4]);
+              cmac(ar1, ai1, m[5], xr[5]);
+              cmac(ar2, ai2, m[6], xr[6]);
+              cmac(ar3, ai3, m[7], xr[7]);
             }
-            for (; cc < ncol; cc += cstep) cmac(ar0, ai0, M[cc * h + row], xv[cc]);
+            if (cc + 3 * cstep < ncol) {  // remainder spread over the 4 chains
+              cmac(ar0, ai0, M[cc * h + row], xv[cc]);
+              cmac(ar1, ai1, M[(cc + cstep) * h + row], xv[cc + cstep]);
+              cmac(ar2, ai2, M[(cc + 2 * cstep) * h + row], xv[cc + 2 * cstep]);
+              cmac(ar3, ai3, M[(cc + 3 * cstep) * h + row], xv[cc + 3 * cstep]);
+              cc += 4 * cstep;
+            }
+            if (cc + cstep < ncol) {
+              cmac(ar0, ai0, M[cc * h + row], xv[cc]);
+              cmac(ar1, ai1, M[(cc + cstep) * h + row], xv[cc + cstep]);
+              cc += 2 * cstep;
+            }
+            if (cc < ncol) cmac(ar2, ai2, M[cc * h + row], xv[cc]);
           }
           if (PROF) tm[9] += clock64() - tc0;
           __syncwarp();
@@ -442,18 +485,14 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
         }
         cb += n;
       }
-      double yr = ar0 + ar1, yi = ai0 + ai1;
+      double yr = (ar0 + ar1) + (ar2 + ar3), yi = (ai0 + ai1) + (ai2 + ai3);
       if (halves) {  // odd-column half-warp adds into the even one (fixed order)
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
-      if (live && cpar == 0) {
-        int idx = y0 + row;
-        if (io.yperm) idx = io.yperm[idx];
-        // The stored value is the readiness signal of this row: never let a
-        // result alias the "not yet written" sentinel.
-        yout[idx] = make_double2(unsentinel(yr), unsentinel(yi));
-      }
+      // The stored value is the readiness signal of this row: never let a
+      // result alias the "not yet written" sentinel.
+      FLOW_T(7, if (live && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
       bool pref = false;
       if (Cn) {
         FLOW_T(5, pref = x_regs_ready(*Cn, nx, lane));

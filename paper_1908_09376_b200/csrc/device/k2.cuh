@@ -9,8 +9,8 @@
 // so the FP64 tensor path is the warp-level mma.sync.m8n8k4.f64 (DMMA),
 // measured at 36.8 TFLOP/s on this B200 (tools/fp64_probe.cu).
 //
-// CTA = one strip x 64 right-hand sides, 4 warps; warp w owns rows
-// [8w, 8w+8) and all 8 column blocks of 8 RHS.  A complex MAC is four real
+// CTA = one strip x 64 right-hand sides, 8 warps (8 rows x 32 RHS each).
+// A complex MAC is four real
 // DMMAs (re*re, -im*im, re*im, im*re) into separate re/im accumulators.
 // Operands move global -> shared with cp.async (16 B per complex entry) in
 // 32-column K chunks, double-buffered; the shared layouts are padded so
@@ -58,32 +58,38 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // One stage.  x/y: column-major (len x nrhs, leading dims xld/yld); stage 0
 // gathers rows through xperm, the last stage scatters through yperm.
-__global__ void __launch_bounds__(128) k2_stage(const Strip* __restrict__ strips, const Seg* __restrict__ segs,
-                                                const double2* __restrict__ arena, const double2* __restrict__ x,
-                                                int64_t xld, const int* __restrict__ xperm, double2* __restrict__ y,
-                                                int64_t yld, const int* __restrict__ yperm, int nrhs) {
+// 8 warps: warp w owns rows 8*(w&3) .. +8 and RHS 32*(w>>2) .. +32 (4 column
+// blocks of 8) of the CTA's 32 x 64 output tile.
+constexpr int kK2Threads = 256;
+__global__ void __launch_bounds__(kK2Threads, 2) k2_stage(const Strip* __restrict__ strips, const Seg* __restrict__ segs,
+                                                       const double2* __restrict__ arena,
+                                                       const double2* __restrict__ x, int64_t xld,
+                                                       const int* __restrict__ xperm, double2* __restrict__ y,
+                                                       int64_t yld, const int* __restrict__ yperm, int nrhs) {
   using namespace k2dev;
   extern __shared__ __align__(16) double2 k2smem[];
-  double2* const Pb = k2smem;                 // 2 panel buffers
-  double2* const Xb = k2smem + 2 * kK2PBuf;   // 2 X buffers
+  double2* const Pb = k2smem;                // 2 panel buffers
+  double2* const Xb = k2smem + 2 * kK2PBuf;  // 2 X buffers
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int rb = w & 3, ch = w >> 2;  // row block, RHS half
   const Strip st = strips[blockIdx.x];
   const int h = st.h;
-  const int c0 = blockIdx.y * kK2Rhs;                  // first RHS of this tile
-  const int ncv = min(kK2Rhs, nrhs - c0);              // valid RHS in the tile
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // previous stage's output
+  const int c0 = blockIdx.y * kK2Rhs;      // first RHS of this tile
+  const int ncv = min(kK2Rhs, nrhs - c0);  // valid RHS in the tile
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous stage's output
   asm volatile("griddepcontrol.launch_dependents;" :::);
 
-  double acc[8][2][2];  // [col block][re, im][2 entries]
+  double acc[4][2][2];  // [col block][re, im][2 entries]
 #pragma unroll
-  for (int cb = 0; cb < 8; ++cb)
+  for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
     for (int r = 0; r < 2; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
 
-  // zero the padding rows/cols once (rows >= h, RHS >= ncv) in both buffers
-  for (int i = tid; i < 2 * kK2PBuf; i += 128) k2smem[i] = make_double2(0, 0);
-  for (int i = tid; i < 2 * kK2XBuf; i += 128) k2smem[2 * kK2PBuf + i] = make_double2(0, 0);
+  // Zero both buffers once: rows >= h, RHS >= ncv and K tails of short
+  // chunks stay zero (tails are re-zeroed per chunk below), so the inner
+  // loop needs no masking.
+  for (int i = tid; i < 2 * (kK2PBuf + kK2XBuf); i += kK2Threads) k2smem[i] = make_double2(0, 0);
   __syncthreads();
 
   // chunk enumeration over the strip's panels: (seg j, column c)
@@ -92,15 +98,26 @@ __global__ void __launch_bounds__(128) k2_stage(const Strip* __restrict__ strips
     const Seg s = segs[st.seg0 + jj];
     const int kc = min(kK2Kc, s.n - cc);
     const double2* P = arena + s.off + static_cast<int64_t>(cc) * h;
-    for (int e = tid; e < kc * h; e += 128) {  // panel: contiguous h x kc
-      const int col = e / h, row = e - col * h;
-      cp_async16(Pb + buf * kK2PBuf + col * kK2Ps + row, P + e);
+    double2* pd = Pb + buf * kK2PBuf;
+    double2* xd = Xb + buf * kK2XBuf;
+    for (int col = w; col < kK2Kc; col += kK2Threads / 32) {  // panel columns (lane = row)
+      if (lane < h) {
+        if (col < kc)
+          cp_async16(pd + col * kK2Ps + lane, P + col * h + lane);
+        else
+          pd[col * kK2Ps + lane] = make_double2(0, 0);
+      }
     }
-    for (int e = tid; e < kc * ncv; e += 128) {  // X rows x0+cc .. +kc, RHS c0 ..
-      const int rhs = e / kc, k = e - rhs * kc;
-      int idx = s.x0 + cc + k;
-      if (xperm) idx = __ldg(xperm + idx);
-      cp_async16(Xb + buf * kK2XBuf + k * kK2Xs + rhs, x + static_cast<int64_t>(c0 + rhs) * xld + idx);
+    for (int rhs = w; rhs < ncv; rhs += kK2Threads / 32) {  // X rows x0+cc .. (lane = k)
+      const double2* xc = x + static_cast<int64_t>(c0 + rhs) * xld;
+      const int k = lane;
+      if (k < kc) {
+        int idx = s.x0 + cc + k;
+        if (xperm) idx = __ldg(xperm + idx);
+        cp_async16(xd + k * kK2Xs + rhs, xc + idx);
+      } else {
+        xd[k * kK2Xs + rhs] = make_double2(0, 0);
+      }
     }
     cp_async_commit();
     return kc;
@@ -109,7 +126,6 @@ __global__ void __launch_bounds__(128) k2_stage(const Strip* __restrict__ strips
     int kc_cur = stage(0, 0, 0);
     int buf = 0;
     while (true) {
-      // next chunk
       int jn = j, cn = c + kc_cur;
       if (cn >= segs[st.seg0 + jn].n) {
         ++jn;
@@ -124,21 +140,18 @@ __global__ void __launch_bounds__(128) k2_stage(const Strip* __restrict__ strips
         cp_async_wait<0>();
       __syncthreads();
       const double2* Ps = Pb + buf * kK2PBuf;
-      const double2* Xs = Xb + buf * kK2XBuf;
-      for (int kk = 0; kk < kc_cur; kk += 4) {
-        // A fragment: row 8w+g, k = kk+t (zero beyond kc_cur: stale tail of a
-        // previous chunk is masked by the B fragment below)
-        const bool kv = kk + t < kc_cur;
-        const double2 a = Ps[(kk + t) * kK2Ps + 8 * w + g];
-        const double are = kv ? a.x : 0.0, aim = kv ? a.y : 0.0, naim = -aim;
+      const double2* Xs = Xb + buf * kK2XBuf + ch * 32;
+      const int kend = (kc_cur + 3) & ~3;
+      for (int kk = 0; kk < kend; kk += 4) {
+        const double2 a = Ps[(kk + t) * kK2Ps + 8 * rb + g];
+        const double naim = -a.y;
 #pragma unroll
-        for (int cb = 0; cb < 8; ++cb) {
+        for (int cb = 0; cb < 4; ++cb) {
           const double2 b = Xs[(kk + t) * kK2Xs + cb * 8 + g];
-          const double bre = kv ? b.x : 0.0, bim = kv ? b.y : 0.0;
-          dmma(acc[cb][0][0], acc[cb][0][1], are, bre);
-          dmma(acc[cb][0][0], acc[cb][0][1], naim, bim);
-          dmma(acc[cb][1][0], acc[cb][1][1], are, bim);
-          dmma(acc[cb][1][0], acc[cb][1][1], aim, bre);
+          dmma(acc[cb][0][0], acc[cb][0][1], a.x, b.x);
+          dmma(acc[cb][0][0], acc[cb][0][1], naim, b.y);
+          dmma(acc[cb][1][0], acc[cb][1][1], a.x, b.y);
+          dmma(acc[cb][1][0], acc[cb][1][1], a.y, b.x);
         }
       }
       __syncthreads();
@@ -149,16 +162,16 @@ __global__ void __launch_bounds__(128) k2_stage(const Strip* __restrict__ strips
       buf ^= 1;
     }
   }
-  // D fragment: row 8w+g, columns cb*8 + 2t + {0,1}
-  const int row = 8 * w + g;
+  // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}
+  const int row = 8 * rb + g;
   if (row < h) {
     int idx = st.y0 + row;
     if (yperm) idx = yperm[idx];
 #pragma unroll
-    for (int cb = 0; cb < 8; ++cb)
+    for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int rhs = cb * 8 + 2 * t + i;
+        const int rhs = 32 * ch + cb * 8 + 2 * t + i;
         if (rhs < ncv) y[static_cast<int64_t>(c0 + rhs) * yld + idx] = make_double2(acc[cb][0][i], acc[cb][1][i]);
       }
   }

@@ -221,7 +221,9 @@ void Plan::build_direction(int d, const PlanTables& T) {
   std::vector<Seg> segs;
   std::vector<double> arena;
   arena.reserve(static_cast<size_t>(2 * T.total_nnz));
-  int64_t bufoff = 0;
+  // stage buffer layout: [permuted input of stage 0 | output of stage 0 | ...]
+  D.in_len = d == 0 ? T.factors[static_cast<size_t>(nf - 1)].cols : T.factors[0].rows;
+  int64_t bufoff = std::max<int64_t>(D.in_len, 1);
 
   for (int64_t s = 0; s < nf; ++s) {
     const int64_t fi = d == 0 ? nf - 1 - s : s;
@@ -466,13 +468,16 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   const int ns = static_cast<int>(D.stages.size());
   for (int s = 0; s < ns; ++s) {
     StageIO& io = P.st[s];
-    io.x = s == 0 ? in : D.d_stagebuf + D.stages[s - 1].buf_off;
+    io.x = s == 0 ? D.d_stagebuf : D.d_stagebuf + D.stages[s - 1].buf_off;  // stage 0: permuted input
     io.y = s == ns - 1 ? out : D.d_stagebuf + D.stages[s].buf_off;
-    io.xperm = s == 0 ? (d == 0 ? d_col_perm : d_row_perm) : nullptr;
+    io.xperm = nullptr;
     io.yperm = s == ns - 1 ? (d == 0 ? d_row_perm : d_col_perm) : nullptr;
-    io.x_par = s == 0 ? 0 : 1;
+    io.x_par = 1;
     io.y_par = s == ns - 1 ? 0 : 1;
   }
+  P.in = in;
+  P.in_perm = d == 0 ? d_col_perm : d_row_perm;
+  P.in_len = D.in_len;
   switch (variant) {
     case 1:
       flow_launch<8, 2, 8192>(P, flow_grid[1], stream);
@@ -535,7 +540,7 @@ void Plan::launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaS
     const int64_t yld = s == ns - 1 ? (d == 0 ? nrows : ncols) : max_len;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(st.nstrips), static_cast<unsigned>((nrhs + kK2Rhs - 1) / kK2Rhs), 1);
-    cfg.blockDim = dim3(128, 1, 1);
+    cfg.blockDim = dim3(kK2Threads, 1, 1);
     cfg.dynamicSmemBytes = kK2Smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];

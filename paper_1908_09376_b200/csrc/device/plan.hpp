@@ -67,6 +67,7 @@ struct Direction {
   unsigned* d_sync = nullptr;     // per-CTA apply epochs (kMaxFlowCtas)
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
   int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
+  int64_t in_len = 0;  // input length of the first stage (head of the stage buffers)
 };
 
 struct GraphEntry {

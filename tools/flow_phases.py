@@ -15,7 +15,7 @@ import bench  # noqa: E402
 import paper_1908_09376_b200 as M  # noqa: E402
 
 NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "-", "C: x gather+poll (not prefetched)",
-         "C: next-x validate", "-", "-", "C: wait full slot", "C: FMA loop", "total", "strips w/o prefetched x"]
+         "C: next-x validate", "C: next-x load issue", "C: y store", "C: wait full slot", "C: FMA loop", "total", "strips w/o prefetched x"]
 
 
 def main():
