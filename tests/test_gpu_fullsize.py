@@ -1,0 +1,97 @@
+"""Parity at BASELINE.json's full sizes.
+
+cfg1 / cfg3 are factorized on the device (K3 entries, host IDs), handed to
+the oracle as MIDBF001, and the device apply (K1, K2) must match the
+oracle's restated reference apply to rel-L2 <= 1e-12.  Size-independent
+identities (adjoint, linearity) are checked on the device alone, and the
+Omega = X companion is checked against the direct sum (K4)."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1908_09376_b200 as M
+from helpers import cvec, integer_grid, rel, unit_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_factorization(kind, X, Om, n0, k):
+    K = M.Kernel(kind, X=X, Omega=Om)
+    F = M.idbf_factorize(K, n0, k=k, eps=1e-9, t=5, seed=M.chain(0, 0x666163))
+    return K, F
+
+
+@pytest.fixture(scope="module")
+def cfg1(gpu):
+    X, Om = unit_grid(256, 2), integer_grid(256, 2)
+    K, F = _device_factorization(M.KIND_FIO2D, X, Om, 64, 30)
+    fd, path = tempfile.mkstemp(suffix=".midbf")
+    os.close(fd)
+    F.save(path)
+    Fo = O.load(path)
+    plan = M.DevicePlan.load(path, directions=3)
+    os.unlink(path)
+    return K, F, Fo, plan
+
+
+def test_cfg1_structure_matches_appendix_b(cfg1):
+    K, F, Fo, plan = cfg1
+    assert (F.L, F.h, F.nfactors) == (5, 3, 7)
+    assert F.total_nnz == 22364160  # every ID saturates at k for integer xi
+    assert F.max_factor_nnz <= F.nnz_bound(4.0)
+    entries, calls, _ = F.sample_stats()
+    assert entries == 93388800 and calls == 7
+
+
+def test_cfg1_apply_matches_oracle(cfg1):
+    K, F, Fo, plan = cfg1
+    f = O.random_coefficients(65536, O.chain(0, 0x66))
+    go = Fo.apply(f)
+    assert rel(F.apply(f), go) <= 1e-12  # k1_flow through the C++ drop-in
+    assert rel(plan.apply(f), go) <= 1e-12  # MIDBF001 -> device plan
+    g = cvec(65536, 5)
+    assert rel(plan.apply(g, transpose=True), Fo.apply_transpose(g)) <= 1e-12
+
+
+def test_cfg4_multi_rhs_matches_oracle(cfg1):
+    K, F, Fo, plan = cfg1
+    X = cvec(65536, 6, cols=64)
+    assert rel(plan.apply(X), Fo.apply(X)) <= 1e-12  # K2 (DMMA)
+
+
+def test_cfg1_identities_on_device(cfg1):
+    K, F, Fo, plan = cfg1
+    f, g = cvec(65536, 7), cvec(65536, 8)
+    lhs, rhs = plan.apply(f) @ g, f @ plan.apply(g, transpose=True)
+    assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(f) * np.linalg.norm(g)
+    a, b = 0.3 - 1.1j, -2.0 + 0.7j
+    assert rel(plan.apply(a * f + b * g), a * plan.apply(f) + b * plan.apply(g)) <= 1e-12
+    assert np.array_equal(plan.apply(f), plan.apply(f))
+
+
+def test_cfg1_unit_xi_companion_accuracy(gpu):
+    """Omega = X (the reference's convention, src/experiment.cpp:41-42): the
+    factorization is accurate against the direct sum (K4) on 256 sampled
+    rows, as metrics::eps_b does (src/metrics.cpp:26-48)."""
+    X = unit_grid(256, 2)
+    K, F = _device_factorization(M.KIND_FIO2D, X, X.copy(), 64, 30)
+    f = M.random_coefficients(65536, M.chain(0, 0x66))
+    eps_b = K.eps_b(F.apply(f), f, nrows=256, seed=M.chain(0, 0x657062))
+    assert eps_b <= 1e-6
+    assert F.total_nnz < 22364160  # adaptive ranks below k
+
+
+def test_cfg3_apply_matches_oracle(gpu):
+    X, Om = unit_grid(32, 3), integer_grid(32, 3)
+    K, F = _device_factorization(M.KIND_FIO3D, X, Om, 64, 64)
+    assert (F.L, F.nfactors) == (3, 5)
+    fd, path = tempfile.mkstemp(suffix=".midbf")
+    os.close(fd)
+    F.save(path)
+    Fo = O.load(path)
+    os.unlink(path)
+    f = cvec(32768, 9)
+    assert rel(F.apply(f), Fo.apply(f)) <= 1e-12
