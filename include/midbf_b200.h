@@ -98,6 +98,13 @@ int midbf_plan_info(midbf_plan_t plan, int64_t* out);
  * `stream` is a cudaStream_t (NULL = legacy default).  Replaces bf::apply /
  * bf::apply_transpose (include/midbf/butterfly.hpp:123-126). */
 int midbf_apply(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose, void* stream);
+/* Pipelined variant for host operands (serving): enqueues H2D, apply and D2H
+ * on internal streams with rotating device staging, and returns at once;
+ * `stream` waits for this call's result (synchronize it before reading g or
+ * reusing f; f is read asynchronously and is not ordered after earlier
+ * work on `stream`).  Consecutive calls overlap their copies with the
+ * previous apply.  Pinned host memory is needed for real overlap. */
+int midbf_apply_async(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose, void* stream);
 
 /* ------------------------------------------------------- entry sampling
  * Batched K(rows, cols) blocks (replaces the EntryFn fills of shared_sweep,

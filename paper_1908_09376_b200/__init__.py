@@ -64,6 +64,7 @@ def lib():
         L.midbf_factorize.argtypes = [C.POINTER(vp), C.POINTER(_KernelDesc), i64, i64, C.c_double, i64, u64,
                                       C.c_int, C.c_int]
         L.midbf_apply.argtypes = [vp, vp, vp, i64, C.c_int, vp]
+        L.midbf_apply_async.argtypes = [vp, vp, vp, i64, C.c_int, vp]
         L.midbf_fact_apply.argtypes = [vp, vp, vp, i64, C.c_int, vp]
         L.midbf_plan_set_flags.argtypes = [vp, C.c_uint]
         L.midbf_fact_plan.argtypes = [vp, C.c_uint, C.POINTER(vp)]
@@ -264,6 +265,11 @@ class DevicePlan:
     def apply_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
         """Raw-pointer apply (device or host pointers, cudaStream_t as int)."""
         _check(lib().midbf_apply(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))
+
+    def apply_async_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
+        """Pipelined host-operand apply (midbf_apply_async): returns after
+        enqueueing; synchronize `stream` before reading g / reusing f."""
+        _check(lib().midbf_apply_async(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))
 
     def apply(self, f, transpose=False, out=None, stream=0):
         if hasattr(f, "data_ptr"):  # device tensor

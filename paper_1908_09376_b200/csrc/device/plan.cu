@@ -414,6 +414,20 @@ Plan::~Plan() {
     cudaFree(D.d_sync);
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  if (s_h2d) {
+    cudaStreamSynchronize(s_d2h);
+    for (auto& a : aslots) {
+      cudaFree(a.d_in);
+      cudaFree(a.d_out);
+      cudaEventDestroy(a.in_ready);
+      cudaEventDestroy(a.applied);
+      cudaEventDestroy(a.done);
+    }
+    cudaEventDestroy(ev_user);
+    cudaStreamDestroy(s_h2d);
+    cudaStreamDestroy(s_comp);
+    cudaStreamDestroy(s_d2h);
+  }
   cudaFree(d_prof);
   cudaFree(d_row_perm);
   cudaFree(d_col_perm);
@@ -654,6 +668,53 @@ void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaS
     cuda_check(cudaMemcpyAsync(g, dst, nout * nrhs * sizeof(double2), cudaMemcpyDeviceToHost, stream), "D2H");
     cuda_check(cudaStreamSynchronize(stream), "apply sync");
   }
+}
+
+// Pipelined apply on host operands: H2D on one stream, the apply on another,
+// D2H on a third, rotating through kAsyncSlots device staging slots, so the
+// copies of consecutive calls overlap the previous apply.  Returns after
+// enqueueing; `user` waits for this call's D2H.  f is read asynchronously
+// (host-written input: it is not ordered after work on `user`), so it must
+// not change until `user` is synchronized.
+void Plan::apply_async(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t user) {
+  if (nrhs < 1) throw std::invalid_argument("nrhs must be >= 1");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  const int d = transpose ? 1 : 0;
+  if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
+  const int64_t nin = transpose ? nrows : ncols, nout = transpose ? ncols : nrows;
+  const int64_t need = std::max<int64_t>(1, std::max(nrows, ncols)) * nrhs;
+  if (!s_h2d) {
+    cuda_check(cudaStreamCreateWithFlags(&s_h2d, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&s_d2h, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming), "event");
+    for (auto& a : aslots) {
+      cuda_check(cudaEventCreateWithFlags(&a.in_ready, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&a.applied, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming), "event");
+    }
+  }
+  AsyncSlot& S = aslots[acount++ % kAsyncSlots];
+  if (S.used) cuda_check(cudaStreamWaitEvent(s_h2d, S.done, 0), "slot reuse");
+  if (need > S.elems) {
+    cuda_check(cudaStreamSynchronize(s_d2h), "slot resize");
+    cudaFree(S.d_in);
+    cudaFree(S.d_out);
+    S.d_in = S.d_out = nullptr;
+    cuda_check(cudaMalloc(&S.d_in, need * sizeof(double2)), "cudaMalloc async staging");
+    cuda_check(cudaMalloc(&S.d_out, need * sizeof(double2)), "cudaMalloc async staging");
+    S.elems = need;
+  }
+  cuda_check(cudaMemcpyAsync(S.d_in, f, nin * nrhs * sizeof(double2), cudaMemcpyHostToDevice, s_h2d), "H2D");
+  cuda_check(cudaEventRecord(S.in_ready, s_h2d), "event");
+  cuda_check(cudaStreamWaitEvent(s_comp, S.in_ready, 0), "wait H2D");
+  apply_device(d, S.d_in, S.d_out, nrhs, s_comp);
+  cuda_check(cudaEventRecord(S.applied, s_comp), "event");
+  cuda_check(cudaStreamWaitEvent(s_d2h, S.applied, 0), "wait apply");
+  cuda_check(cudaMemcpyAsync(g, S.d_out, nout * nrhs * sizeof(double2), cudaMemcpyDeviceToHost, s_d2h), "D2H");
+  cuda_check(cudaEventRecord(S.done, s_d2h), "event");
+  cuda_check(cudaStreamWaitEvent(user, S.done, 0), "signal user");
+  S.used = true;
 }
 
 }  // namespace midbf::dev

@@ -70,6 +70,14 @@ struct Direction {
   int64_t in_len = 0;  // input length of the first stage (head of the stage buffers)
 };
 
+struct AsyncSlot {  // device staging of one in-flight host-operand apply
+  double2* d_in = nullptr;
+  double2* d_out = nullptr;
+  int64_t elems = 0;
+  bool used = false;
+  cudaEvent_t in_ready = nullptr, applied = nullptr, done = nullptr;
+};
+
 struct GraphEntry {
   int d;
   const double2* in;
@@ -89,6 +97,8 @@ class Plan {
   // f, g: host or device, column-major N x nrhs complex.
   void apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t stream);
   void apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+  // host f/g, enqueue only; `stream` waits for completion (midbf_apply_async)
+  void apply_async(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t stream);
 
   int device = 0;
   int num_sms = 0;
@@ -122,6 +132,11 @@ class Plan {
   int64_t buf_elems = 0;
   double2* d_io[2] = {nullptr, nullptr};
   int64_t io_elems = 0;
+  static constexpr int kAsyncSlots = 3;
+  AsyncSlot aslots[kAsyncSlots];
+  int64_t acount = 0;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_user = nullptr;
 };
 
 std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions);

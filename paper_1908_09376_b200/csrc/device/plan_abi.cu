@@ -227,6 +227,14 @@ extern "C" int midbf_apply(midbf_plan_t plan, const double* f, double* g, int64_
   });
 }
 
+extern "C" int midbf_apply_async(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose,
+                                 void* stream) {
+  return guard([&] {
+    if (!plan || !f || !g) throw std::invalid_argument("null argument");
+    plan->p->apply_async(f, g, nrhs, transpose != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
 // Stage table for benchmarks / roofline accounting:
 // out[s*4 + 0..3] = strips, payload bytes, in_len, out_len of stage s.
 extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap) {

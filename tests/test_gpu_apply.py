@@ -132,3 +132,23 @@ def test_device_pointer_operands(gpu):
     plan.apply(fd, out=gd, stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert rel(gd.cpu().numpy(), Fo.apply(f)) <= TOL
+
+
+def test_pipelined_host_apply(gpu):
+    """midbf_apply_async: several calls in flight on rotating pinned buffers
+    return exactly what the blocking apply returns."""
+    torch = pytest.importorskip("torch")
+    X = O.grid2d(32)
+    K, Fo = oracle_factorization(O.KIND_FIO2D, X, X, 64, 30, 1e-9)
+    path = saved(Fo)
+    plan = M.DevicePlan.load(path, directions=3)
+    os.unlink(path)
+    ins = [torch.from_numpy(cvec(1024, 60 + i)).pin_memory() for i in range(5)]
+    outs = [torch.empty(1024, dtype=torch.complex128).pin_memory() for _ in range(5)]
+    stream = torch.cuda.current_stream()
+    for fi, go in zip(ins, outs):
+        plan.apply_async_ptr(fi.data_ptr(), go.data_ptr(), 1, False, stream.cuda_stream)
+    stream.synchronize()
+    for fi, go in zip(ins, outs):
+        assert np.array_equal(go.numpy(), plan.apply(fi.numpy()))
+        assert rel(go.numpy(), Fo.apply(fi.numpy())) <= TOL
