@@ -10,13 +10,16 @@
 // measured at 36.8 TFLOP/s on this B200 (tools/fp64_probe.cu).
 //
 // CTA = one strip x 64 right-hand sides, 8 warps (8 rows x 32 RHS each).
-// A complex MAC is four real
-// DMMAs (re*re, -im*im, re*im, im*re) into separate re/im accumulators.
-// Operands move global -> shared with cp.async (16 B per complex entry) in
-// 32-column K chunks, double-buffered; the shared layouts are padded so
-// every fragment load is bank-conflict free: panel column stride 34
-// complex, X row stride 66 complex (stride/16B == 2 mod 8 puts the 8 lanes
-// of a quarter-warp phase on distinct bank groups).
+// A complex MAC is four real DMMAs (re*re, -im*im, re*im, im*re) into
+// separate re/im accumulators.  The strip's panels are walked as ONE
+// concatenated K dimension (sum of panel widths, panel order kept) in
+// 16-column chunks through a 4-deep cp.async ring with one barrier per
+// chunk; panel chunks (plan constants) are prefetched before the PDL wait
+// on the previous stage.  Shared layouts are padded so every fragment load
+// is bank-conflict free: panel column stride 34 complex, X row stride 66
+// complex (stride/16B == 2 mod 8 puts the 8 lanes of a quarter-warp phase
+// on distinct bank groups).  Up to kK2MaxSeg panel records per strip are
+// held one per lane.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,12 +31,14 @@
 namespace midbf::dev {
 
 constexpr int kK2Rhs = 64;    // right-hand sides per CTA tile
-constexpr int kK2Kc = 32;     // K (panel columns) per staged chunk
+constexpr int kK2Kc = 16;     // K (panel columns) per staged chunk
+constexpr int kK2Stages = 4;  // cp.async ring depth
+constexpr int kK2MaxSeg = 32; // panel records per strip (one per lane)
 constexpr int kK2Ps = 34;     // padded panel column stride (complex)
 constexpr int kK2Xs = 66;     // padded X row stride (complex)
 constexpr int kK2PBuf = kK2Kc * kK2Ps;   // complex per panel buffer
 constexpr int kK2XBuf = kK2Kc * kK2Xs;   // complex per X buffer
-constexpr size_t kK2Smem = size_t(2) * (kK2PBuf + kK2XBuf) * 16;
+constexpr size_t kK2Smem = size_t(kK2Stages) * (kK2PBuf + kK2XBuf) * 16;
 
 namespace k2dev {
 
@@ -48,10 +53,11 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// pure register op: not volatile, so ptxas schedules it freely
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 }  // namespace k2dev
@@ -68,8 +74,8 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_stage(const Strip* __restric
                                                        int64_t yld, const int* __restrict__ yperm, int nrhs) {
   using namespace k2dev;
   extern __shared__ __align__(16) double2 k2smem[];
-  double2* const Pb = k2smem;                // 2 panel buffers
-  double2* const Xb = k2smem + 2 * kK2PBuf;  // 2 X buffers
+  double2* const Pb = k2smem;                        // kK2Stages panel buffers
+  double2* const Xb = k2smem + kK2Stages * kK2PBuf;  // kK2Stages X buffers
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int rb = w & 3, ch = w >> 2;  // row block, RHS half
@@ -77,8 +83,84 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_stage(const Strip* __restric
   const int h = st.h;
   const int c0 = blockIdx.y * kK2Rhs;      // first RHS of this tile
   const int ncv = min(kK2Rhs, nrhs - c0);  // valid RHS in the tile
+  const int K = st.xcols;
+  const int nq = (K + kK2Kc - 1) / kK2Kc;  // chunks
+
+  // lane l holds panel l: arena offset, first input entry, start in K
+  int64_t s_off = 0;
+  int s_x0 = 0, s_n = 0;
+  if (lane < st.nseg) {
+    const Seg sg = segs[st.seg0 + lane];
+    s_off = sg.off;
+    s_x0 = sg.x0;
+    s_n = sg.n;
+  }
+  int s_k0 = s_n;  // inclusive -> exclusive prefix of the panel widths
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, s_k0, o);
+    if (lane >= o) s_k0 += v;
+  }
+  s_k0 -= s_n;
+
+  // K column kg -> (panel, column within it); every lane resolves column
+  // q*16 + (lane & 15).
+  auto locate = [&](int q, int& seg, int& cc) {
+    const int kg = q * kK2Kc + (lane & (kK2Kc - 1));
+    int sidx = 0;
+    for (int l = 1; l < st.nseg; ++l) sidx += __shfl_sync(0xffffffffu, s_k0, l) <= kg;
+    seg = sidx;
+    cc = kg - __shfl_sync(0xffffffffu, s_k0, sidx);
+    return kg < K;
+  };
+  // panel chunk q -> buffer b: warp w copies columns 2w, 2w+1 (lane = row)
+  auto issue_p = [&](int q, int b) {
+    int seg, cc;
+    const bool ok = locate(q, seg, cc);
+    const int64_t src = __shfl_sync(0xffffffffu, s_off, seg) + static_cast<int64_t>(cc) * h;
+    double2* pd = Pb + b * kK2PBuf;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int col = 2 * w + i;
+      const int64_t cs = __shfl_sync(0xffffffffu, src, col);
+      const bool cok = __shfl_sync(0xffffffffu, ok, col);
+      if (cok) {
+        if (lane < h) cp_async16(pd + col * kK2Ps + lane, arena + cs + lane);
+      } else {
+        pd[col * kK2Ps + lane] = make_double2(0, 0);  // K tail
+      }
+    }
+  };
+  // X chunk q -> buffer b: lane&15 = k, RHS = 16*it + 2w + (lane >> 4)
+  auto issue_x = [&](int q, int b) {
+    int seg, cc;
+    const bool ok = locate(q, seg, cc);
+    int xi = __shfl_sync(0xffffffffu, s_x0, seg) + cc;
+    if (ok && xperm) xi = __ldg(xperm + xi);
+    double2* xd = Xb + b * kK2XBuf + (lane & (kK2Kc - 1)) * kK2Xs;
+#pragma unroll
+    for (int it = 0; it < kK2Rhs / 16; ++it) {
+      const int rhs = 16 * it + 2 * w + (lane >> 4);
+      if (ok) {
+        if (rhs < ncv) cp_async16(xd + rhs, x + static_cast<int64_t>(c0 + rhs) * xld + xi);
+      } else {
+        xd[rhs] = make_double2(0, 0);  // K tail
+      }
+    }
+  };
+
+  // prologue: panel chunks need no predecessor; X chunks wait for it.
+  // Rows >= h and RHS >= ncv of the buffers are never written: they only
+  // feed output rows / RHS that are not stored.
+  for (int q = 0; q < kK2Stages - 1; ++q)
+    if (q < nq) issue_p(q, q);
+  cp_async_commit();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // previous stage's output
   asm volatile("griddepcontrol.launch_dependents;" :::);
+  for (int q = 0; q < kK2Stages - 1; ++q) {
+    if (q < nq) issue_x(q, q);
+    cp_async_commit();
+  }
 
   double acc[4][2][2];  // [col block][re, im][2 entries]
 #pragma unroll
@@ -86,80 +168,36 @@ __global__ void __launch_bounds__(kK2Threads, 2) k2_stage(const Strip* __restric
 #pragma unroll
     for (int r = 0; r < 2; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
 
-  // Zero both buffers once: rows >= h, RHS >= ncv and K tails of short
-  // chunks stay zero (tails are re-zeroed per chunk below), so the inner
-  // loop needs no masking.
-  for (int i = tid; i < 2 * (kK2PBuf + kK2XBuf); i += kK2Threads) k2smem[i] = make_double2(0, 0);
-  __syncthreads();
-
-  // chunk enumeration over the strip's panels: (seg j, column c)
-  int j = 0, c = 0;
-  auto stage = [&](int jj, int cc, int buf) {
-    const Seg s = segs[st.seg0 + jj];
-    const int kc = min(kK2Kc, s.n - cc);
-    const double2* P = arena + s.off + static_cast<int64_t>(cc) * h;
-    double2* pd = Pb + buf * kK2PBuf;
-    double2* xd = Xb + buf * kK2XBuf;
-    for (int col = w; col < kK2Kc; col += kK2Threads / 32) {  // panel columns (lane = row)
-      if (lane < h) {
-        if (col < kc)
-          cp_async16(pd + col * kK2Ps + lane, P + col * h + lane);
-        else
-          pd[col * kK2Ps + lane] = make_double2(0, 0);
-      }
-    }
-    for (int rhs = w; rhs < ncv; rhs += kK2Threads / 32) {  // X rows x0+cc .. (lane = k)
-      const double2* xc = x + static_cast<int64_t>(c0 + rhs) * xld;
-      const int k = lane;
-      if (k < kc) {
-        int idx = s.x0 + cc + k;
-        if (xperm) idx = __ldg(xperm + idx);
-        cp_async16(xd + k * kK2Xs + rhs, xc + idx);
-      } else {
-        xd[k * kK2Xs + rhs] = make_double2(0, 0);
-      }
+  for (int q = 0; q < nq; ++q) {
+    cp_async_wait<kK2Stages - 2>();  // chunk q landed (this thread's copies)
+    __syncthreads();                 // ... everyone's; buffer (q-1) is free
+    const int qn = q + kK2Stages - 1;
+    if (qn < nq) {
+      issue_p(qn, qn % kK2Stages);
+      issue_x(qn, qn % kK2Stages);
     }
     cp_async_commit();
-    return kc;
-  };
-  if (st.nseg > 0) {
-    int kc_cur = stage(0, 0, 0);
-    int buf = 0;
-    while (true) {
-      int jn = j, cn = c + kc_cur;
-      if (cn >= segs[st.seg0 + jn].n) {
-        ++jn;
-        cn = 0;
-      }
-      const bool more = jn < st.nseg;
-      int kc_next = 0;
-      if (more) kc_next = stage(jn, cn, buf ^ 1);
-      if (more)
-        cp_async_wait<1>();
-      else
-        cp_async_wait<0>();
-      __syncthreads();
-      const double2* Ps = Pb + buf * kK2PBuf;
-      const double2* Xs = Xb + buf * kK2XBuf + ch * 32;
-      const int kend = (kc_cur + 3) & ~3;
-      for (int kk = 0; kk < kend; kk += 4) {
-        const double2 a = Ps[(kk + t) * kK2Ps + 8 * rb + g];
-        const double naim = -a.y;
+    const int b = q % kK2Stages;
+    const double2* Ps = Pb + b * kK2PBuf;
+    const double2* Xs = Xb + b * kK2XBuf + ch * 32;
+    const int kend = q + 1 < nq ? kK2Kc : ((K - q * kK2Kc + 3) & ~3);
+#pragma unroll 4
+    for (int kk = 0; kk < kend; kk += 4) {
+      const double2 a = Ps[(kk + t) * kK2Ps + 8 * rb + g];
+      const double naim = -a.y;
+      double2 bv[4];
 #pragma unroll
-        for (int cb = 0; cb < 4; ++cb) {
-          const double2 b = Xs[(kk + t) * kK2Xs + cb * 8 + g];
-          dmma(acc[cb][0][0], acc[cb][0][1], a.x, b.x);
-          dmma(acc[cb][0][0], acc[cb][0][1], naim, b.y);
-          dmma(acc[cb][1][0], acc[cb][1][1], a.x, b.y);
-          dmma(acc[cb][1][0], acc[cb][1][1], a.y, b.x);
-        }
+      for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[(kk + t) * kK2Xs + cb * 8 + g];
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
+        dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
       }
-      __syncthreads();
-      if (!more) break;
-      j = jn;
-      c = cn;
-      kc_cur = kc_next;
-      buf ^= 1;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
+        dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
+      }
     }
   }
   // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}

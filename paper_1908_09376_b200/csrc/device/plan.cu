@@ -443,7 +443,7 @@ bool Plan::flow_ok(int d, int64_t nrhs) const {
 
 int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
   if (flow_ok(d, nrhs)) return 1;
-  if (k2_ok(nrhs)) {
+  if (k2_ok(d, nrhs)) {
     int64_t n = 0;
     for (const auto& st : dir[d].stages) n += st.nstrips > 0;
     return n;
@@ -569,12 +569,14 @@ void Plan::launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaS
   }
 }
 
-bool Plan::k2_ok(int64_t nrhs) const { return nrhs > 1 && !(flags & 2048u); }
+bool Plan::k2_ok(int d, int64_t nrhs) const {
+  return nrhs > 1 && !(flags & 2048u) && dir[d].max_seg <= kK2MaxSeg;
+}
 
 void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   if (flow_ok(d, nrhs))
     launch_flow(d, in, out, stream);
-  else if (k2_ok(nrhs))
+  else if (k2_ok(d, nrhs))
     launch_k2(d, in, out, nrhs, stream);
   else
     launch_stages(d, in, out, nrhs, stream);

@@ -115,7 +115,7 @@ class Plan {
   long long* d_prof = nullptr;  // k1_flow phase timers (flag bit 12)
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
-  bool k2_ok(int64_t nrhs) const;
+  bool k2_ok(int d, int64_t nrhs) const;
   int last_grid[2] = {-1, -1};
   void prepare_flow(int d);
 
