@@ -245,10 +245,13 @@ class DevicePlan:
             lib().midbf_plan_destroy(self._h)
             self._h = None
 
-    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True):
+    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
-        RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs."""
+        RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
+        multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
+        64-RHS slice (dmma_flow) or one launch per stage."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
+        f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192)
         _check(lib().midbf_plan_set_flags(self._h, f))
 
     def launches(self, nrhs=1, transpose=False):

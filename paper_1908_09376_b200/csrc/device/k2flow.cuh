@@ -1,0 +1,255 @@
+// K2-flow — the multi-RHS MIDBF apply as ONE persistent dataflow launch per
+// 64-RHS slice, on the FP64 tensor cores (DMMA), sm_100a.
+//
+// Same arithmetic as k2_stage (k2.cuh) — per strip, Y(rows, 64 RHS) = sum
+// over its panels P (h x n) * X(x0 .. x0+n, :), the panels walked as one
+// concatenated K dimension in 16-column chunks — with every stage in one
+// cooperative launch, which removes the per-stage launch gaps and the
+// per-stage wave tails (cfg4: 1024 strips per stage on 296 CTA slots is
+// 3.46 waves).  Reference: apply_factor's GEMM path for x.cols() > 1
+// (src/butterfly.cpp:633-637 with bf::apply(F, MatXc), :779).
+//
+// CTA = 8 consumer warps + 1 producer warp, 2 CTAs per SM.
+//   * Producer: walks this CTA's strips (global strip list, stage-major,
+//     dealt round-robin over the grid), and streams each strip's chunks
+//     (panel: 16 columns x h rows; X: 16 rows x 64 RHS) into a 4-slot shared
+//     ring with cp.async, completion signalled by
+//     cp.async.mbarrier.arrive.noinc on the slot's `full` barrier.  Before
+//     the first X chunk of a strip it acquires the completion counters of
+//     the previous-stage strips that produce its input rows (Seg::dep0/dep1).
+//   * Consumers: LDS + DMMA only (8 rows x 32 RHS per warp, as in k2_stage);
+//     release the slot on its `empty` barrier; at the end of a strip store
+//     the 32 x 64 tile and add 1 (release, gpu scope) to the strip's counter.
+//   * Per-CTA apply epochs (all CTAs run every launch): a strip of launch e
+//     is complete when its counter reaches 8 e.
+// Deadlock freedom: CTAs are co-resident (cooperative launch) and each
+// walks its strips in increasing global order; the smallest incomplete strip
+// has all its inputs complete, and its CTA's producer has reached it.
+// Stages overlap, so every stage but the last writes its own buffer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "flow.cuh"
+#include "k2.cuh"
+#include "plan.hpp"
+
+namespace midbf::dev {
+
+constexpr int kK2FConsumers = 8;                      // consumer warps
+constexpr int kK2FThreads = (kK2FConsumers + 1) * 32;  // + one producer warp
+constexpr int kK2FSlots = 4;                           // ring depth
+constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FSlots * (16 + 16);
+
+struct K2FStage {
+  const double2* x;  // input (stage 0: user operand, gathered through xperm)
+  double2* y;        // output (last stage: user operand, scattered through yperm)
+  int64_t xld, yld;
+  const int* xperm;
+  const int* yperm;
+};
+
+struct K2FParams {
+  const Strip* strips;  // all stages, application order
+  const Seg* segs;
+  const double2* arena;
+  unsigned* done;   // per strip: consumer-warp completions, all launches
+  unsigned* epoch;  // per CTA: launches completed
+  int nstrips;
+  int nstages;
+  int ncv;  // valid RHS of this slice (<= 64)
+  K2FStage st[kMaxStages];
+};
+
+namespace k2fdev {
+
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(flowdev::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+}  // namespace k2fdev
+
+__global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant__ K2FParams P) {
+  using namespace k2dev;
+  using namespace k2fdev;
+  using flowdev::mbar_arrive;
+  using flowdev::mbar_init;
+  using flowdev::mbar_wait;
+  extern __shared__ __align__(16) double2 k2smem[];
+  double2* const Pb = k2smem;                        // kK2FSlots panel buffers
+  double2* const Xb = k2smem + kK2FSlots * kK2PBuf;  // kK2FSlots X buffers
+  uint64_t* const full = reinterpret_cast<uint64_t*>(Xb + kK2FSlots * kK2XBuf);
+  uint64_t* const empty = full + kK2FSlots;
+  int4* const meta = reinterpret_cast<int4*>(empty + kK2FSlots);  // per slot: {y0, h, stage, K}
+  __shared__ unsigned s_epoch;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) {
+    for (int i = 0; i < kK2FSlots; ++i) {
+      mbar_init(&full[i], 33);  // 32 cp.async arrivals + the meta writer
+      mbar_init(&empty[i], kK2FConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_epoch = P.epoch[blockIdx.x] + 1;
+  }
+  __syncthreads();
+  const unsigned target = s_epoch * kK2FConsumers;
+
+  if (w == kK2FConsumers) {
+    // ------------------------------ producer -------------------------------
+    int gc = 0;  // chunks issued
+    for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
+      const Strip st = P.strips[item];
+      const K2FStage io = P.st[st.stage];
+      int64_t s_off = 0;
+      int s_x0 = 0, s_n = 0, s_d0 = 0, s_d1 = 0;
+      if (lane < st.nseg) {
+        const Seg sg = P.segs[st.seg0 + lane];
+        s_off = sg.off, s_x0 = sg.x0, s_n = sg.n, s_d0 = sg.dep0, s_d1 = sg.dep1;
+      }
+      int s_k0 = s_n;  // exclusive prefix of the panel widths
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, s_k0, o);
+        if (lane >= o) s_k0 += v;
+      }
+      s_k0 -= s_n;
+      const int K = st.xcols, h = st.h;
+      const int nq = K > 0 ? (K + kK2Kc - 1) / kK2Kc : 1;
+      bool deps = st.stage == 0;
+      for (int q = 0; q < nq; ++q, ++gc) {
+        const int slot = gc % kK2FSlots, use = gc / kK2FSlots;
+        if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
+        // lane resolves K column q*16 + (lane & 15)
+        const int kg = q * kK2Kc + (lane & (kK2Kc - 1));
+        int sidx = 0;
+        for (int l = 1; l < st.nseg; ++l) sidx += __shfl_sync(0xffffffffu, s_k0, l) <= kg;
+        const int cc = kg - __shfl_sync(0xffffffffu, s_k0, sidx);
+        const bool ok = kg < K;
+        // panel: lane = row, 16 columns
+        {
+          const int64_t src = __shfl_sync(0xffffffffu, s_off, sidx) + static_cast<int64_t>(cc) * h;
+          double2* pd = Pb + slot * kK2PBuf + lane;
+#pragma unroll 4
+          for (int col = 0; col < kK2Kc; ++col) {
+            const int64_t cs = __shfl_sync(0xffffffffu, src, col);
+            const bool cok = __shfl_sync(0xffffffffu, ok, col);
+            if (cok && lane < h) cp_async16(pd + col * kK2Ps, P.arena + cs + lane);
+          }
+        }
+        if (!deps) {  // previous-stage producers of this strip's input rows
+          for (int l = 0; l < st.nseg; ++l) {
+            const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
+            for (int s = d0 + lane; s < d1; s += 32)
+              while (ld_acquire(P.done + s) < target) __nanosleep(64);
+          }
+          __syncwarp();
+          deps = true;
+        }
+        // X: lane & 15 = k, RHS pair (lane >> 4) + 2 it
+        int xi = __shfl_sync(0xffffffffu, s_x0, sidx) + cc;  // all lanes: full-mask shuffle
+        if (ok) {
+          if (io.xperm) xi = __ldg(io.xperm + xi);
+          const double2* xs = io.x + xi;
+          double2* xd = Xb + slot * kK2XBuf + (lane & (kK2Kc - 1)) * kK2Xs;
+#pragma unroll 4
+          for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xd + rhs, xs + rhs * io.xld);
+        }
+        if (lane == 0) meta[slot] = make_int4(st.y0, h, st.stage, K);
+        cp_async_arrive_noinc(&full[slot]);
+        if (lane == 0) mbar_arrive(&full[slot]);
+      }
+    }
+  } else {
+    // ------------------------------ consumers ------------------------------
+    const int g = lane >> 2, t = lane & 3;
+    const int rb = w & 3, ch = w >> 2;  // row block, RHS half
+    const int row = 8 * rb + g;
+    int gc = 0;
+    for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
+      double acc[4][2][2];
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
+      int4 m = make_int4(0, 0, 0, 0);
+      int nq = 1;
+      for (int q = 0; q < nq; ++q, ++gc) {
+        const int slot = gc % kK2FSlots;
+        mbar_wait(&full[slot], (gc / kK2FSlots) & 1);
+        if (q == 0) {
+          m = meta[slot];
+          nq = m.w > 0 ? (m.w + kK2Kc - 1) / kK2Kc : 1;
+        }
+        const int krem = min(kK2Kc, m.w - q * kK2Kc);
+        const int kfull = krem & ~3;
+        const double2* Ps = Pb + slot * kK2PBuf + 8 * rb + g;
+        const double2* Xs = Xb + slot * kK2XBuf + ch * 32 + g;
+        auto step = [&](int kk, bool live) {
+          double2 a = Ps[(kk + t) * kK2Ps];
+          double2 bv[4];
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[(kk + t) * kK2Xs + cb * 8];
+          if (!live) {  // K tail: stale slot contents must not reach the sums
+            a = make_double2(0, 0);
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) bv[cb] = make_double2(0, 0);
+          }
+          const double naim = -a.y;
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
+            dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
+          }
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
+            dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
+          }
+        };
+        if (kfull == kK2Kc) {
+#pragma unroll
+          for (int kk = 0; kk < kK2Kc; kk += 4) step(kk, true);
+        } else {
+          for (int kk = 0; kk < kfull; kk += 4) step(kk, true);
+          if (kfull < krem) step(kfull, t < krem - kfull);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+      // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}
+      const K2FStage io = P.st[m.z];
+      if (row < m.y) {
+        int idx = m.x + row;
+        if (io.yperm) idx = __ldg(io.yperm + idx);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int rhs = 32 * ch + cb * 8 + 2 * t + i;
+            if (rhs < P.ncv) io.y[rhs * io.yld + idx] = make_double2(acc[cb][0][i], acc[cb][1][i]);
+          }
+      }
+      if (m.z + 1 < P.nstages) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          red_release_add(P.done + item, 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) P.epoch[blockIdx.x] = s_epoch;
+}
+
+}  // namespace midbf::dev

@@ -45,6 +45,7 @@
 #include "plan.hpp"
 #include "flow.cuh"
 #include "k2.cuh"
+#include "k2flow.cuh"
 
 namespace midbf::dev {
 
@@ -402,6 +403,11 @@ Plan::Plan(const PlanTables& T, unsigned directions) {
   flow_grid[3] = flow_grid[0];
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
+  cuda_check(cudaFuncSetAttribute(k2_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2FSmem)),
+             "k2_flow smem attribute");
+  int per_sm = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_flow, kK2FThreads, kK2FSmem), "occupancy");
+  k2flow_grid = std::min(per_sm * num_sms, kMaxFlowCtas);  // 0: k2_flow unavailable
 }
 
 Plan::~Plan() {
@@ -410,6 +416,9 @@ Plan::~Plan() {
     cudaFree(D.d_segs);
     cudaFree(D.d_arena);
     cudaFree(D.d_ctx);
+    cudaFree(D.d_k2buf);
+    cudaFree(D.d_k2done);
+    cudaFree(D.d_k2epoch);
     cudaFree(D.d_stagebuf);
     cudaFree(D.d_sync);
   }
@@ -443,6 +452,7 @@ bool Plan::flow_ok(int d, int64_t nrhs) const {
 
 int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
   if (flow_ok(d, nrhs)) return 1;
+  if (k2flow_ok(d, nrhs)) return (nrhs + kK2Rhs - 1) / kK2Rhs;
   if (k2_ok(d, nrhs)) {
     int64_t n = 0;
     for (const auto& st : dir[d].stages) n += st.nstrips > 0;
@@ -569,6 +579,75 @@ void Plan::launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaS
   }
 }
 
+bool Plan::k2flow_ok(int d, int64_t nrhs) const {
+  return k2_ok(d, nrhs) && !(flags & 8192u) && k2flow_grid > 0;
+}
+
+void Plan::ensure_k2flow(int d) {
+  Direction& D = dir[d];
+  if (D.d_k2done) return;
+  int64_t rows = 0;
+  for (size_t s = 0; s + 1 < D.stages.size(); ++s) rows += D.stages[s].out_len;
+  cuda_check(cudaMalloc(&D.d_k2buf, std::max<int64_t>(rows, 1) * kK2Rhs * sizeof(double2)), "cudaMalloc k2 stages");
+  cuda_check(cudaMalloc(&D.d_k2done, std::max<int64_t>(D.nstrips, 1) * sizeof(unsigned)), "cudaMalloc k2 counters");
+  cuda_check(cudaMalloc(&D.d_k2epoch, kMaxFlowCtas * sizeof(unsigned)), "cudaMalloc k2 epochs");
+  cuda_check(cudaMemset(D.d_k2done, 0, std::max<int64_t>(D.nstrips, 1) * sizeof(unsigned)), "reset k2 counters");
+  cuda_check(cudaMemset(D.d_k2epoch, 0, kMaxFlowCtas * sizeof(unsigned)), "reset k2 epochs");
+}
+
+// K2-flow: one cooperative dataflow launch per 64-RHS slice (k2flow.cuh).
+void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
+  const Direction& D = dir[d];
+  const int ns = static_cast<int>(D.stages.size());
+  const int64_t in_ld = d == 0 ? ncols : nrows, out_ld = d == 0 ? nrows : ncols;
+  K2FParams P{};
+  P.strips = D.d_strips;
+  P.segs = D.d_segs;
+  P.arena = D.d_arena;
+  P.done = D.d_k2done;
+  P.epoch = D.d_k2epoch;
+  P.nstrips = static_cast<int>(D.nstrips);
+  P.nstages = ns;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(k2flow_grid), 1, 1);
+  cfg.blockDim = dim3(kK2FThreads, 1, 1);
+  cfg.dynamicSmemBytes = kK2FSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's strips
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  for (int64_t c0 = 0; c0 < nrhs; c0 += kK2Rhs) {
+    P.ncv = static_cast<int>(std::min<int64_t>(kK2Rhs, nrhs - c0));
+    int64_t off = 0;
+    for (int s = 0; s < ns; ++s) {
+      K2FStage& io = P.st[s];
+      const int64_t len = D.stages[static_cast<size_t>(s)].out_len;
+      if (s == 0) {
+        io.x = in + c0 * in_ld;
+        io.xld = in_ld;
+        io.xperm = d == 0 ? d_col_perm : d_row_perm;
+      } else {
+        io.x = P.st[s - 1].y;
+        io.xld = P.st[s - 1].yld;
+        io.xperm = nullptr;
+      }
+      if (s == ns - 1) {
+        io.y = out + c0 * out_ld;
+        io.yld = out_ld;
+        io.yperm = d == 0 ? d_row_perm : d_col_perm;
+      } else {
+        io.y = D.d_k2buf + off * kK2Rhs;
+        io.yld = len;
+        io.yperm = nullptr;
+        off += len;
+      }
+    }
+    cuda_check(cudaLaunchKernelEx(&cfg, k2_flow, P), "k2_flow launch");
+  }
+}
+
 bool Plan::k2_ok(int d, int64_t nrhs) const {
   return nrhs > 1 && !(flags & 2048u) && dir[d].max_seg <= kK2MaxSeg;
 }
@@ -576,6 +655,8 @@ bool Plan::k2_ok(int d, int64_t nrhs) const {
 void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   if (flow_ok(d, nrhs))
     launch_flow(d, in, out, stream);
+  else if (k2flow_ok(d, nrhs))
+    launch_k2flow(d, in, out, nrhs, stream);
   else if (k2_ok(d, nrhs))
     launch_k2(d, in, out, nrhs, stream);
   else
@@ -602,6 +683,7 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
   ensure_buffers(nrhs);
   if (flow_ok(d, nrhs)) prepare_flow(d);
   if (dir[d].stages.empty()) return;
+  if (k2flow_ok(d, nrhs)) ensure_k2flow(d);
   if (!(flags & 4u)) {
     launch(d, in, out, nrhs, stream);
     cuda_check(cudaGetLastError(), "apply");

@@ -68,6 +68,11 @@ struct Direction {
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
   int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
   int64_t in_len = 0;  // input length of the first stage (head of the stage buffers)
+  // k2_flow (multi-RHS dataflow): per-stage outputs for one 64-RHS slice,
+  // per-strip completion counters, per-CTA launch epochs; allocated on first use
+  double2* d_k2buf = nullptr;
+  unsigned* d_k2done = nullptr;
+  unsigned* d_k2epoch = nullptr;
 };
 
 struct AsyncSlot {  // device staging of one in-flight host-operand apply
@@ -107,7 +112,8 @@ class Plan {
   // bit0 PDL + bit1 L2 prefetch (stage kernels), bit2 CUDA graphs,
   // bit3 persistent dataflow kernel for single-RHS applies,
   // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size),
-  // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS).
+  // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS),
+  // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel.
   unsigned flags = 0xF;  // default: k1_flow variant 0 (4 pairs x 3 x 16 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
@@ -116,6 +122,8 @@ class Plan {
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
   bool k2_ok(int d, int64_t nrhs) const;
+  bool k2flow_ok(int d, int64_t nrhs) const;
+  int k2flow_grid = 0;
   int last_grid[2] = {-1, -1};
   void prepare_flow(int d);
 
@@ -126,6 +134,8 @@ class Plan {
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_flow(int d, const double2* in, double2* out, cudaStream_t stream);
   void launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+  void launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
+  void ensure_k2flow(int d);
   int* d_row_perm = nullptr;
   int* d_col_perm = nullptr;
   double2* d_buf[2] = {nullptr, nullptr};

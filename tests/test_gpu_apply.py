@@ -62,6 +62,28 @@ def test_dmma_multi_rhs_matches_oracle(pair, nrhs):
     assert rel(plan.apply(Y, transpose=True), Fo.apply_transpose(Y)) <= TOL
 
 
+@pytest.mark.parametrize("path", ["k2_stage", "k1_stage"])
+def test_multi_rhs_fallback_paths(pair, path):
+    """Per-stage DMMA launches (flag bit 13) and the per-stage FMA kernels
+    (bit 11) give the same result as the dataflow default."""
+    name, K, Fo, Fm, plan = pair
+    X = cvec(Fo.ncols, 18, cols=67)
+    want = Fo.apply(X)
+    default = plan.apply(X)
+    try:
+        if path == "k2_stage":
+            plan.set_flags(dmma_flow=False)
+            assert plan.launches(67) == Fo.nfactors  # one DMMA launch per stage
+        else:
+            plan.set_flags(dmma=False)
+        got = plan.apply(X)
+    finally:
+        plan.set_flags()
+    assert plan.launches(67) == 2  # k2_flow: one launch per 64-RHS slice
+    assert rel(got, want) <= TOL
+    assert rel(default, want) <= TOL
+
+
 def test_runs_are_bitwise_identical(pair):
     name, K, Fo, Fm, plan = pair
     f = cvec(Fo.ncols, 14)
