@@ -13,15 +13,20 @@
 //   * Producer: walks this CTA's strips (global strip list, stage-major,
 //     dealt round-robin over the grid), and streams each strip's chunks
 //     (panel: 16 columns x h rows; X: 16 rows x 64 RHS) into a 4-slot shared
-//     ring with cp.async, completion signalled by
-//     cp.async.mbarrier.arrive.noinc on the slot's `full` barrier.  Before
-//     the first X chunk of a strip it acquires the completion counters of
-//     the previous-stage strips that produce its input rows (Seg::dep0/dep1).
+//     ring with TMA bulk copies (cp.async.bulk, complete_tx on the slot's
+//     `full` barrier): one copy per panel column (h x 16 B) and one per input
+//     row (64 x 16 B: intermediate stage buffers are row-major, RHS fastest),
+//     16 lanes issuing in parallel, into the padded layouts of k2_stage.
+//     Stage 0 gathers its input rows (user operand, column-major) through
+//     the column permutation with cp.async (cp.async.mbarrier.arrive.noinc).  Before the
+//     first X chunk of a strip it acquires the completion counters of the
+//     previous-stage strips that produce its input rows (Seg::dep0/dep1).
 //   * Consumers: LDS + DMMA only (8 rows x 32 RHS per warp, as in k2_stage);
 //     release the slot on its `empty` barrier; at the end of a strip store
-//     the 32 x 64 tile and add 1 (release, gpu scope) to the strip's counter.
+//     the 32 x 64 tile; after a consumer barrier one thread adds 1 (release,
+//     gpu scope) to the strip's counter.
 //   * Per-CTA apply epochs (all CTAs run every launch): a strip of launch e
-//     is complete when its counter reaches 8 e.
+//     is complete when its counter reaches e.
 // Deadlock freedom: CTAs are co-resident (cooperative launch) and each
 // walks its strips in increasing global order; the smallest incomplete strip
 // has all its inputs complete, and its CTA's producer has reached it.
@@ -46,7 +51,7 @@ constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FS
 struct K2FStage {
   const double2* x;  // input (stage 0: user operand, gathered through xperm)
   double2* y;        // output (last stage: user operand, scattered through yperm)
-  int64_t xld, yld;
+  int64_t xld, yld;  // user operands: column-major ld; stage buffers: row-major, ld 64
   const int* xperm;
   const int* yperm;
 };
@@ -55,11 +60,14 @@ struct K2FParams {
   const Strip* strips;  // all stages, application order
   const Seg* segs;
   const double2* arena;
-  unsigned* done;   // per strip: consumer-warp completions, all launches
+  unsigned* done;   // per strip: completions over all launches
   unsigned* epoch;  // per CTA: launches completed
   int nstrips;
   int nstages;
-  int ncv;  // valid RHS of this slice (<= 64)
+  int ncv;     // valid RHS of this slice (<= 64)
+  // timing experiments only (flag bits 14-15), results invalid: 1 skip the
+  // dependency waits, 2 stream only (no math), 3 math only (no loads)
+  int mode;
   K2FStage st[kMaxStages];
 };
 
@@ -102,7 +110,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
     s_epoch = P.epoch[blockIdx.x] + 1;
   }
   __syncthreads();
-  const unsigned target = s_epoch * kK2FConsumers;
+  const unsigned target = s_epoch;
 
   if (w == kK2FConsumers) {
     // ------------------------------ producer -------------------------------
@@ -125,27 +133,33 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
       s_k0 -= s_n;
       const int K = st.xcols, h = st.h;
       const int nq = K > 0 ? (K + kK2Kc - 1) / kK2Kc : 1;
-      bool deps = st.stage == 0;
+      bool deps = st.stage == 0 || P.mode != 0;
       for (int q = 0; q < nq; ++q, ++gc) {
         const int slot = gc % kK2FSlots, use = gc / kK2FSlots;
         if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
-        // lane resolves K column q*16 + (lane & 15)
-        const int kg = q * kK2Kc + (lane & (kK2Kc - 1));
+        // lane resolves K column c = lane & 15 of the chunk
+        const int c = lane & (kK2Kc - 1);
+        const int kg = q * kK2Kc + c;
         int sidx = 0;
         for (int l = 1; l < st.nseg; ++l) sidx += __shfl_sync(0xffffffffu, s_k0, l) <= kg;
         const int cc = kg - __shfl_sync(0xffffffffu, s_k0, sidx);
         const bool ok = kg < K;
-        // panel: lane = row, 16 columns
-        {
-          const int64_t src = __shfl_sync(0xffffffffu, s_off, sidx) + static_cast<int64_t>(cc) * h;
-          double2* pd = Pb + slot * kK2PBuf + lane;
-#pragma unroll 4
-          for (int col = 0; col < kK2Kc; ++col) {
-            const int64_t cs = __shfl_sync(0xffffffffu, src, col);
-            const bool cok = __shfl_sync(0xffffffffu, ok, col);
-            if (cok && lane < h) cp_async16(pd + col * kK2Ps, P.arena + cs + lane);
-          }
+        const int kval = min(kK2Kc, K - q * kK2Kc);  // valid columns (<= 0: none)
+        const int64_t psrc = __shfl_sync(0xffffffffu, s_off, sidx) + static_cast<int64_t>(cc) * h;
+        int xi = __shfl_sync(0xffffffffu, s_x0, sidx) + cc;
+        const bool gather = io.xperm != nullptr;
+        const bool load = P.mode != 3 && kval > 0;
+        double2* pd = Pb + slot * kK2PBuf;
+        double2* xd = Xb + slot * kK2XBuf + c * kK2Xs;
+        if (lane == 0) {
+          meta[slot] = make_int4(st.y0, h, st.stage, K);
+          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : P.ncv)) : 0u;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(flowdev::smem_u32(&full[slot])),
+                       "r"(bytes)
+                       : "memory");
         }
+        __syncwarp();
+        if (load && ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
         if (!deps) {  // previous-stage producers of this strip's input rows
           for (int l = 0; l < st.nseg; ++l) {
             const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
@@ -155,18 +169,16 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
           __syncwarp();
           deps = true;
         }
-        // X: lane & 15 = k, RHS pair (lane >> 4) + 2 it
-        int xi = __shfl_sync(0xffffffffu, s_x0, sidx) + cc;  // all lanes: full-mask shuffle
-        if (ok) {
-          if (io.xperm) xi = __ldg(io.xperm + xi);
-          const double2* xs = io.x + xi;
-          double2* xd = Xb + slot * kK2XBuf + (lane & (kK2Kc - 1)) * kK2Xs;
+        if (load && ok) {
+          if (gather) {  // stage 0: lane & 15 = k, RHS (lane >> 4) + 2 i
+            const double2* xs = io.x + __ldg(io.xperm + xi);
 #pragma unroll 4
-          for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xd + rhs, xs + rhs * io.xld);
+            for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xd + rhs, xs + rhs * io.xld);
+          } else if (lane < kK2Kc) {  // one input row, all RHS
+            flowdev::bulk_g2s(xd, io.x + static_cast<int64_t>(xi) * kK2Rhs, P.ncv * 16u, &full[slot]);
+          }
         }
-        if (lane == 0) meta[slot] = make_int4(st.y0, h, st.stage, K);
         cp_async_arrive_noinc(&full[slot]);
-        if (lane == 0) mbar_arrive(&full[slot]);
       }
     }
   } else {
@@ -193,12 +205,12 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int krem = min(kK2Kc, m.w - q * kK2Kc);
         const int kfull = krem & ~3;
         const double2* Ps = Pb + slot * kK2PBuf + 8 * rb + g;
-        const double2* Xs = Xb + slot * kK2XBuf + ch * 32 + g;
+        const double2* Xs = Xb + slot * kK2XBuf + t * kK2Xs + ch * 32 + g;
         auto step = [&](int kk, bool live) {
           double2 a = Ps[(kk + t) * kK2Ps];
           double2 bv[4];
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[(kk + t) * kK2Xs + cb * 8];
+          for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[kk * kK2Xs + cb * 8];
           if (!live) {  // K tail: stale slot contents must not reach the sums
             a = make_double2(0, 0);
 #pragma unroll
@@ -216,7 +228,8 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
             dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
           }
         };
-        if (kfull == kK2Kc) {
+        if (P.mode == 2) {
+        } else if (kfull == kK2Kc) {
 #pragma unroll
           for (int kk = 0; kk < kK2Kc; kk += 4) step(kk, true);
         } else {
@@ -228,6 +241,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
       }
       // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}
       const K2FStage io = P.st[m.z];
+      const bool last = m.z + 1 == P.nstages;
       if (row < m.y) {
         int idx = m.x + row;
         if (io.yperm) idx = __ldg(io.yperm + idx);
@@ -236,15 +250,15 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int rhs = 32 * ch + cb * 8 + 2 * t + i;
-            if (rhs < P.ncv) io.y[rhs * io.yld + idx] = make_double2(acc[cb][0][i], acc[cb][1][i]);
+            if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : static_cast<int64_t>(idx) * kK2Rhs + rhs] =
+                make_double2(acc[cb][0][i], acc[cb][1][i]);
           }
       }
       if (m.z + 1 < P.nstages) {
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          red_release_add(P.done + item, 1u);
-        }
+        // all consumer warps' stores, then one gpu-scope release (cumulative
+        // over the barrier) by a rotating warp
+        asm volatile("bar.sync 1, %0;" ::"n"(kK2FConsumers * 32) : "memory");
+        if (w == item % kK2FConsumers && lane == 0) red_release_add(P.done + item, 1u);
       }
     }
   }

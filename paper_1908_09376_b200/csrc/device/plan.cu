@@ -608,6 +608,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   P.epoch = D.d_k2epoch;
   P.nstrips = static_cast<int>(D.nstrips);
   P.nstages = ns;
+  P.mode = static_cast<int>((flags >> 14) & 3u);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(k2flow_grid), 1, 1);
   cfg.blockDim = dim3(kK2FThreads, 1, 1);
@@ -639,7 +640,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         io.yperm = d == 0 ? d_row_perm : d_col_perm;
       } else {
         io.y = D.d_k2buf + off * kK2Rhs;
-        io.yld = len;
+        io.yld = kK2Rhs;  // row-major, RHS fastest
         io.yperm = nullptr;
         off += len;
       }

@@ -113,7 +113,8 @@ class Plan {
   // bit3 persistent dataflow kernel for single-RHS applies,
   // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size),
   // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS),
-  // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel.
+  // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel,
+  // bits14-15 k2_flow timing experiments (k2flow.cuh, results invalid).
   unsigned flags = 0xF;  // default: k1_flow variant 0 (4 pairs x 3 x 16 KB), fastest measured at cfg1
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
