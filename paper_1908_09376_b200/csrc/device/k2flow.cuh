@@ -14,9 +14,11 @@
 //     dealt round-robin over the grid), and streams each strip's chunks
 //     (panel: 16 columns x h rows; X: 16 rows x 64 RHS) into a 4-slot shared
 //     ring with TMA bulk copies (cp.async.bulk, complete_tx on the slot's
-//     `full` barrier): one copy per panel column (h x 16 B) and one per input
-//     row (64 x 16 B: intermediate stage buffers are row-major, RHS fastest),
-//     16 lanes issuing in parallel, into the padded layouts of k2_stage.
+//     `full` barrier), into the padded layouts of k2_stage: intermediate
+//     stage buffers are row-major with the slot's padded row stride (66), so
+//     a run of consecutive input rows is ONE copy; panel columns are one copy
+//     per run when the strip height h == 2, 6 (mod 8) (stride h is then
+//     conflict-free for the A fragments), else one copy per column (stride 34).
 //     Stage 0 gathers its input rows (user operand, column-major) through
 //     the column permutation with cp.async (cp.async.mbarrier.arrive.noinc).  Before the
 //     first X chunk of a strip it acquires the completion counters of the
@@ -51,7 +53,7 @@ constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FS
 struct K2FStage {
   const double2* x;  // input (stage 0: user operand, gathered through xperm)
   double2* y;        // output (last stage: user operand, scattered through yperm)
-  int64_t xld, yld;  // user operands: column-major ld; stage buffers: row-major, ld 64
+  int64_t xld, yld;  // user operands: column-major ld; stage buffers: row-major, row stride kK2Xs
   const int* xperm;
   const int* yperm;
 };
@@ -149,17 +151,37 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         int xi = __shfl_sync(0xffffffffu, s_x0, sidx) + cc;
         const bool gather = io.xperm != nullptr;
         const bool load = P.mode != 3 && kval > 0;
+        // panel column stride in the slot: h itself when h == 2, 6 (mod 8)
+        // (A fragment loads conflict-free, one copy per column run), else 34
+        const bool prun = (h & 3) == 2;
+        const int pst = prun ? h : kK2Ps;
+        // runs of columns on one panel (consecutive panel columns and input rows)
+        const int prev = __shfl_up_sync(0xffffffffu, sidx, 1);
+        unsigned runs = __ballot_sync(0xffffffffu, ok && lane < kK2Kc && (c == 0 || prev != sidx));
         double2* pd = Pb + slot * kK2PBuf;
-        double2* xd = Xb + slot * kK2XBuf + c * kK2Xs;
+        double2* xd = Xb + slot * kK2XBuf;
         if (lane == 0) {
-          meta[slot] = make_int4(st.y0, h, st.stage, K);
-          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : P.ncv)) : 0u;
+          meta[slot] = make_int4(st.y0, h, st.stage | (pst << 8), K);
+          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : kK2Xs)) : 0u;
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(flowdev::smem_u32(&full[slot])),
                        "r"(bytes)
                        : "memory");
         }
         __syncwarp();
-        if (load && ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
+        if (load) {
+          if (!prun) {
+            if (ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
+          } else {
+            unsigned r = runs;
+            while (r) {
+              const int r0 = __ffs(r) - 1;
+              r &= r - 1;
+              const int r1 = r ? __ffs(r) - 1 : kval;
+              const int64_t src = __shfl_sync(0xffffffffu, psrc, r0);
+              if (lane == 0) flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
+            }
+          }
+        }
         if (!deps) {  // previous-stage producers of this strip's input rows
           for (int l = 0; l < st.nseg; ++l) {
             const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
@@ -169,13 +191,22 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
           __syncwarp();
           deps = true;
         }
-        if (load && ok) {
+        if (load) {
           if (gather) {  // stage 0: lane & 15 = k, RHS (lane >> 4) + 2 i
-            const double2* xs = io.x + __ldg(io.xperm + xi);
+            if (ok) {
+              const double2* xs = io.x + __ldg(io.xperm + xi);
+              double2* xk = xd + c * kK2Xs;
 #pragma unroll 4
-            for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xd + rhs, xs + rhs * io.xld);
-          } else if (lane < kK2Kc) {  // one input row, all RHS
-            flowdev::bulk_g2s(xd, io.x + static_cast<int64_t>(xi) * kK2Rhs, P.ncv * 16u, &full[slot]);
+              for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xk + rhs, xs + rhs * io.xld);
+            }
+          } else {  // stage buffers: rows padded to the slot stride, one copy per run
+            while (runs) {
+              const int r0 = __ffs(runs) - 1;
+              runs &= runs - 1;
+              const int r1 = runs ? __ffs(runs) - 1 : kval;
+              const int64_t src = static_cast<int64_t>(__shfl_sync(0xffffffffu, xi, r0)) * kK2Xs;
+              if (lane == 0) flowdev::bulk_g2s(xd + r0 * kK2Xs, io.x + src, (r1 - r0) * kK2Xs * 16u, &full[slot]);
+            }
           }
         }
         cp_async_arrive_noinc(&full[slot]);
@@ -204,10 +235,11 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         }
         const int krem = min(kK2Kc, m.w - q * kK2Kc);
         const int kfull = krem & ~3;
+        const int pst = m.z >> 8;
         const double2* Ps = Pb + slot * kK2PBuf + 8 * rb + g;
         const double2* Xs = Xb + slot * kK2XBuf + t * kK2Xs + ch * 32 + g;
         auto step = [&](int kk, bool live) {
-          double2 a = Ps[(kk + t) * kK2Ps];
+          double2 a = Ps[(kk + t) * pst];
           double2 bv[4];
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[kk * kK2Xs + cb * 8];
@@ -240,8 +272,9 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
       // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}
-      const K2FStage io = P.st[m.z];
-      const bool last = m.z + 1 == P.nstages;
+      const int stage = m.z & 255;
+      const K2FStage io = P.st[stage];
+      const bool last = stage + 1 == P.nstages;
       if (row < m.y) {
         int idx = m.x + row;
         if (io.yperm) idx = __ldg(io.yperm + idx);
@@ -250,11 +283,11 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int rhs = 32 * ch + cb * 8 + 2 * t + i;
-            if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : static_cast<int64_t>(idx) * kK2Rhs + rhs] =
+            if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : idx * io.yld + rhs] =
                 make_double2(acc[cb][0][i], acc[cb][1][i]);
           }
       }
-      if (m.z + 1 < P.nstages) {
+      if (!last) {
         // all consumer warps' stores, then one gpu-scope release (cumulative
         // over the barrier) by a rotating warp
         asm volatile("bar.sync 1, %0;" ::"n"(kK2FConsumers * 32) : "memory");

@@ -588,7 +588,7 @@ void Plan::ensure_k2flow(int d) {
   if (D.d_k2done) return;
   int64_t rows = 0;
   for (size_t s = 0; s + 1 < D.stages.size(); ++s) rows += D.stages[s].out_len;
-  cuda_check(cudaMalloc(&D.d_k2buf, std::max<int64_t>(rows, 1) * kK2Rhs * sizeof(double2)), "cudaMalloc k2 stages");
+  cuda_check(cudaMalloc(&D.d_k2buf, std::max<int64_t>(rows, 1) * kK2Xs * sizeof(double2)), "cudaMalloc k2 stages");
   cuda_check(cudaMalloc(&D.d_k2done, std::max<int64_t>(D.nstrips, 1) * sizeof(unsigned)), "cudaMalloc k2 counters");
   cuda_check(cudaMalloc(&D.d_k2epoch, kMaxFlowCtas * sizeof(unsigned)), "cudaMalloc k2 epochs");
   cuda_check(cudaMemset(D.d_k2done, 0, std::max<int64_t>(D.nstrips, 1) * sizeof(unsigned)), "reset k2 counters");
@@ -639,8 +639,8 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         io.yld = out_ld;
         io.yperm = d == 0 ? d_row_perm : d_col_perm;
       } else {
-        io.y = D.d_k2buf + off * kK2Rhs;
-        io.yld = kK2Rhs;  // row-major, RHS fastest
+        io.y = D.d_k2buf + off * kK2Xs;
+        io.yld = kK2Xs;  // row-major, RHS fastest, rows padded to the smem slot stride
         io.yperm = nullptr;
         off += len;
       }
