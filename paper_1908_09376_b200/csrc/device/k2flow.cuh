@@ -9,7 +9,7 @@
 // 3.46 waves).  Reference: apply_factor's GEMM path for x.cols() > 1
 // (src/butterfly.cpp:633-637 with bf::apply(F, MatXc), :779).
 //
-// CTA = 8 consumer warps + 1 producer warp, 2 CTAs per SM.
+// CTA = 8 consumer warps + 1 producer warp + 1 publisher warp, 2 CTAs per SM.
 //   * Producer: walks this CTA's strips (global strip list, stage-major,
 //     dealt round-robin over the grid), and streams each strip's chunks
 //     (panel: 16 columns x h rows; X: 16 rows x 64 RHS) into a 4-slot shared
@@ -25,13 +25,17 @@
 //     previous-stage strips that produce its input rows (Seg::dep0/dep1).
 //   * Consumers: LDS + DMMA only (8 rows x 32 RHS per warp, as in k2_stage);
 //     release the slot on its `empty` barrier; at the end of a strip store
-//     the 32 x 64 tile; after a consumer barrier one thread adds 1 (release,
-//     gpu scope) to the strip's counter.
+//     the 32 x 64 tile and arrive on the strip's `done` barrier (8-deep ring).
+//   * A publisher warp waits on the `done` ring and publishes each completed
+//     strip with one gpu-scope release add on its counter (a warp with no
+//     loads in flight, so the release fence is cheap); the producer never
+//     runs more than 8 strips ahead of the publications.
 //   * Per-CTA apply epochs (all CTAs run every launch): a strip of launch e
 //     is complete when its counter reaches e.
 // Deadlock freedom: CTAs are co-resident (cooperative launch) and each
-// walks its strips in increasing global order; the smallest incomplete strip
-// has all its inputs complete, and its CTA's producer has reached it.
+// walks its strips in increasing global order; the smallest unpublished
+// strip has all its inputs published, its CTA's producer has issued it or is
+// at it, and publication waits on nothing but this CTA's consumers.
 // Stages overlap, so every stage but the last writes its own buffer.
 #pragma once
 
@@ -46,9 +50,10 @@
 namespace midbf::dev {
 
 constexpr int kK2FConsumers = 8;                      // consumer warps
-constexpr int kK2FThreads = (kK2FConsumers + 1) * 32;  // + one producer warp
+constexpr int kK2FThreads = (kK2FConsumers + 2) * 32;  // + producer and publisher warps
 constexpr int kK2FSlots = 4;                           // ring depth
-constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FSlots * (16 + 16);
+constexpr int kK2FDone = 8;                            // strip-completion barrier ring
+constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FSlots * (16 + 16) + kK2FDone * 8;
 
 struct K2FStage {
   const double2* x;  // input (stage 0: user operand, gathered through xperm)
@@ -83,6 +88,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// bounded wait: true once the phase with `parity` has completed
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(flowdev::smem_u32(bar)), "r"(parity), "r"(2000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -100,16 +117,20 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
   double2* const Xb = k2smem + kK2FSlots * kK2PBuf;  // kK2FSlots X buffers
   uint64_t* const full = reinterpret_cast<uint64_t*>(Xb + kK2FSlots * kK2XBuf);
   uint64_t* const empty = full + kK2FSlots;
-  int4* const meta = reinterpret_cast<int4*>(empty + kK2FSlots);  // per slot: {y0, h, stage, K}
+  int4* const meta = reinterpret_cast<int4*>(empty + kK2FSlots);  // per slot: {y0, h, stage | A stride, K}
+  uint64_t* const done = reinterpret_cast<uint64_t*>(meta + kK2FSlots);
   __shared__ unsigned s_epoch;
+  __shared__ int s_pub;  // strips of this CTA published so far
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (int i = 0; i < kK2FSlots; ++i) {
       mbar_init(&full[i], 33);  // 32 cp.async arrivals + the meta writer
       mbar_init(&empty[i], kK2FConsumers);
     }
+    for (int i = 0; i < kK2FDone; ++i) mbar_init(&done[i], kK2FConsumers);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_epoch = P.epoch[blockIdx.x] + 1;
+    s_pub = 0;
   }
   __syncthreads();
   const unsigned target = s_epoch;
@@ -117,7 +138,10 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
   if (w == kK2FConsumers) {
     // ------------------------------ producer -------------------------------
     int gc = 0;  // chunks issued
+    int started = 0;  // this CTA's strips started
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
+      while (started - *reinterpret_cast<volatile int*>(&s_pub) >= kK2FDone) __nanosleep(64);  // done-ring slot free
+      ++started;
       const Strip st = P.strips[item];
       const K2FStage io = P.st[st.stage];
       int64_t s_off = 0;
@@ -182,14 +206,14 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
             }
           }
         }
-        if (!deps) {  // previous-stage producers of this strip's input rows
+        while (!deps) {  // previous-stage producers of this strip's input rows
+          bool ready = true;
           for (int l = 0; l < st.nseg; ++l) {
             const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
-            for (int s = d0 + lane; s < d1; s += 32)
-              while (ld_acquire(P.done + s) < target) __nanosleep(64);
+            for (int s = d0 + lane; s < d1 && ready; s += 32) ready = ld_acquire(P.done + s) >= target;
           }
-          __syncwarp();
-          deps = true;
+          deps = __all_sync(0xffffffffu, ready);
+          if (!deps) __nanosleep(64);
         }
         if (load) {
           if (gather) {  // stage 0: lane & 15 = k, RHS (lane >> 4) + 2 i
@@ -212,12 +236,22 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         cp_async_arrive_noinc(&full[slot]);
       }
     }
+  } else if (w == kK2FConsumers + 1) {
+    // ------------------------------ publisher ------------------------------
+    int n = 0;
+    for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x, ++n) {
+      mbar_wait(&done[n % kK2FDone], (n / kK2FDone) & 1);
+      if (lane == 0) {
+        red_release_add(P.done + item, 1u);
+        *reinterpret_cast<volatile int*>(&s_pub) = n + 1;
+      }
+    }
   } else {
     // ------------------------------ consumers ------------------------------
     const int g = lane >> 2, t = lane & 3;
     const int rb = w & 3, ch = w >> 2;  // row block, RHS half
     const int row = 8 * rb + g;
-    int gc = 0;
+    int gc = 0, nit = 0;
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
       double acc[4][2][2];
 #pragma unroll
@@ -287,12 +321,9 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
                 make_double2(acc[cb][0][i], acc[cb][1][i]);
           }
       }
-      if (!last) {
-        // all consumer warps' stores, then one gpu-scope release (cumulative
-        // over the barrier) by a rotating warp
-        asm volatile("bar.sync 1, %0;" ::"n"(kK2FConsumers * 32) : "memory");
-        if (w == item % kK2FConsumers && lane == 0) red_release_add(P.done + item, 1u);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[nit % kK2FDone]);
+      ++nit;
     }
   }
   __syncthreads();
