@@ -123,11 +123,28 @@ int midbf_sample(const midbf_kernel_desc* kernel, int64_t ntasks, const int64_t*
 int midbf_direct_sum(const midbf_kernel_desc* kernel, const double* f, const int64_t* rows, int64_t nsel,
                      double* g);
 
+/* ----------------------------------------- batched interpolative decompositions
+ * Column IDs of explicit blocks on the GPU (K5): la::cid_from_rows
+ * (src/linalg.cpp:266-286) = truncated pivoted QR pqr_impl (:23-107) +
+ * id_rank (:249-264) + V = [I, R11^-1 R12] P^T.  Block b is m_b x n_b complex
+ * column-major (dims[2b], dims[2b+1]), blocks packed back to back in
+ * `blocks`.  Out: ranks[b] (-1: not computed on the device -- m > 256,
+ * n > 512, or the rank rule needs the full QR, the host's fallback case;
+ * recompute with the host ID), skel[b*kcap + i] for i < rank (kcap >=
+ * min(m_b, n_b, k_max) for every b), V (rank x n_b, ld rank) at
+ * vals + 2*voff_b with voff_b = sum over earlier blocks of
+ * min(m, n, k_max) * n.  Host pointers; returns when done. */
+int midbf_cid_batch(const double* blocks, const int64_t* dims, int64_t nblocks, int64_t k_max, double eps,
+                    int64_t* ranks, int64_t* skel, int64_t kcap, double* vals);
+
 /* ------------------------------------------- host factorization object
  * bf::idbf_factorize (src/butterfly.cpp:708-769) with trees built the way
  * the reference tests and experiment do (both sides at a common depth,
- * src/experiment.cpp:140-144).  sampler = 0: entries sampled on the GPU;
- * 1: host evaluation of the same descriptor.  exec = 0 serial, 1 OpenMP.*/
+ * src/experiment.cpp:140-144).  sampler = 0: entries sampled on the GPU (K3),
+ * IDs on the host; 1: host evaluation of the same descriptor, host IDs;
+ * 2: entries AND interpolative decompositions on the GPU (K3 + K5, replacing
+ * la::rid_from_cols / la::cid_from_rows, src/linalg.cpp:266-295; blocks the
+ * device hands back are recomputed on the host).  exec = 0 serial, 1 OpenMP.*/
 int midbf_factorize(midbf_fact_t* out, const midbf_kernel_desc* kernel, int64_t n0, int64_t k_max, double eps,
                     int64_t t, uint64_t seed, int exec, int sampler);
 int midbf_fact_load(midbf_fact_t* out, const char* path);       /* bf::load_factorization */
@@ -148,6 +165,10 @@ int midbf_fact_apply(midbf_fact_t fact, const double* f, double* g, int64_t nrhs
 /* Statistics of a device-sampled factorize: out[0] entries, out[1] sampler calls,
  * out[2] nanoseconds spent in the device sampler (kernel + copies). */
 int midbf_fact_stats(midbf_fact_t fact, int64_t* out);
+/* out[0] IDs computed on the GPU (K5), out[1] IDs handed back to the host,
+ * out[2] nanoseconds in the device ID batches (K3 + K5 + copies), out[3]
+ * nanoseconds for the whole factorize (sampler 0 / 2). */
+int midbf_fact_id_stats(midbf_fact_t fact, int64_t* out);
 
 /* Plan introspection / tuning (benchmarks, profiling):
  * stage table out[s*4 + 0..3] = strips, payload bytes, in_len, out_len

@@ -321,6 +321,13 @@ class Factorization:
         _check(lib().midbf_fact_stats(self._h, _ip(o)))
         return int(o[0]), int(o[1]), o[2] * 1e-9
 
+    def id_stats(self):
+        """(IDs on the GPU, IDs handed back to the host, seconds in the device
+        ID batches, seconds for the whole factorize)."""
+        o = np.zeros(4, dtype=np.int64)
+        _check(lib().midbf_fact_id_stats(self._h, _ip(o)))
+        return int(o[0]), int(o[1]), o[2] * 1e-9, o[3] * 1e-9
+
     def perms(self):
         rp = np.empty(self.nrows, dtype=np.int64)
         cp = np.empty(self.ncols, dtype=np.int64)
@@ -370,13 +377,43 @@ class Factorization:
         _check(lib().midbf_fact_save(self._h, str(path).encode()))
 
 
-def idbf_factorize(kernel, n0, k=30, eps=1e-9, t=5, seed=0, parallel=True, sampler="device"):
+def cid_batch(blocks, k_max, eps):
+    """Column IDs of complex blocks on the GPU (K5, midbf_cid_batch).  Returns
+    per block (skeleton, V, rank), or None where the device hands the block
+    back (rank -1: the caller recomputes it with the host ID)."""
+    blocks = [np.asfortranarray(b, dtype=np.complex128) for b in blocks]
+    if not blocks:
+        return []
+    dims = np.array([b.shape for b in blocks], dtype=np.int64).reshape(-1)
+    caps = [min(b.shape[0], b.shape[1], k_max if k_max > 0 else 1 << 62) for b in blocks]
+    kcap = max(caps)
+    packed = np.concatenate([b.reshape(-1, order="F") for b in blocks])
+    ranks = np.empty(len(blocks), dtype=np.int64)
+    skel = np.empty(len(blocks) * kcap, dtype=np.int64)
+    vals = np.zeros(sum(c * b.shape[1] for c, b in zip(caps, blocks)), dtype=np.complex128)
+    _check(lib().midbf_cid_batch(_p(packed.view(np.float64)), _ip(dims), i64(len(blocks)), i64(k_max),
+                                 C.c_double(eps), _ip(ranks), _ip(skel), i64(kcap), _p(vals.view(np.float64))))
+    out, off = [], 0
+    for q, (c, b) in enumerate(zip(caps, blocks)):
+        k, n = int(ranks[q]), b.shape[1]
+        out.append(None if k < 0 else (skel[q * kcap: q * kcap + k].copy(),
+                                       vals[off: off + k * n].reshape((k, n), order="F").copy(), k))
+        off += c * n
+    return out
+
+
+def idbf_factorize(kernel, n0, k=30, eps=1e-9, t=5, seed=0, parallel=True, sampler="device", ids="device"):
     """bf::idbf_factorize on trees built at a common depth from the kernel's
     point sets.  sampler="device": every entry from the GPU sampler (K3);
-    "host": the same descriptor evaluated on the CPU (reference EntryFn path)."""
+    "host": the same descriptor evaluated on the CPU (reference EntryFn path).
+    ids="device" (with the device sampler): the interpolative decompositions
+    run on the GPU too (K5); "host": la::rid_from_cols / cid_from_rows on the
+    CPU, bitwise the oracle's arithmetic."""
+    if sampler not in ("device", "host") or ids not in ("device", "host"):
+        raise ValueError("sampler and ids are 'device' or 'host'")
+    mode = 1 if sampler == "host" else (2 if ids == "device" else 0)
     h = vp()
-    _check(lib().midbf_factorize(C.byref(h), C.byref(kernel.desc), n0, k, eps, t, seed, 1 if parallel else 0,
-                                 0 if sampler == "device" else 1))
+    _check(lib().midbf_factorize(C.byref(h), C.byref(kernel.desc), n0, k, eps, t, seed, 1 if parallel else 0, mode))
     return Factorization(h)
 
 

@@ -1,0 +1,278 @@
+// K5 — batched interpolative decompositions on the device, sm_100a
+// (SURVEY.md §8(f)1).
+//
+// Replaces the host IDs of shared_sweep (reference src/butterfly.cpp:466-472,
+// 516-519 -> la::rid_from_cols / la::cid_from_rows, src/linalg.cpp:266-295),
+// i.e. the truncated pivoted Householder QR pqr_impl (src/linalg.cpp:23-107)
+// plus id_rank (:249-264) and V = [I, R11^-1 R12] P^T.  Same step sequence as
+// the host restatement (csrc/host/linalg.cpp householder_qr): pivot = largest
+// remaining squared norm (lowest index on ties), Householder vector
+// v = [1; x(k+1:)/v0] with v0 = a0 + phase(a0) |x|, beta = 2 / (1 + |v|^2),
+// trailing update c -= beta v (v^H c), squared-norm downdate with the
+// reference's recompute guard (cur < 0 or cur <= 1e-12 ref).  Sums are warp
+// butterfly reductions (fixed order: bitwise run to run, not bitwise equal
+// to the host's serial sums).  The phase fix of R's rows is skipped: it
+// cancels in R11^-1 R12 and leaves |R_ii| unchanged.
+//
+// One warp per block, rows distributed over lanes (row i -> lane i % 32,
+// register slot i / 32; m <= 32 * kIdRows), squared norms and the column
+// permutation in shared memory (n <= kIdCols).  Blocks outside those limits,
+// and blocks whose first min(m,n,k_max) diagonals hit id_rank's 1e-14 tail
+// trim below the full factorization (the host's fallback case), return
+// rank -1: the caller recomputes them on the host.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace midbf::dev {
+
+constexpr int kIdRows = 8;             // register slots per lane: m <= 256
+constexpr int kIdMaxRows = 32 * kIdRows;
+constexpr int kIdCols = 512;           // n <= 512
+constexpr int kIdWarps = 4;            // warps (blocks) per CTA
+constexpr size_t kIdSmem = size_t(kIdWarps) * kIdCols * (8 + 8 + 4);
+
+struct IdTask {
+  int64_t off;   // block B (m x n, column-major) in the workspace
+  int64_t ooff;  // output slot: cap x n complex
+  int32_t m, n;
+};
+
+namespace k5dev {
+
+__device__ __forceinline__ double wsum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double nrm2(double2 z) { return z.x * z.x + z.y * z.y; }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+
+}  // namespace k5dev
+
+// ranks[t] = k (or -1: recompute on the host); skel[t * kcap + i] = perm[i];
+// out + ooff: V (k x n, ld k) for a column ID, W = V^T (n x k, ld n) for a row
+// ID (`rowid`: the workspace holds the transposed block).
+__global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
+                                                       int ntasks, int kmax, double eps, int rowid,
+                                                       double2* __restrict__ out, int* __restrict__ ranks,
+                                                       int* __restrict__ skel, int kcap) {
+  using namespace k5dev;
+  extern __shared__ __align__(16) unsigned char k5smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* cur = reinterpret_cast<double*>(k5smem) + wib * kIdCols;
+  double* ref = reinterpret_cast<double*>(k5smem) + (kIdWarps + wib) * kIdCols;
+  int* perm = reinterpret_cast<int*>(reinterpret_cast<double*>(k5smem) + 2 * kIdWarps * kIdCols) + wib * kIdCols;
+  const int t = blockIdx.x * kIdWarps + wib;
+  if (t >= ntasks) return;
+  const IdTask tk = tasks[t];
+  const int m = tk.m, n = tk.n;
+  if (m > kIdMaxRows || n > kIdCols || m <= 0 || n <= 0) {
+    if (lane == 0) ranks[t] = -1;
+    return;
+  }
+  double2* B = ws + tk.off;
+  const int full = min(m, n);
+  const int cap = kmax > 0 ? min(full, kmax) : full;
+
+  // squared column norms
+  for (int j = 0; j < n; ++j) {
+    const double2* c = B + static_cast<int64_t>(j) * m;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r) {
+      const int i = lane + 32 * r;
+      if (i < m) s += nrm2(c[i]);
+    }
+    s = wsum(s);
+    if (lane == 0) cur[j] = ref[j] = s;
+  }
+  for (int j = lane; j < n; j += 32) perm[j] = j;
+  __syncwarp();
+
+  int k = 0;
+  for (; k < cap; ++k) {
+    // pivot: largest remaining norm, lowest index on ties
+    double bv = -1.0;
+    int bp = n;
+    for (int j = k + lane; j < n; j += 32)
+      if (cur[j] > bv) bv = cur[j], bp = j;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+    }
+    const int p = bp;
+    if (p != k) {
+      double2* a = B + static_cast<int64_t>(k) * m;
+      double2* b = B + static_cast<int64_t>(p) * m;
+      for (int i = lane; i < m; i += 32) {
+        const double2 tmp = a[i];
+        a[i] = b[i];
+        b[i] = tmp;
+      }
+      if (lane == 0) {
+        const int tp = perm[k];
+        perm[k] = perm[p];
+        perm[p] = tp;
+        double tv = cur[k];
+        cur[k] = cur[p];
+        cur[p] = tv;
+        tv = ref[k];
+        ref[k] = ref[p];
+        ref[p] = tv;
+      }
+      __syncwarp();
+    }
+    // Householder vector from column k (rows k..m-1)
+    double2* col = B + static_cast<int64_t>(k) * m;
+    double2 x[kIdRows];
+    double xs = 0.0;
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r) {
+      const int i = lane + 32 * r;
+      x[r] = (i >= k && i < m) ? col[i] : make_double2(0, 0);
+      xs += nrm2(x[r]);
+    }
+    xs = wsum(xs);
+    const double xn = sqrt(xs);
+    if (xn == 0.0) break;
+    double2 mine = make_double2(0, 0);  // row k's entry (static register indexing)
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r)
+      if (r == (k >> 5)) mine = x[r];
+    const double2 a0 = make_double2(__shfl_sync(0xffffffffu, mine.x, k & 31), __shfl_sync(0xffffffffu, mine.y, k & 31));
+    const double aa = sqrt(nrm2(a0));
+    const double2 ph = aa == 0.0 ? make_double2(1.0, 0.0) : make_double2(a0.x / aa, a0.y / aa);
+    const double2 v0 = make_double2(a0.x + ph.x * xn, a0.y + ph.y * xn);
+    double vs = 0.0;
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r) {
+      const int i = lane + 32 * r;
+      if (i > k && i < m) {
+        x[r] = cdiv(x[r], v0);
+        vs += nrm2(x[r]);
+        col[i] = x[r];
+      }
+    }
+    vs = wsum(vs);
+    const double beta = 2.0 / (1.0 + vs);
+    if (lane == (k & 31)) col[k] = make_double2(-ph.x * xn, -ph.y * xn);
+    // v = [1; x(k+1:)], zero above row k
+    double2 v[kIdRows];
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r) {
+      const int i = lane + 32 * r;
+      v[r] = i == k ? make_double2(1.0, 0.0) : (i > k && i < m ? x[r] : make_double2(0, 0));
+    }
+    // trailing columns: c -= beta v (v^H c); squared-norm downdate
+    for (int j = k + 1; j < n; ++j) {
+      double2* c = B + static_cast<int64_t>(j) * m;
+      double2 cv[kIdRows];
+      double wr = 0.0, wi = 0.0;
+#pragma unroll
+      for (int r = 0; r < kIdRows; ++r) {
+        const int i = lane + 32 * r;
+        cv[r] = (i >= k && i < m) ? c[i] : make_double2(0, 0);
+        const double2 q = cmulc(cv[r], v[r]);
+        wr += q.x;
+        wi += q.y;
+      }
+      wr = wsum(wr);
+      wi = wsum(wi);
+      const double2 cw = make_double2(wr, -wi);  // conj(w)
+      double rest = 0.0, ck = 0.0;
+#pragma unroll
+      for (int r = 0; r < kIdRows; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= k && i < m) {
+          const double2 d = cmul(make_double2(beta * v[r].x, beta * v[r].y), cw);
+          cv[r].x -= d.x;
+          cv[r].y -= d.y;
+          c[i] = cv[r];
+          if (i == k) ck = nrm2(cv[r]);
+          else rest += nrm2(cv[r]);
+        }
+      }
+      ck = __shfl_sync(0xffffffffu, ck, k & 31);
+      double cj = cur[j] - ck;
+      double rj = ref[j];
+      if (cj < 0.0 || cj <= 1e-12 * rj) {  // recompute guard
+        const double s = wsum(rest);
+        cj = m - k > 1 ? s : 0.0;
+        rj = cj;
+      }
+      __syncwarp();
+      if (lane == 0) cur[j] = cj, ref[j] = rj;
+      __syncwarp();
+    }
+  }
+  const int steps = k;
+  __syncwarp();
+
+  // rank (id_rank, src/linalg.cpp:249-264) on |R_ii|, i < steps
+  int rank = 0;
+  bool fallback = false;
+  if (lane == 0) {
+    const double d0 = steps > 0 ? sqrt(nrm2(B[0])) : 0.0;
+    if (steps > 0 && d0 != 0.0) {
+      if (steps == cap && cap < full)
+        for (int i = 0; i < steps; ++i)
+          fallback = fallback || sqrt(nrm2(B[static_cast<int64_t>(i) * m + i])) <= 1e-14 * d0;
+      int mm = steps;
+      while (mm > 0 && sqrt(nrm2(B[static_cast<int64_t>(mm - 1) * m + mm - 1])) <= 1e-14 * d0) --mm;
+      rank = mm;
+      if (eps > 0.0)
+        for (int i = 0; i < mm; ++i)
+          if (sqrt(nrm2(B[static_cast<int64_t>(i) * m + i])) <= eps * d0) {
+            rank = i + 1;
+            break;
+          }
+      if (kmax > 0) rank = min(rank, kmax);
+    }
+  }
+  rank = __shfl_sync(0xffffffffu, rank, 0);
+  fallback = __shfl_sync(0xffffffffu, fallback, 0);
+  if (fallback) {
+    if (lane == 0) ranks[t] = -1;
+    return;
+  }
+  if (lane == 0) ranks[t] = rank;
+  for (int i = lane; i < rank; i += 32) skel[static_cast<int64_t>(t) * kcap + i] = perm[i];
+
+  // V(:, perm[j]) = e_j (j < rank), else R11^-1 R(0:rank, j); lane per column
+  double2* V = out + tk.ooff;
+  for (int j = lane; j < n; j += 32) {
+    const int pj = perm[j];
+    auto at = [&](int i) -> double2& {
+      return rowid ? V[static_cast<int64_t>(i) * n + pj] : V[static_cast<int64_t>(pj) * rank + i];
+    };
+    if (j < rank) {
+      for (int i = 0; i < rank; ++i) at(i) = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      continue;
+    }
+    for (int i = rank - 1; i >= 0; --i) {
+      double2 s = B[static_cast<int64_t>(j) * m + i];
+      for (int l = i + 1; l < rank; ++l) {
+        const double2 q = cmul(B[static_cast<int64_t>(l) * m + i], at(l));
+        s.x -= q.x;
+        s.y -= q.y;
+      }
+      at(i) = cdiv(s, B[static_cast<int64_t>(i) * m + i]);
+    }
+  }
+}
+
+}  // namespace midbf::dev

@@ -22,10 +22,15 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
 
 #include "common.cuh"
+#include "k5_id.cuh"
 #include "sample.hpp"
 
 namespace midbf::dev {
@@ -108,6 +113,23 @@ __global__ void __launch_bounds__(256) k3_sample(DevK k, const int* __restrict__
   }
 }
 
+// K3 into the K5 workspace: task t's block B (m x n column-major at
+// ws + off): B = K(rows, cols) (m = nr, n = nc), or with TRANS its transpose
+// (m = nc, n = nr) for a row ID.  rc = {row_off, nr, col_off, nc}.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) k3_sample_ws(DevK k, const int4* __restrict__ rc,
+                                                    const IdTask* __restrict__ tasks, const int* __restrict__ rid,
+                                                    const int* __restrict__ cid, double2* __restrict__ ws) {
+  const int4 q = rc[blockIdx.x];
+  const IdTask tk = tasks[blockIdx.x];
+  const int m = tk.m, total = tk.m * tk.n;
+  double2* B = ws + tk.off;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int c = e / m, r = e - c * m;
+    B[e] = TRANS ? entry(k, rid[q.x + c], cid[q.z + r]) : entry(k, rid[q.x + r], cid[q.z + c]);
+  }
+}
+
 // Direct sum: blockIdx.x covers 256 selected rows (one per thread),
 // blockIdx.y a contiguous column split.  Column data staged in shared memory.
 constexpr int kTile = 256;
@@ -164,32 +186,71 @@ T* upload(const T* h, size_t n, const char* what) {
 
 }  // namespace
 
-struct EntrySampler::Impl {
-  DevK k{};
-  std::vector<void*> owned;
-  int64_t nrows = 0, ncols = 0;
-  int64_t launched_entries = 0;
-  // double-buffered device output / pinned staging, allocated on first use
+// K5 workspace, process-wide and grow-only (a factorization builds its own
+// sampler; reallocating ~0.5 GB of device and pinned memory per call cost
+// more than the IDs themselves).  Held under `mu` for a whole ID batch.
+struct IdPool {
+  std::mutex mu;
+  double2* d_ws = nullptr;
+  double2* d_vals = nullptr;
+  double2* h_vals = nullptr;
+  int* d_rank = nullptr;
+  int* d_skel = nullptr;
+  int64_t ws_cap = 0, vals_cap = 0, hvals_cap = 0, rank_cap = 0, skel_cap = 0;
+  template <typename T>
+  static void grow(T*& p, int64_t& cap, int64_t need, bool pinned, const char* what) {
+    if (need <= cap) return;
+    const int64_t n = std::max<int64_t>(need, cap + cap / 2);
+    if (pinned) {
+      cudaFreeHost(p);
+      p = nullptr;
+      cuda_check(cudaMallocHost(&p, n * sizeof(T)), what);
+    } else {
+      cudaFree(p);
+      p = nullptr;
+      cuda_check(cudaMalloc(&p, n * sizeof(T)), what);
+    }
+    cap = n;
+  }
+};
+IdPool& id_pool() {
+  static IdPool* p = new IdPool;  // never destroyed: may outlive the CUDA context teardown order
+  return *p;
+}
+
+// Double-buffered device output / pinned staging of sample_blocks, also
+// process-wide (allocated on first use; held under `mu` for a whole call).
+struct ChunkPool {
   static constexpr int64_t kChunk = int64_t{4} << 20;  // complex entries per chunk (64 MB)
+  std::mutex mu;
   double2* d_out[2] = {nullptr, nullptr};
   double2* h_pin[2] = {nullptr, nullptr};
-  cudaStream_t stream = nullptr;
   cudaEvent_t done[2] = {nullptr, nullptr};
-  void ensure_buffers() {
+  void ensure() {
     if (d_out[0]) return;
     for (int b = 0; b < 2; ++b) {
       cuda_check(cudaMalloc(&d_out[b], kChunk * sizeof(double2)), "cudaMalloc sample buffer");
       cuda_check(cudaMallocHost(&h_pin[b], kChunk * sizeof(double2)), "cudaMallocHost sample buffer");
       cuda_check(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
     }
-    cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  }
+};
+ChunkPool& chunk_pool() {
+  static ChunkPool* p = new ChunkPool;
+  return *p;
+}
+
+struct EntrySampler::Impl {
+  DevK k{};
+  std::vector<void*> owned;
+  int64_t nrows = 0, ncols = 0;
+  int64_t launched_entries = 0;
+  static constexpr int64_t kChunk = ChunkPool::kChunk;
+  cudaStream_t stream = nullptr;
+  void ensure_stream() {
+    if (!stream) cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
   }
   ~Impl() {
-    for (int b = 0; b < 2; ++b) {
-      cudaFree(d_out[b]);
-      cudaFreeHost(h_pin[b]);
-      if (done[b]) cudaEventDestroy(done[b]);
-    }
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -334,15 +395,18 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   }
   chunk_entries.push_back(acc);
   chunk_begin.push_back(nsub);
-  I.ensure_buffers();
+  I.ensure_stream();
+  ChunkPool& CP = chunk_pool();
+  std::lock_guard<std::mutex> lock(CP.mu);
+  CP.ensure();
   int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
   int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
   int* d_tasks = upload(dt.data(), dt.size(), "upload tasks");
   const int64_t nchunks = static_cast<int64_t>(chunk_entries.size());
   auto scatter = [&](int64_t c) {
     const int b = static_cast<int>(c & 1);
-    cuda_check(cudaEventSynchronize(I.done[b]), "sample chunk");
-    const double2* src = I.h_pin[b];
+    cuda_check(cudaEventSynchronize(CP.done[b]), "sample chunk");
+    const double2* src = CP.h_pin[b];
     const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = t0; t < t1; ++t) {
@@ -353,17 +417,17 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   try {
     for (int64_t c = 0; c < nchunks; ++c) {
       const int b = static_cast<int>(c & 1);
-      if (c >= 2) cuda_check(cudaEventSynchronize(I.done[b]), "sample buffer reuse");
+      if (c >= 2) cuda_check(cudaEventSynchronize(CP.done[b]), "sample buffer reuse");
       const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
       if (chunk_entries[static_cast<size_t>(c)] > 0) {
         k3_sample<<<static_cast<unsigned>(t1 - t0), 256, 0, I.stream>>>(I.k, d_tasks + 5 * t0, d_rid, d_cid,
-                                                                         I.d_out[b]);
+                                                                         CP.d_out[b]);
         cuda_check(cudaGetLastError(), "k3_sample launch");
-        cuda_check(cudaMemcpyAsync(I.h_pin[b], I.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
+        cuda_check(cudaMemcpyAsync(CP.h_pin[b], CP.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
                                    cudaMemcpyDeviceToHost, I.stream),
                    "sample D2H");
       }
-      cuda_check(cudaEventRecord(I.done[b], I.stream), "event record");
+      cuda_check(cudaEventRecord(CP.done[b], I.stream), "event record");
       if (c >= 1) scatter(c - 1);
       I.launched_entries += chunk_entries[static_cast<size_t>(c)];
     }
@@ -378,6 +442,110 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   cudaFree(d_rid);
   cudaFree(d_cid);
   cudaFree(d_tasks);
+}
+
+void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+                              const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps,
+                              IdBatch& out) {
+  Impl& I = *impl_;
+  static const bool timing = std::getenv("MIDBF_ID_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_start = now();
+  out.rank.assign(static_cast<size_t>(ntasks), 0);
+  out.ooff.assign(static_cast<size_t>(ntasks), 0);
+  out.kcap = 0;
+  out.vals = nullptr;
+  if (ntasks <= 0) return;
+  if (ntasks > 0x7fffffff || n_row_ids > 0x7fffffff || n_col_ids > 0x7fffffff)
+    throw std::invalid_argument("too many ID tasks");
+  std::vector<int> rid(static_cast<size_t>(n_row_ids)), cid(static_cast<size_t>(n_col_ids));
+  for (int64_t q = 0; q < n_row_ids; ++q) {
+    if (row_ids[q] < 0 || row_ids[q] >= I.nrows) throw std::invalid_argument("row id out of range");
+    rid[q] = static_cast<int>(row_ids[q]);
+  }
+  for (int64_t q = 0; q < n_col_ids; ++q) {
+    if (col_ids[q] < 0 || col_ids[q] >= I.ncols) throw std::invalid_argument("column id out of range");
+    cid[q] = static_cast<int>(col_ids[q]);
+  }
+  std::vector<int4> rc(static_cast<size_t>(ntasks));
+  std::vector<IdTask> tk(static_cast<size_t>(ntasks));
+  int64_t ws = 0, vals = 0;
+  int kcap = 1;
+  for (int64_t t = 0; t < ntasks; ++t) {
+    const int64_t* q = tasks + 5 * t;
+    if (q[1] <= 0 || q[3] <= 0 || q[0] < 0 || q[2] < 0 || q[0] + q[1] > n_row_ids || q[2] + q[3] > n_col_ids)
+      throw std::invalid_argument("ID task outside its id lists (or empty)");
+    const int64_t m = rowid ? q[3] : q[1], n = rowid ? q[1] : q[3];
+    if (m * n > 0x7fffffff) throw std::invalid_argument("ID block too large");
+    const int64_t full = std::min(m, n), cap = k_max > 0 ? std::min(full, k_max) : full;
+    rc[t] = make_int4(static_cast<int>(q[0]), static_cast<int>(q[1]), static_cast<int>(q[2]), static_cast<int>(q[3]));
+    tk[t] = IdTask{ws, vals, static_cast<int32_t>(m), static_cast<int32_t>(n)};
+    out.ooff[t] = 2 * vals;  // in doubles
+    ws += m * n;
+    vals += cap * n;
+    kcap = std::max<int>(kcap, static_cast<int>(cap));
+  }
+  out.kcap = kcap;
+  out.skel.assign(static_cast<size_t>(ntasks * kcap), 0);
+  const auto t_prep = now();
+  I.ensure_stream();
+  IdPool& P = id_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  IdPool::grow(P.d_ws, P.ws_cap, ws, false, "cudaMalloc ID workspace");
+  IdPool::grow(P.d_vals, P.vals_cap, vals, false, "cudaMalloc ID values");
+  IdPool::grow(P.h_vals, P.hvals_cap, vals, true, "cudaMallocHost ID values");
+  IdPool::grow(P.d_rank, P.rank_cap, ntasks, false, "cudaMalloc ranks");
+  IdPool::grow(P.d_skel, P.skel_cap, ntasks * kcap, false, "cudaMalloc skeletons");
+  int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
+  int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
+  int4* d_rc = upload(rc.data(), rc.size(), "upload ID tasks");
+  IdTask* d_tk = upload(tk.data(), tk.size(), "upload ID tasks");
+  const auto t_up = now();
+  auto cleanup = [&] {
+    cudaFree(d_rid);
+    cudaFree(d_cid);
+    cudaFree(d_rc);
+    cudaFree(d_tk);
+  };
+  try {
+    const unsigned nt = static_cast<unsigned>(ntasks);
+    if (rowid)
+      k3_sample_ws<true><<<nt, 256, 0, I.stream>>>(I.k, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+    else
+      k3_sample_ws<false><<<nt, 256, 0, I.stream>>>(I.k, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+    cuda_check(cudaGetLastError(), "k3_sample_ws launch");
+    cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
+               "k5 smem attribute");
+    k5_id<<<(nt + kIdWarps - 1) / kIdWarps, kIdWarps * 32, kIdSmem, I.stream>>>(
+        P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0,
+        P.d_vals, P.d_rank, P.d_skel, kcap);
+    cuda_check(cudaGetLastError(), "k5_id launch");
+    if (timing) cuda_check(cudaStreamSynchronize(I.stream), "ID kernels");
+    const auto t_k = now();
+    if (timing)
+      std::fprintf(stderr, "[id] tasks %lld prep %.2f ms upload+alloc %.2f ms kernels %.2f ms\n",
+                   static_cast<long long>(ntasks), 1e3 * std::chrono::duration<double>(t_prep - t_start).count(),
+                   1e3 * std::chrono::duration<double>(t_up - t_prep).count(),
+                   1e3 * std::chrono::duration<double>(t_k - t_up).count());
+    cuda_check(cudaMemcpyAsync(P.h_vals, P.d_vals, vals * sizeof(double2), cudaMemcpyDeviceToHost, I.stream),
+               "ID values D2H");
+    cuda_check(cudaMemcpyAsync(out.rank.data(), P.d_rank, ntasks * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
+               "ID ranks D2H");
+    cuda_check(
+        cudaMemcpyAsync(out.skel.data(), P.d_skel, ntasks * kcap * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
+        "ID skeletons D2H");
+    cuda_check(cudaStreamSynchronize(I.stream), "ID batch");
+    if (timing)
+      std::fprintf(stderr, "[id] D2H %.2f ms (%lld MB)\n", 1e3 * std::chrono::duration<double>(now() - t_k).count(),
+                   static_cast<long long>(vals * 16 >> 20));
+  } catch (...) {
+    cudaStreamSynchronize(I.stream);
+    cleanup();
+    throw;
+  }
+  cleanup();
+  I.launched_entries += ws;
+  out.vals = reinterpret_cast<const double*>(P.h_vals);
 }
 
 void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g) {
@@ -415,6 +583,56 @@ void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel
 }  // namespace midbf::dev
 
 using midbf::detail::guard;
+
+// Batched column IDs of explicit host blocks (K5 only; midbf_cid_batch).
+extern "C" int midbf_cid_batch(const double* blocks, const int64_t* dims, int64_t nblocks, int64_t k_max, double eps,
+                               int64_t* ranks, int64_t* skel, int64_t kcap, double* vals) {
+  using namespace midbf::dev;
+  return guard([&] {
+    require_device();
+    if (nblocks < 0 || (nblocks > 0 && (!blocks || !dims || !ranks || !skel || !vals)))
+      throw std::invalid_argument("null argument");
+    if (nblocks == 0) return;
+    if (nblocks > 0x7fffffff) throw std::invalid_argument("too many blocks");
+    std::vector<IdTask> tk(static_cast<size_t>(nblocks));
+    int64_t ws = 0, nv = 0;
+    for (int64_t b = 0; b < nblocks; ++b) {
+      const int64_t m = dims[2 * b], n = dims[2 * b + 1];
+      if (m <= 0 || n <= 0 || m * n > 0x7fffffff) throw std::invalid_argument("ID block dimensions out of range");
+      const int64_t full = std::min(m, n), cap = k_max > 0 ? std::min(full, k_max) : full;
+      if (cap > kcap) throw std::invalid_argument("kcap smaller than a block's step cap");
+      tk[b] = IdTask{ws, nv, static_cast<int32_t>(m), static_cast<int32_t>(n)};
+      ws += m * n;
+      nv += cap * n;
+    }
+    IdPool& P = id_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    IdPool::grow(P.d_ws, P.ws_cap, ws, false, "cudaMalloc ID workspace");
+    IdPool::grow(P.d_vals, P.vals_cap, nv, false, "cudaMalloc ID values");
+    IdPool::grow(P.d_rank, P.rank_cap, nblocks, false, "cudaMalloc ranks");
+    IdPool::grow(P.d_skel, P.skel_cap, nblocks * kcap, false, "cudaMalloc skeletons");
+    cuda_check(cudaMemcpy(P.d_ws, blocks, ws * sizeof(double2), cudaMemcpyHostToDevice), "ID blocks H2D");
+    IdTask* d_tk = upload(tk.data(), tk.size(), "upload ID tasks");
+    cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
+               "k5 smem attribute");
+    const unsigned nt = static_cast<unsigned>(nblocks);
+    k5_id<<<(nt + kIdWarps - 1) / kIdWarps, kIdWarps * 32, kIdSmem>>>(
+        P.d_ws, d_tk, static_cast<int>(nblocks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, 0, P.d_vals,
+        P.d_rank, P.d_skel, static_cast<int>(kcap));
+    const cudaError_t e = cudaGetLastError();
+    std::vector<int> r(static_cast<size_t>(nblocks)), sk(static_cast<size_t>(nblocks * kcap), 0);
+    if (e == cudaSuccess) {
+      cuda_check(cudaMemcpy(r.data(), P.d_rank, nblocks * sizeof(int), cudaMemcpyDeviceToHost), "ranks D2H");
+      cuda_check(cudaMemcpy(sk.data(), P.d_skel, nblocks * kcap * sizeof(int), cudaMemcpyDeviceToHost), "skel D2H");
+      cuda_check(cudaMemcpy(vals, P.d_vals, nv * sizeof(double2), cudaMemcpyDeviceToHost), "V D2H");
+    }
+    cudaFree(d_tk);
+    cuda_check(e, "k5_id launch");
+    for (int64_t b = 0; b < nblocks; ++b) ranks[b] = r[b];
+    for (int64_t q = 0; q < nblocks * kcap; ++q) skel[q] = sk[q];
+  });
+}
+
 
 extern "C" int midbf_sample(const midbf_kernel_desc* kernel, int64_t ntasks, const int64_t* tasks,
                             const int64_t* row_ids, int64_t n_row_ids, const int64_t* col_ids, int64_t n_col_ids,

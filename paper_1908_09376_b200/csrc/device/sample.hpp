@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <vector>
 
 extern "C" {
 #include "midbf_b200.h"
@@ -25,6 +26,20 @@ class EntrySampler {
   // Same, each task's block written to its own destination outs[t].
   void sample_blocks(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
                      const int64_t* col_ids, int64_t n_col_ids, double* const* outs);
+  // K3 + K5: sample each task's block into a device workspace and compute
+  // its interpolative decomposition there (column ID of the block, or with
+  // `rowid` a row ID = column ID of its transpose).  Per task: rank (-1: not
+  // computed on the device, recompute on the host), skeleton positions and
+  // the interpolation matrix (V: rank x n, ld rank; W: n x rank, ld n) at
+  // vals + ooff[t].  kcap = skeleton stride.
+  struct IdBatch {
+    std::vector<int> rank, skel;
+    std::vector<int64_t> ooff;
+    int kcap = 0;
+    const double* vals = nullptr;  // pinned, process-wide: valid until the next sample_ids call
+  };
+  void sample_ids(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
+                  const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps, IdBatch& out);
   void direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g);
   int64_t entries_evaluated() const;
 

@@ -14,6 +14,8 @@
 // the reference algorithm's.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <numeric>
@@ -68,6 +70,46 @@ struct FillJob {
   MatXc* out;
 };
 using Filler = std::function<void(std::vector<FillJob>&)>;
+
+// One interpolative decomposition of K(rows, cols): a row ID (W: nr x k,
+// skeleton rows) or a column ID (V: k x nc, skeleton columns).
+struct IdJob {
+  const Index* rows;
+  Index nr;
+  const Index* cols;
+  Index nc;
+};
+struct IdRes {
+  MatXc M;
+  IndexVec pos;
+};
+using IdFn = std::function<void(const std::vector<IdJob>&, bool rowid, std::vector<IdRes>&)>;
+
+// Host IDs (src/butterfly.cpp:466-472, 516-519): fill the blocks, then
+// la::rid_from_cols / la::cid_from_rows under OpenMP.
+void host_ids(const Filler& fill, const Config& cfg, const std::vector<IdJob>& jobs, bool rowid,
+              std::vector<IdRes>& res) {
+  std::vector<MatXc> blk(jobs.size());
+  std::vector<FillJob> fj;
+  fj.reserve(jobs.size());
+  for (size_t q = 0; q < jobs.size(); ++q) fj.push_back({jobs[q].rows, jobs[q].nr, jobs[q].cols, jobs[q].nc, &blk[q]});
+  fill(fj);
+  res.resize(jobs.size());
+  const bool par = cfg.exec == Exec::Parallel;
+#pragma omp parallel for schedule(dynamic) if (par)
+  for (std::int64_t q = 0; q < static_cast<std::int64_t>(jobs.size()); ++q) {
+    if (rowid) {
+      la::RowID id = la::rid_from_cols(blk[q], cfg.rank);
+      res[q].M = std::move(id.W);
+      res[q].pos = std::move(id.skeleton);
+    } else {
+      la::ColumnID id = la::cid_from_rows(blk[q], cfg.rank);
+      res[q].M = std::move(id.V);
+      res[q].pos = std::move(id.skeleton);
+    }
+    blk[q] = MatXc();
+  }
+}
 
 Index lift(const tree::ClusterTree& t, Index node, int from, int to) {
   for (int l = from; l > to; --l) node = t.levels[static_cast<size_t>(l)][static_cast<size_t>(node)].parent;
@@ -140,13 +182,12 @@ struct SweepOut {
   std::vector<System> next;
 };
 
-SweepOut sweep(const Filler& fill, const tree::ClusterTree& tx, const tree::ClusterTree& to, const MatXd& X,
+SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx, const tree::ClusterTree& to, const MatXd& X,
                const MatXd& Om, const Config& cfg, const std::vector<System>& sys, Index nB, int level, bool last,
                std::uint64_t salt, Index stage_rows, Index stage_cols) {
   const Index ns = static_cast<Index>(sys.size());
   const Index nA = ns / std::max<Index>(nB, 1);
   const Index want = cfg.rank.k_max * cfg.t;
-  const bool par = cfg.exec == Exec::Parallel;
   for (Index a = 0; a < nA; ++a)
     for (Index b = 1; b < nB; ++b)
       if (sys[a * nB + b].row.cells.size() != sys[a * nB].row.cells.size())
@@ -174,29 +215,27 @@ SweepOut sweep(const Filler& fill, const tree::ClusterTree& tx, const tree::Clus
     for (Index u = 0; u < static_cast<Index>(sys[s].row.cells.size()); ++u) rjobs.emplace_back(s, u);
   }
   {
-    std::vector<MatXc> blk(rjobs.size());
-    std::vector<FillJob> jobs;
+    std::vector<IdJob> jobs;
+    std::vector<size_t> which;
     for (size_t q = 0; q < rjobs.size(); ++q) {
       const auto [s, u] = rjobs[q];
       const Cell& c = sys[s].row.cells[u];
-      if (c.ids.empty() || csamp[s].empty()) continue;
-      jobs.push_back({c.ids.data(), static_cast<Index>(c.ids.size()), csamp[s].data(),
-                      static_cast<Index>(csamp[s].size()), &blk[q]});
-    }
-    fill(jobs);
-#pragma omp parallel for schedule(dynamic) if (par)
-    for (std::int64_t q = 0; q < static_cast<std::int64_t>(rjobs.size()); ++q) {
-      const auto [s, u] = rjobs[q];
-      const Cell& c = sys[s].row.cells[u];
-      Skel& o = rsk[s][u];
       if (c.ids.empty() || csamp[s].empty()) {
-        o.M = MatXc(static_cast<Index>(c.ids.size()), 0);
+        rsk[s][u].M = MatXc(static_cast<Index>(c.ids.size()), 0);
         continue;
       }
-      la::RowID id = la::rid_from_cols(blk[q], cfg.rank);
-      blk[q] = MatXc();
-      o.M = std::move(id.W);
-      for (Index p : id.skeleton) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
+      jobs.push_back({c.ids.data(), static_cast<Index>(c.ids.size()), csamp[s].data(),
+                      static_cast<Index>(csamp[s].size())});
+      which.push_back(q);
+    }
+    std::vector<IdRes> res;
+    ids(jobs, true, res);
+    for (size_t i = 0; i < which.size(); ++i) {
+      const auto [s, u] = rjobs[which[i]];
+      const Cell& c = sys[s].row.cells[u];
+      Skel& o = rsk[s][u];
+      o.M = std::move(res[i].M);
+      for (Index p : res[i].pos) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
     }
   }
 
@@ -228,29 +267,27 @@ SweepOut sweep(const Filler& fill, const tree::ClusterTree& tx, const tree::Clus
     for (Index w = 0; w < static_cast<Index>(sys[s].col.cells.size()); ++w) cjobs.emplace_back(s, w);
   }
   {
-    std::vector<MatXc> blk(cjobs.size());
-    std::vector<FillJob> jobs;
+    std::vector<IdJob> jobs;
+    std::vector<size_t> which;
     for (size_t q = 0; q < cjobs.size(); ++q) {
       const auto [s, w] = cjobs[q];
       const Cell& c = sys[s].col.cells[w];
-      if (c.ids.empty() || rsamp[s].empty()) continue;
-      jobs.push_back({rsamp[s].data(), static_cast<Index>(rsamp[s].size()), c.ids.data(),
-                      static_cast<Index>(c.ids.size()), &blk[q]});
-    }
-    fill(jobs);
-#pragma omp parallel for schedule(dynamic) if (par)
-    for (std::int64_t q = 0; q < static_cast<std::int64_t>(cjobs.size()); ++q) {
-      const auto [s, w] = cjobs[q];
-      const Cell& c = sys[s].col.cells[w];
-      Skel& o = csk[s][w];
       if (c.ids.empty() || rsamp[s].empty()) {
-        o.M = MatXc(0, static_cast<Index>(c.ids.size()));
+        csk[s][w].M = MatXc(0, static_cast<Index>(c.ids.size()));
         continue;
       }
-      la::ColumnID id = la::cid_from_rows(blk[q], cfg.rank);
-      blk[q] = MatXc();
-      o.M = std::move(id.V);
-      for (Index p : id.skeleton) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
+      jobs.push_back({rsamp[s].data(), static_cast<Index>(rsamp[s].size()), c.ids.data(),
+                      static_cast<Index>(c.ids.size())});
+      which.push_back(q);
+    }
+    std::vector<IdRes> res;
+    ids(jobs, false, res);
+    for (size_t i = 0; i < which.size(); ++i) {
+      const auto [s, w] = cjobs[which[i]];
+      const Cell& c = sys[s].col.cells[w];
+      Skel& o = csk[s][w];
+      o.M = std::move(res[i].M);
+      for (Index p : res[i].pos) o.keep.push_back(c.ids[static_cast<size_t>(p)]);
     }
   }
 
@@ -356,8 +393,8 @@ Factor eye(Index n) {
   return f;
 }
 
-Factorization factorize(const Filler& fill, const tree::ClusterTree& tx, const tree::ClusterTree& to,
-                        const MatXd& X, const MatXd& Om, const Config& cfg) {
+Factorization factorize(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
+                        const tree::ClusterTree& to, const MatXd& X, const MatXd& Om, const Config& cfg) {
   if (tx.dim != to.dim) throw std::invalid_argument("row and column trees have different dimensions");
   if (X.rows() != tx.npoints() || Om.rows() != to.npoints())
     throw std::invalid_argument("point set sizes do not match the trees");
@@ -397,7 +434,7 @@ Factorization factorize(const Filler& fill, const tree::ClusterTree& tx, const t
   std::vector<Factor> Us, Vs;
   Factor S;
   for (int t = 1; t <= T; ++t) {
-    SweepOut o = sweep(fill, tx, to, X, Om, cfg, sys, nB, t, t == T,
+    SweepOut o = sweep(fill, ids, tx, to, X, Om, cfg, sys, nB, t, t == T,
                        mix(cfg.seed ^ mix(static_cast<std::uint64_t>(t))), sr, sc);
     Us.push_back(std::move(o.U));
     Vs.push_back(std::move(o.V));
@@ -460,6 +497,64 @@ Filler device_filler(dev::EntrySampler& smp, FactorizeStats* stats) {
   };
 }
 
+// K3 + K5 on the device; tasks the device does not
+// finish (rank -1) are recomputed with the host IDs on device-sampled blocks.
+IdFn device_ids(dev::EntrySampler& smp, const Filler& fill, const Config& cfg, FactorizeStats* stats) {
+  return [&smp, &fill, &cfg, stats](const std::vector<IdJob>& jobs, bool rowid, std::vector<IdRes>& res) {
+    res.clear();
+    res.resize(jobs.size());
+    if (jobs.empty()) return;
+    std::vector<std::int64_t> tasks(5 * jobs.size());
+    IndexVec rid, cid;
+    for (size_t q = 0; q < jobs.size(); ++q) {
+      tasks[5 * q] = static_cast<std::int64_t>(rid.size());
+      tasks[5 * q + 1] = jobs[q].nr;
+      tasks[5 * q + 2] = static_cast<std::int64_t>(cid.size());
+      tasks[5 * q + 3] = jobs[q].nc;
+      tasks[5 * q + 4] = 0;
+      rid.insert(rid.end(), jobs[q].rows, jobs[q].rows + jobs[q].nr);
+      cid.insert(cid.end(), jobs[q].cols, jobs[q].cols + jobs[q].nc);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    dev::EntrySampler::IdBatch b;
+    smp.sample_ids(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(),
+                   static_cast<std::int64_t>(rid.size()), cid.data(), static_cast<std::int64_t>(cid.size()), rowid,
+                   cfg.rank.k_max, cfg.rank.eps, b);
+    std::vector<IdJob> redo;
+    std::vector<size_t> at;
+    for (size_t q = 0; q < jobs.size(); ++q)
+      if (b.rank[q] < 0) {
+        redo.push_back(jobs[q]);
+        at.push_back(q);
+      }
+#pragma omp parallel for schedule(dynamic, 16)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(jobs.size()); ++q) {
+      const int k = b.rank[q];
+      if (k < 0) continue;
+      const Index r = rowid ? jobs[q].nr : k, c = rowid ? k : jobs[q].nc;
+      res[q].M = MatXc(r, c);
+      if (r * c > 0)
+        std::memcpy(static_cast<void*>(res[q].M.data()), b.vals + b.ooff[q], static_cast<size_t>(16 * r * c));
+      res[q].pos.assign(b.skel.begin() + q * b.kcap, b.skel.begin() + q * b.kcap + k);
+    }
+    static const bool timing = std::getenv("MIDBF_ID_TIMING") != nullptr;
+    if (timing)
+      std::fprintf(stderr, "[id] batch total %.2f ms (incl. copy-out)\n",
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    if (stats) {
+      stats->launches += 1;
+      stats->device_ids += static_cast<std::int64_t>(jobs.size() - redo.size());
+      stats->id_fallbacks += static_cast<std::int64_t>(redo.size());
+      stats->id_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (!redo.empty()) {
+      std::vector<IdRes> rr;
+      host_ids(fill, cfg, redo, rowid, rr);
+      for (size_t i = 0; i < at.size(); ++i) res[at[i]] = std::move(rr[i]);
+    }
+  };
+}
+
 }  // namespace
 
 Index Factor::nnz() const {
@@ -485,21 +580,36 @@ double Factorization::nnz_bound(double c) const {
 
 Factorization idbf_factorize(const EntryFn& K, const tree::ClusterTree& tx, const tree::ClusterTree& to,
                              const MatXd& X, const MatXd& Om, const Config& cfg) {
-  return factorize(host_filler(K, cfg.exec == Exec::Parallel), tx, to, X, Om, cfg);
+  const Filler fill = host_filler(K, cfg.exec == Exec::Parallel);
+  const IdFn ids = [&fill, &cfg](const std::vector<IdJob>& j, bool rowid, std::vector<IdRes>& r) {
+    host_ids(fill, cfg, j, rowid, r);
+  };
+  return factorize(fill, ids, tx, to, X, Om, cfg);
 }
 
 Factorization idbf_factorize(const ker::KernelDesc& K, const tree::ClusterTree& tx, const tree::ClusterTree& to,
                              const MatXd& X, const MatXd& Om, const Config& cfg) {
-  return idbf_factorize_stats(K, tx, to, X, Om, cfg, nullptr);
+  return idbf_factorize_stats(K, tx, to, X, Om, cfg, nullptr, true);
 }
 
 Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,
                                    const tree::ClusterTree& to, const MatXd& X, const MatXd& Om, const Config& cfg,
-                                   FactorizeStats* stats) {
+                                   FactorizeStats* stats, bool device_id) {
   if (K.nrows != X.rows() || K.ncols != Om.rows())
     throw std::invalid_argument("kernel description does not match the point sets");
   dev::EntrySampler smp(K);
-  return factorize(device_filler(smp, stats), tx, to, X, Om, cfg);
+  const Filler fill = device_filler(smp, stats);
+  const IdFn ids = device_id ? device_ids(smp, fill, cfg, stats)
+                             : IdFn([&fill, &cfg](const std::vector<IdJob>& j, bool rowid, std::vector<IdRes>& r) {
+                                 host_ids(fill, cfg, j, rowid, r);
+                               });
+  const auto t0 = std::chrono::steady_clock::now();
+  Factorization F = factorize(fill, ids, tx, to, X, Om, cfg);
+  if (stats) {
+    stats->entries = smp.entries_evaluated();
+    stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return F;
 }
 
 MatXc factor_dense(const Factor& F) {

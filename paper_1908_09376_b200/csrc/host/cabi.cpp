@@ -105,12 +105,14 @@ int midbf_factorize(midbf_fact_t* out, const midbf_kernel_desc* kernel, int64_t 
     cfg.seed = seed;
     cfg.exec = exec ? midbf::Exec::Parallel : midbf::Exec::Serial;
     auto h = std::make_unique<midbf_fact_s>();
-    if (sampler == 0) {
-      h->F = midbf::bf::idbf_factorize_stats(*kernel, tx, to, X, O, cfg, &h->stats);
-    } else {
+    if (sampler == 0 || sampler == 2) {
+      h->F = midbf::bf::idbf_factorize_stats(*kernel, tx, to, X, O, cfg, &h->stats, sampler == 2);
+    } else if (sampler == 1) {
       const midbf_kernel_desc kd = *kernel;
       midbf::bf::EntryFn K = [kd](Index i, Index j) { return midbf::ker::entry(kd, i, j); };
       h->F = midbf::bf::idbf_factorize(K, tx, to, X, O, cfg);
+    } else {
+      throw std::invalid_argument("sampler must be 0, 1 or 2");
     }
     *out = h.release();
   });
@@ -157,6 +159,15 @@ int midbf_fact_stats(midbf_fact_t fact, int64_t* o) {
     o[0] = fact->stats.entries;
     o[1] = fact->stats.launches;
     o[2] = static_cast<int64_t>(fact->stats.sample_seconds * 1e9);  // ns
+  });
+}
+
+int midbf_fact_id_stats(midbf_fact_t fact, int64_t* o) {
+  return guard([&] {
+    o[0] = fact->stats.device_ids;
+    o[1] = fact->stats.id_fallbacks;
+    o[2] = static_cast<int64_t>(fact->stats.id_seconds * 1e9);  // ns
+    o[3] = static_cast<int64_t>(fact->stats.seconds * 1e9);     // ns, whole factorization
   });
 }
 

@@ -12,11 +12,15 @@ struct FactorizeStats {
   std::int64_t entries = 0;   // kernel entries sampled on the device
   std::int64_t launches = 0;  // sampler calls (one per sweep pass)
   double sample_seconds = 0;  // wall time inside the device sampler (kernel + copies)
+  std::int64_t device_ids = 0;    // IDs computed on the device (K5)
+  std::int64_t id_fallbacks = 0;  // IDs the device handed back to the host
+  double id_seconds = 0;          // wall time inside K3 + K5 ID batches (incl. copies)
+  double seconds = 0;             // whole factorization
 };
 
 Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,
                                    const tree::ClusterTree& to, const MatXd& X, const MatXd& Om, const Config& cfg,
-                                   FactorizeStats* stats);
+                                   FactorizeStats* stats, bool device_id);
 
 // Device plan cached inside the factorization; built (or rebuilt with the
 // union of directions) on demand.

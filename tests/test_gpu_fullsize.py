@@ -44,6 +44,8 @@ def test_cfg1_structure_matches_appendix_b(cfg1):
     assert F.max_factor_nnz <= F.nnz_bound(4.0)
     entries, calls, _ = F.sample_stats()
     assert entries == 93388800 and calls == 7
+    ndev, nback, _, _ = F.id_stats()
+    assert ndev == 6144 and nback == 0  # every ID on the device (K5)
 
 
 def test_cfg1_apply_matches_oracle(cfg1):
