@@ -56,34 +56,6 @@ def unit_grid(n, dim):
     return np.stack(np.meshgrid(*([ax] * dim), indexing="ij"), -1).reshape(-1, dim)
 
 
-def lowrank_phase(X, Om, r=8, s=16, seed=7):
-    """configs[2]: rank-r factors A (N x r), B (N x r) of the explicit 2D FIO
-    phase, from s sampled rows/columns (CUR skeleton + truncated SVD, the
-    sampling shape of la::rsvd, src/linalg.cpp:134-219), V <- V*Sigma as
-    src/phase_md.cpp:211-217.  Input generation only (not timed)."""
-    tw = 2 * np.pi
-    c1 = (2 + np.sin(tw * X[:, 0]) * np.sin(tw * X[:, 1])) / 16
-    c2 = (2 + np.cos(tw * X[:, 0]) * np.cos(tw * X[:, 1])) / 16
-
-    def phi(ri, ci):
-        x, w = X[ri], Om[ci]
-        return x @ w.T + np.sqrt((c1[ri, None] * w[None, :, 0]) ** 2 + (c2[ri, None] * w[None, :, 1]) ** 2)
-
-    rng = np.random.default_rng(seed)
-    I = rng.choice(len(X), s, replace=False)
-    J = rng.choice(len(Om), s, replace=False)
-    Cm = phi(np.arange(len(X)), J)          # N x s
-    Rm = phi(I, np.arange(len(Om)))         # s x N
-    Wm = phi(I, J)                          # s x s
-    Qc, _ = np.linalg.qr(Cm)
-    Qr, _ = np.linalg.qr(Rm.T)
-    core = np.linalg.pinv(Qc[I]) @ Wm @ np.linalg.pinv(Qr[J].T)
-    u, sv, vt = np.linalg.svd(core)
-    A = Qc @ u[:, :r]
-    B = (Qr @ vt.T[:, :r]) * sv[:r]
-    return np.ascontiguousarray(A), np.ascontiguousarray(B)
-
-
 def workload(name):
     import paper_1908_09376_b200 as M
 
@@ -101,11 +73,20 @@ def workload(name):
         n = 512
         X = unit_grid(n, 2)
         Om = integer_grid(n, 2)
-        A, B = lowrank_phase(X, Om)
+        # configs[2]: rank-8 phase factors of the explicit 2D FIO phase from
+        # la::rsvd over 16 sampled rows / columns (q = 2), V <- V*Sigma
+        # (src/phase_md.cpp:184-224 with recovery = identity), produced by
+        # this repo's low-rank phase path (Phi rows / columns on the GPU).
+        Kf = M.Kernel(M.KIND_FIO2D, X=X, Omega=Om)
+        t0 = time.perf_counter()
+        A, B, _, _ = M.lowrank_phase(Kf, 8, 2, seed=7)
+        t_phase = time.perf_counter() - t0
+        eps_k = M.eps_K(Kf, A, B, 256, 7)
         # point sets define the trees; entries come only from A, B
         K = _lowrank_kernel(M, X, Om, A, B)
         return K, X, Om, dict(n0=64, k=30), 1, dict(model="MIDBF 2D low-rank phase r=8", n_per_dim=n, N=n * n,
-                                                    k=30, n0=64, t=5, eps=1e-9, xi="integer grid")
+                                                    k=30, n0=64, t=5, eps=1e-9, xi="integer grid",
+                                                    phase=dict(rank=8, q=2, seconds=t_phase, eps_K=eps_k))
     if name == "cfg3":
         n = 32
         X = unit_grid(n, 3)

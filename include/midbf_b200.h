@@ -137,6 +137,27 @@ int midbf_direct_sum(const midbf_kernel_desc* kernel, const double* f, const int
 int midbf_cid_batch(const double* blocks, const int64_t* dims, int64_t nblocks, int64_t k_max, double eps,
                     int64_t* ranks, int64_t* skel, int64_t kcap, double* vals);
 
+/* ------------------------------------------- low-rank phase
+ * la::thin_q / la::pinv / la::rsvd (src/linalg.cpp:109-219) on dense host
+ * matrices (column-major; complex interleaved when is_complex), the
+ * explicit-phase low_rank_phase_factorization (src/phase_md.cpp:184-224,
+ * recovery = identity for closed-form phases; rows / columns of Phi
+ * evaluated on the GPU) and metrics::eps_K (src/metrics.cpp:55-86, entries
+ * sampled on the GPU).  thin_q: Q is m x min(m,n).  pinv: P is n x m, cond =
+ * sigma_max / sigma_min.  rsvd_dense: U m x r, S r, V n x r (zero-padded past
+ * the returned rank); rng = std::mt19937_64(seed) draws the enlargement
+ * sets; info = {rank, rows evaluated, cols evaluated, ill conditioned}.
+ * lowrank_phase: rng = std::mt19937_64(seed) draws R, C then rsvd's sets;
+ * U nrows x r, V ncols x r (V scaled by S); info = {rank, rows, cols}. */
+int midbf_thin_q(const double* A, int64_t m, int64_t n, int is_complex, double* Q);
+int midbf_pinv(const double* A, int64_t m, int64_t n, int is_complex, double rel_cutoff, double* P, double* cond);
+int midbf_rsvd_dense(const double* A, int64_t m, int64_t n, int is_complex, const int64_t* R0, const int64_t* C0,
+                     int64_t s, int64_t r, uint64_t seed, double* U, double* S, double* V, int64_t* info);
+int midbf_lowrank_phase(const midbf_kernel_desc* kernel, int64_t r, int64_t q, uint64_t seed, double* U, double* V,
+                        int64_t* info);
+int midbf_eps_K(const midbf_kernel_desc* kernel, const double* U, const double* V, int64_t r, int64_t nsamp,
+                uint64_t seed, double* out);
+
 /* ------------------------------------------- host factorization object
  * bf::idbf_factorize (src/butterfly.cpp:708-769) with trees built the way
  * the reference tests and experiment do (both sides at a common depth,

@@ -59,6 +59,7 @@ def lib():
         L.orc_mock_cheb_rows.restype = i64
         L.orc_mock_cheb_points.restype = i64
         L.orc_rand_subset.restype = i64
+        L.orc_rand_subset_seq.restype = i64
         L.orc_fio2d_phase.restype = C.c_double
         L.orc_fio3d_phase.restype = C.c_double
         _lib = L
@@ -350,6 +351,20 @@ def mock_chebyshev_points(P, s, seed):
     out = np.empty(max(P.shape[0], s), dtype=np.int64)
     n = lib().orc_mock_cheb_points(_p(P), i64(P.shape[0]), P.shape[1], i64(s), u64(seed), _ip(out))
     return out[:n].copy()
+
+
+def rand_subset_seq(seed, draws):
+    """[(n, k), ...] drawn in order from one std::mt19937_64(seed)."""
+    ns = np.array([d[0] for d in draws], dtype=np.int64)
+    ks = np.array([d[1] for d in draws], dtype=np.int64)
+    out = np.empty(max(1, int(np.minimum(ns, ks).sum())), dtype=np.int64)
+    lib().orc_rand_subset_seq(u64(seed), i64(len(draws)), _ip(ns), _ip(ks), _ip(out))
+    res, off = [], 0
+    for n, k in draws:
+        c = min(n, k)
+        res.append(out[off: off + c].copy())
+        off += c
+    return res
 
 
 def rand_subset(n, k, seed):

@@ -281,4 +281,20 @@ std::int64_t orc_rand_subset(std::int64_t n, std::int64_t k, std::uint64_t seed,
   return static_cast<std::int64_t>(r.size());
 }
 
+// Several rand_subset draws in sequence from ONE std::mt19937_64(seed), as
+// consecutive calls on one engine (low_rank_phase_factorization / rsvd /
+// eps_K draw their index sets this way, src/phase_md.cpp:198-199,
+// src/linalg.cpp:186-189, src/metrics.cpp:61-71).  Outputs concatenated.
+std::int64_t orc_rand_subset_seq(std::uint64_t seed, std::int64_t ndraw, const std::int64_t* ns,
+                                 const std::int64_t* ks, std::int64_t* out) {
+  std::mt19937_64 rng(seed);
+  std::int64_t off = 0;
+  for (std::int64_t d = 0; d < ndraw; ++d) {
+    IndexVec r = rand_subset(ns[d], ks[d], rng);
+    std::memcpy(out + off, r.data(), 8 * r.size());
+    off += static_cast<std::int64_t>(r.size());
+  }
+  return off;
+}
+
 }  // extern "C"

@@ -402,6 +402,77 @@ def cid_batch(blocks, k_max, eps):
     return out
 
 
+# ---- low-rank phase production (csrc/host/lowrank.cpp)
+def _dense(A):
+    """Column-major flat copy (float64 view) of a real or complex matrix."""
+    cplx = np.iscomplexobj(A)
+    A = np.asarray(A, dtype=np.complex128 if cplx else np.float64)
+    flat = np.ascontiguousarray(A.reshape(-1, order="F"))
+    return flat.view(np.float64), A.shape, A.dtype, cplx
+
+
+def _out(shape, dtype):
+    return np.zeros(int(np.prod(shape)), dtype=dtype)
+
+
+def _shaped(buf, shape):
+    return buf.reshape(shape, order="F")
+
+
+def thin_q(A):
+    """la::thin_q: orthonormal basis of range(A), m x min(m, n)."""
+    a, (m, n), dt, cplx = _dense(A)
+    Q = _out((m, min(m, n)), dt)
+    _check(lib().midbf_thin_q(_p(a), i64(m), i64(n), 1 if cplx else 0, _p(Q.view(np.float64))))
+    return _shaped(Q, (m, min(m, n)))
+
+
+def pinv(A, rel_cutoff=1e-12):
+    """la::pinv -> (pseudoinverse, sigma_max / sigma_min)."""
+    a, (m, n), dt, cplx = _dense(A)
+    P = _out((n, m), dt)
+    cond = C.c_double()
+    _check(lib().midbf_pinv(_p(a), i64(m), i64(n), 1 if cplx else 0, C.c_double(rel_cutoff),
+                            _p(P.view(np.float64)), C.byref(cond)))
+    return _shaped(P, (n, m)), cond.value
+
+
+def rsvd_dense(A, R0, C0, r, seed):
+    """la::rsvd on a dense matrix (std::mt19937_64(seed) draws the enlarged
+    index sets) -> U, S, V, rows_evaluated, cols_evaluated, ill_conditioned."""
+    a, (m, n), dt, cplx = _dense(A)
+    R0 = np.ascontiguousarray(R0, dtype=np.int64)
+    C0 = np.ascontiguousarray(C0, dtype=np.int64)
+    U, V, S = _out((m, r), dt), _out((n, r), dt), np.zeros(r)
+    info = np.zeros(4, dtype=np.int64)
+    _check(lib().midbf_rsvd_dense(_p(a), i64(m), i64(n), 1 if cplx else 0, _ip(R0), _ip(C0), i64(len(R0)), i64(r),
+                                  u64(seed), _p(U.view(np.float64)), _p(S), _p(V.view(np.float64)), _ip(info)))
+    k = int(info[0])
+    return _shaped(U, (m, r))[:, :k], S[:k], _shaped(V, (n, r))[:, :k], int(info[1]), int(info[2]), bool(info[3])
+
+
+def lowrank_phase(kernel, r, q=2, seed=0):
+    """phase::low_rank_phase_factorization of the kernel's closed-form phase
+    (rows / columns of Phi on the GPU) -> U (nrows x k), V (ncols x k, scaled
+    by S), rows_evaluated, cols_evaluated."""
+    U, V = np.zeros(kernel.nrows * r), np.zeros(kernel.ncols * r)
+    info = np.zeros(3, dtype=np.int64)
+    _check(lib().midbf_lowrank_phase(C.byref(kernel.desc), i64(r), i64(q), u64(seed), _p(U), _p(V), _ip(info)))
+    k = int(info[0])
+    return (_shaped(U, (kernel.nrows, r))[:, :k], _shaped(V, (kernel.ncols, r))[:, :k], int(info[1]),
+            int(info[2]))
+
+
+def eps_K(kernel, U, V, nsamp=256, seed=0):
+    """metrics::eps_K of a low-rank phase U V^T against the kernel (GPU entries)."""
+    r = np.shape(U)[1]
+    u, _, _, _ = _dense(np.asarray(U, dtype=np.float64))
+    v, _, _, _ = _dense(np.asarray(V, dtype=np.float64))
+    out = C.c_double()
+    _check(lib().midbf_eps_K(C.byref(kernel.desc), _p(u), _p(v), i64(r), i64(nsamp), u64(seed), C.byref(out)))
+    return out.value
+
+
 def idbf_factorize(kernel, n0, k=30, eps=1e-9, t=5, seed=0, parallel=True, sampler="device", ids="device"):
     """bf::idbf_factorize on trees built at a common depth from the kernel's
     point sets.  sampler="device": every entry from the GPU sampler (K3);

@@ -57,7 +57,9 @@ __device__ __forceinline__ double2 polar1(double phi) {
   return make_double2(c, s);
 }
 
-__device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
+// Phi(x_i, xi_j) of the kernels that have one (FIO 2D/3D, low-rank A.B^T,
+// x.xi), reference operation order, non-contracted.
+__device__ __forceinline__ double phase_of(const DevK& k, int64_t i, int64_t j) {
   switch (k.kind) {
     case MIDBF_KERNEL_FIO2D: {
       const double x0 = k.X[2 * i], x1 = k.X[2 * i + 1];
@@ -66,7 +68,7 @@ __device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
       const double lin = __dadd_rn(__dmul_rn(x0, w0), __dmul_rn(x1, w1));
       const double q = __dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(c1, c1), w0), w0),
                                  __dmul_rn(__dmul_rn(__dmul_rn(c2, c2), w1), w1));
-      return polar1(__dadd_rn(lin, __dsqrt_rn(q)));
+      return __dadd_rn(lin, __dsqrt_rn(q));
     }
     case MIDBF_KERNEL_FIO3D: {
       const double* x = k.X + 3 * i;
@@ -76,25 +78,43 @@ __device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
       const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(__dmul_rn(a[0], a[0]), w[0]), w[0]),
                                            __dmul_rn(__dmul_rn(__dmul_rn(a[1], a[1]), w[1]), w[1])),
                                  __dmul_rn(__dmul_rn(__dmul_rn(a[2], a[2]), w[2]), w[2]));
-      return polar1(__dadd_rn(lin, __dsqrt_rn(q)));
+      return __dadd_rn(lin, __dsqrt_rn(q));
     }
     case MIDBF_KERNEL_LOWRANK: {
       double s = 0.0;
       for (int q = 0; q < k.rank; ++q) s = __dadd_rn(s, __dmul_rn(k.A[i * k.rank + q], k.B[j * k.rank + q]));
-      return polar1(s);
+      return s;
     }
-    case MIDBF_KERNEL_NUFFT: {
+    default: {  // NUFFT: x . xi
       double s = 0.0;
       for (int q = 0; q < k.dim; ++q) s = __dadd_rn(s, __dmul_rn(k.X[i * k.dim + q], k.Om[j * k.dim + q]));
-      return polar1(s);
+      return s;
     }
+  }
+}
+
+__device__ __forceinline__ double2 entry(const DevK& k, int64_t i, int64_t j) {
+  switch (k.kind) {
     case MIDBF_KERNEL_CONST:
       return make_double2(k.cre, k.cim);
-    default: {  // RANK1
+    case MIDBF_KERNEL_RANK1: {
       const double2 a = k.u[i], b = k.v[j];
       return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
                           __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
     }
+    default:
+      return polar1(phase_of(k, i, j));
+  }
+}
+
+// Phi(rows, cols) block, column-major (rid / cid null: 0..n-1).
+__global__ void __launch_bounds__(256) k3_phase(DevK k, const int* __restrict__ rid, int nr,
+                                                const int* __restrict__ cid, int nc, double* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(nr) * nc;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(e / nr), r = static_cast<int>(e - static_cast<int64_t>(c) * nr);
+    out[e] = phase_of(k, rid ? rid[r] : r, cid ? cid[c] : c);
   }
 }
 
@@ -546,6 +566,48 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   cleanup();
   I.launched_entries += ws;
   out.vals = reinterpret_cast<const double*>(P.h_vals);
+}
+
+void EntrySampler::phase_block(int64_t nr, const int64_t* rows, int64_t nc, const int64_t* cols, double* out) {
+  Impl& I = *impl_;
+  const int kind = I.k.kind;
+  if (kind != MIDBF_KERNEL_FIO2D && kind != MIDBF_KERNEL_FIO3D && kind != MIDBF_KERNEL_LOWRANK &&
+      kind != MIDBF_KERNEL_NUFFT)
+    throw std::invalid_argument("this kernel has no phase");
+  if (nr <= 0 || nc <= 0) return;
+  if (nr > 0x7fffffff || nc > 0x7fffffff) throw std::invalid_argument("phase block too large");
+  auto ids = [](const int64_t* v, int64_t n, int64_t lim, const char* what) {
+    std::vector<int> o;
+    if (!v) return o;
+    o.resize(static_cast<size_t>(n));
+    for (int64_t q = 0; q < n; ++q) {
+      if (v[q] < 0 || v[q] >= lim) throw std::invalid_argument(what);
+      o[q] = static_cast<int>(v[q]);
+    }
+    return o;
+  };
+  if (!rows && nr > I.nrows) throw std::invalid_argument("phase rows out of range");
+  if (!cols && nc > I.ncols) throw std::invalid_argument("phase columns out of range");
+  const std::vector<int> r = ids(rows, nr, I.nrows, "phase row out of range");
+  const std::vector<int> c = ids(cols, nc, I.ncols, "phase column out of range");
+  I.ensure_stream();
+  int* d_r = rows ? upload(r.data(), r.size(), "upload phase rows") : nullptr;
+  int* d_c = cols ? upload(c.data(), c.size(), "upload phase cols") : nullptr;
+  double* d_out = nullptr;
+  const cudaError_t e0 = cudaMalloc(&d_out, nr * nc * sizeof(double));
+  if (e0 == cudaSuccess) {
+    const int64_t blocks = std::min<int64_t>((nr * nc + 255) / 256, 148 * 16);
+    k3_phase<<<static_cast<unsigned>(blocks), 256, 0, I.stream>>>(I.k, d_r, static_cast<int>(nr), d_c,
+                                                                   static_cast<int>(nc), d_out);
+  }
+  cudaError_t e = e0 != cudaSuccess ? e0 : cudaGetLastError();
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, d_out, nr * nc * sizeof(double), cudaMemcpyDeviceToHost, I.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(I.stream);
+  cudaFree(d_out);
+  cudaFree(d_r);
+  cudaFree(d_c);
+  cuda_check(e, "phase block");
 }
 
 void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g) {

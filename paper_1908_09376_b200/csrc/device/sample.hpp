@@ -40,6 +40,9 @@ class EntrySampler {
   };
   void sample_ids(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
                   const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps, IdBatch& out);
+  // Phi(rows, cols) (real, column-major nr x nc; rows / cols null: 0..n-1)
+  // for the kernels with a phase (FIO 2D/3D, low-rank, x.xi).
+  void phase_block(int64_t nr, const int64_t* rows, int64_t nc, const int64_t* cols, double* out);
   void direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g);
   int64_t entries_evaluated() const;
 
