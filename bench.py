@@ -56,6 +56,20 @@ def unit_grid(n, dim):
     return np.stack(np.meshgrid(*([ax] * dim), indexing="ij"), -1).reshape(-1, dim)
 
 
+def measured_traffic(config, launches):
+    """DRAM bytes per launch of this workload's dominant kernel from the
+    committed ncu capture (profiles/r1_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    try:
+        with open(path) as fh:
+            rec = json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None
+    if not rec or launches != 1:
+        return None
+    return rec["dram_bytes_per_launch"]
+
+
 def workload(name):
     import paper_1908_09376_b200 as M
 
@@ -306,9 +320,10 @@ def main():
     hbm, peak_kind = peaks()
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
     launches = plan.launches(nrhs)
+    traffic = measured_traffic(args.config, launches)
     if nrhs == 1:
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes_per_apply": alg_bytes,
+                    "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_apply": alg_bytes,
                     "note": "achieved = (16*total_nnz + 16*(N_in+N_out)) / apply time; one apply = "
                             f"{launches} k1_flow launch in one CUDA graph"}
     else:
@@ -316,9 +331,10 @@ def main():
         tf = flops / (ms_step * 1e-3) / 1e12
         roofline = {"bound": "tensor", "achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                     "frac": tf / FP64_DMMA_TFLOPS, "peak_kind": "measured (tools/fp64_probe.cu, DMMA m8n8k4)",
-                    "traffic": None, "algorithmic_flops_per_apply": flops, "hbm_gbs": achieved,
+                    "traffic": traffic, "algorithmic_flops_per_apply": flops, "hbm_gbs": achieved,
                     "hbm_frac": achieved / hbm,
-                    "note": f"FP64 tensor-core (DMMA) K2 path, {launches} stage launches per apply in one graph"}
+                    "note": f"FP64 tensor-core (DMMA) k2_flow: {launches} cooperative dataflow launch(es) per "
+                            "apply (one per 64-RHS slice) in one graph; traffic = DRAM bytes per launch"}
     line = {
         "metric": "MIDBF matvecs/s at 2D N=256^2 (HBM roofline fraction); rel-L2 err vs ref",
         "value": replica_throughput(world, nrhs, ms_step),
