@@ -245,13 +245,15 @@ class DevicePlan:
             lib().midbf_plan_destroy(self._h)
             self._h = None
 
-    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True):
+    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
-        64-RHS slice (dmma_flow) or one launch per stage."""
+        64-RHS slice (dmma_flow) or one launch per stage.  variant: k1_flow
+        layout 0 (4 warp pairs x 3 x 16 KB), 1 (8 x 2 x 8 KB), 2 (6 x 4 x
+        8 KB), 3 chosen by the plan's size (default)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
-        f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192)
+        f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4)
         _check(lib().midbf_plan_set_flags(self._h, f))
 
     def launches(self, nrhs=1, transpose=False):

@@ -400,7 +400,7 @@ Plan::Plan(const PlanTables& T, unsigned directions) {
   flow_grid[0] = flow_setup<4, 3, 16384>(num_sms);
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
   flow_grid[2] = flow_setup<6, 4, 8192>(num_sms);
-  flow_grid[3] = flow_grid[0];
+  flow_grid[3] = flow_grid[0];  // unused: variant 3 resolves per direction (flow_variant)
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
   cuda_check(cudaFuncSetAttribute(k2_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2FSmem)),
@@ -446,6 +446,19 @@ Plan::~Plan() {
   cudaFree(d_io[1]);
 }
 
+// k1_flow variant: flags bits 4-5 (0: 4 pairs x 3 x 16 KB, 1: 8 x 2 x 8 KB,
+// 2: 6 x 4 x 8 KB), 3 = by size: measured at cfg1 (358 MB of panels) variant
+// 0 is fastest (66.5 vs 74.7 us), at cfg3 / cfg2 (872 / 1726 MB) variant 1
+// (135.7 vs 140.6, 275.1 vs 287.2 us) -- more warps pay off once every
+// warp streams enough panels to amortise its pipeline start and stage waits.
+int Plan::flow_variant(int d) const {
+  const int v = static_cast<int>((flags >> 4) & 3u);
+  if (v != 3) return v;
+  int64_t bytes = 0;
+  for (const auto& st : dir[d].stages) bytes += st.payload_bytes;
+  return bytes > (int64_t{512} << 20) ? 1 : 0;
+}
+
 bool Plan::flow_ok(int d, int64_t nrhs) const {
   return nrhs == 1 && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
 }
@@ -477,7 +490,7 @@ void Plan::ensure_buffers(int64_t nrhs) {
 
 void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stream) {
   Direction& D = dir[d];
-  const int variant = static_cast<int>((flags >> 4) & 3u);
+  const int variant = flow_variant(d);
   FlowParams P{};
   P.ctxs = static_cast<const StripCtx*>(D.d_ctx);
   P.strips = D.d_strips;
@@ -670,7 +683,7 @@ void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStre
 // assume one grid size; a variant switch re-initialises them, outside any
 // stream capture and after all earlier work.
 void Plan::prepare_flow(int d) {
-  const int grid = flow_grid[(flags >> 4) & 3u];
+  const int grid = flow_grid[flow_variant(d)];
   if (last_grid[d] == grid) return;
   Direction& D = dir[d];
   cuda_check(cudaDeviceSynchronize(), "flow reset sync");

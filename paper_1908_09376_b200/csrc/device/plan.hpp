@@ -115,13 +115,14 @@ class Plan {
   // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS),
   // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel,
   // bits14-15 k2_flow timing experiments (k2flow.cuh, results invalid).
-  unsigned flags = 0xF;  // default: k1_flow variant 0 (4 pairs x 3 x 16 KB), fastest measured at cfg1
+  unsigned flags = 0x3F;  // default: k1_flow variant chosen by size (flow_variant), graphs, PDL, prefetch
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
   int strip_rows = 32;  // output rows per strip (one warp's lanes)
   long long* d_prof = nullptr;  // k1_flow phase timers (flag bit 12)
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
+  int flow_variant(int d) const;
   bool k2_ok(int d, int64_t nrhs) const;
   bool k2flow_ok(int d, int64_t nrhs) const;
   int k2flow_grid = 0;

@@ -84,6 +84,26 @@ def test_multi_rhs_fallback_paths(pair, path):
     assert rel(default, want) <= TOL
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, "stages"])
+def test_single_rhs_kernel_variants(pair, variant):
+    """Every k1_flow layout (the size-based default picks 0 or 1) and the
+    per-stage fallback (k1_stage) match the oracle, both directions."""
+    name, K, Fo, Fm, plan = pair
+    f, g = cvec(Fo.ncols, 19), cvec(Fo.nrows, 20)
+    try:
+        if variant == "stages":
+            plan.set_flags(flow=False)
+        else:
+            plan.set_flags(variant=variant)
+        a, b = plan.apply(f), plan.apply(g, transpose=True)
+    finally:
+        plan.set_flags()
+    assert rel(a, Fo.apply(f)) <= TOL
+    assert rel(b, Fo.apply_transpose(g)) <= TOL
+    if variant != "stages":
+        assert plan.launches(1) == 1
+
+
 def test_runs_are_bitwise_identical(pair):
     name, K, Fo, Fm, plan = pair
     f = cvec(Fo.ncols, 14)
