@@ -84,6 +84,14 @@ int midbf_plan_create(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int
                       const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
                       const int64_t* blocks, const int64_t* groups, const double* payload,
                       unsigned directions);
+/* Same, with one payload pointer per block (block b of factor i at
+ * block_payloads[sum of earlier factors' block counts + b], column-major
+ * complex rows x cols): a factorization whose blocks live in separate
+ * allocations (the reference's FactorBlock matrices) needs no host packing. */
+int midbf_plan_create_blocks(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int64_t* row_perm,
+                             const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
+                             const int64_t* blocks, const int64_t* groups, const double* const* block_payloads,
+                             unsigned directions);
 /* MIDBF001 container straight into a device plan
  * (replaces bf::load_factorization, src/butterfly_io.cpp:103-167). */
 int midbf_plan_load(midbf_plan_t* out, const char* path, unsigned directions);

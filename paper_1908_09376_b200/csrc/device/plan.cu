@@ -33,9 +33,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -43,6 +46,7 @@
 
 #include "common.cuh"
 #include "plan.hpp"
+#include "pool.hpp"
 #include "flow.cuh"
 #include "k2.cuh"
 #include "k2flow.cuh"
@@ -166,9 +170,9 @@ __global__ void __launch_bounds__(kWarps * 32) k1_stage(const Strip* __restrict_
 
 struct EffBlock {
   int64_t yoff, xoff, m, n;  // as applied in this direction
-  const double* data;        // original column-major block payload (complex)
+  int64_t raw;               // offset of the column-major block payload in the raw upload (complex)
   int64_t ld;                // original row count
-  bool tr;                   // panel(i,c) = data[c + i*ld] when transposed
+  bool tr;                   // panel(i,c) = block(c, i) when transposed
   int64_t order;
 };
 
@@ -209,19 +213,111 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
 
 }  // namespace
 
+// One panel of the device arena cut out of the raw block payload: panel(i, c)
+// = block(r0 + i, c), or block(c, r0 + i) for the transpose direction.
+struct PanelJob {
+  int64_t dst;  // arena offset (complex)
+  int64_t src;  // raw offset of the block (complex, column-major, leading dim ld)
+  int32_t h, n, ld, r0, tr, pad_;
+};
+
+// K0: one warp per panel, lanes over rows, columns in order (coalesced
+// stores; the transposed gathers read rows of the block from L2).
+__global__ void __launch_bounds__(256) k0_repack(const PanelJob* __restrict__ jobs, int64_t njobs,
+                                                 const double2* __restrict__ raw, double2* __restrict__ arena) {
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= njobs) return;
+  const PanelJob J = jobs[j];
+  for (int c = 0; c < J.n; ++c)
+    for (int i = lane; i < J.h; i += 32) {
+      const int64_t r = J.r0 + i;
+      arena[J.dst + static_cast<int64_t>(c) * J.h + i] =
+          raw[J.src + (J.tr ? c + r * J.ld : r + static_cast<int64_t>(c) * J.ld)];
+    }
+}
+
+// Every block's payload, factor by factor, packed back to back on the device
+// (chunks of whole blocks copied in parallel into pinned memory while the
+// previous chunk uploads).  offs[f][b] = complex offset of block b of factor f.
+double2* upload_raw(const PlanTables& T, std::vector<std::vector<int64_t>>& offs) {
+  offs.assign(T.factors.size(), {});
+  struct Blk {
+    const double* src;
+    int64_t off, n;  // complex entries
+  };
+  std::vector<Blk> blks;
+  int64_t total = 0;
+  for (size_t f = 0; f < T.factors.size(); ++f) {
+    const FactorView& F = T.factors[f];
+    offs[f].resize(static_cast<size_t>(F.nblocks), 0);
+    for (int64_t b = 0; b < F.nblocks; ++b) {
+      const int64_t n = F.blocks[4 * b + 2] * F.blocks[4 * b + 3];
+      offs[f][static_cast<size_t>(b)] = total;
+      if (n > 0) blks.push_back({F.payload[static_cast<size_t>(b)], total, n});
+      total += n;
+    }
+  }
+  double2* d_raw = nullptr;
+  cuda_check(cudaMalloc(&d_raw, std::max<int64_t>(total, 1) * sizeof(double2)), "cudaMalloc raw payload");
+  PinnedPool& P = pinned_pool();
+  std::lock_guard<std::mutex> lock(P.mu);
+  P.ensure();
+  cudaStream_t stream;
+  cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+  const int64_t cap = static_cast<int64_t>(PinnedPool::kBytes / sizeof(double2));
+  size_t i = 0;
+  int buf = 0, used = 0;
+  try {
+    while (i < blks.size()) {
+      // chunk = whole blocks up to the buffer size (a larger block goes alone, in pieces)
+      size_t e = i;
+      int64_t n = 0;
+      while (e < blks.size() && (e == i || n + blks[e].n <= cap) && n < cap) n += blks[e++].n;
+      if (used >= 2) cuda_check(cudaEventSynchronize(P.ev[buf]), "upload buffer reuse");
+      const int64_t base = blks[i].off;
+      if (n <= cap) {
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t q = static_cast<int64_t>(i); q < static_cast<int64_t>(e); ++q)
+          std::memcpy(P.h[buf] + (blks[q].off - base) * sizeof(double2), blks[q].src, blks[q].n * sizeof(double2));
+        cuda_check(cudaMemcpyAsync(d_raw + base, P.h[buf], n * sizeof(double2), cudaMemcpyHostToDevice, stream),
+                   "raw payload H2D");
+        cuda_check(cudaEventRecord(P.ev[buf], stream), "event");
+        buf ^= 1;
+        ++used;
+      } else {  // one block larger than the buffer: synchronous pieces
+        cuda_check(cudaStreamSynchronize(stream), "raw payload");
+        cuda_check(cudaMemcpy(d_raw + base, blks[i].src, n * sizeof(double2), cudaMemcpyHostToDevice),
+                   "raw payload H2D");
+      }
+      i = e;
+    }
+    cuda_check(cudaStreamSynchronize(stream), "raw payload upload");
+  } catch (...) {
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+    cudaFree(d_raw);
+    throw;
+  }
+  cudaStreamDestroy(stream);
+  return d_raw;
+}
+
 // Build one direction (forward or transpose) of the plan on the host and
 // upload it.  Strip construction is general (ragged, overlapping and
 // uncovered rows): breakpoints at every block edge, active blocks in the
 // reference's serial order (groups in order, blocks in group order).
-void Plan::build_direction(int d, const PlanTables& T) {
+void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
+                           const std::vector<std::vector<int64_t>>& raw_off) {
   Direction& D = dir[d];
+  const auto t_begin = std::chrono::steady_clock::now();
   const int64_t nf = T.nfactors;
   if (nf > kMaxStages) throw std::invalid_argument("too many factors for one device plan");
   D.stages.clear();
   std::vector<Strip> strips;
   std::vector<Seg> segs;
-  std::vector<double> arena;
-  arena.reserve(static_cast<size_t>(2 * T.total_nnz));
+  std::vector<PanelJob> jobs;
+  int64_t arena_len = 0;  // complex entries
   // stage buffer layout: [permuted input of stage 0 | output of stage 0 | ...]
   D.in_len = d == 0 ? T.factors[static_cast<size_t>(nf - 1)].cols : T.factors[0].rows;
   int64_t bufoff = std::max<int64_t>(D.in_len, 1);
@@ -233,7 +329,7 @@ void Plan::build_direction(int d, const PlanTables& T) {
     stg.out_len = d == 0 ? F.rows : F.cols;
     stg.in_len = d == 0 ? F.cols : F.rows;
     stg.strip0 = static_cast<int32_t>(strips.size());
-    stg.arena0 = static_cast<int64_t>(arena.size() / 2);
+    stg.arena0 = arena_len;
     stg.buf_off = bufoff;
     if (s + 1 < nf) bufoff += std::max<int64_t>(stg.out_len, 1);
     if (s > 0 && stg.in_len != D.stages.back().out_len)
@@ -246,7 +342,7 @@ void Plan::build_direction(int d, const PlanTables& T) {
         if (bd[2] == 0 || bd[3] == 0) continue;
         EffBlock e;
         e.ld = bd[2];
-        e.data = F.payload[static_cast<size_t>(b)];
+        e.raw = raw_off[static_cast<size_t>(fi)][static_cast<size_t>(b)];
         e.order = ord++;
         e.tr = d != 0;
         e.yoff = d == 0 ? bd[0] : bd[1];
@@ -316,22 +412,14 @@ void Plan::build_direction(int d, const PlanTables& T) {
           // 128-byte aligned panels: every full TMA chunk (h x 32 columns)
           // then starts on a cache-line boundary (unaligned bulk copies
           // stream at a fraction of the rate, tools/bw_probe.cu)
-          arena.resize((arena.size() + 15) & ~size_t(15), 0.0);
-          sg.off = static_cast<int64_t>(arena.size() / 2);
+          arena_len = (arena_len + 7) & ~int64_t(7);
+          sg.off = arena_len;
           sg.x0 = static_cast<int32_t>(e.xoff);
           sg.n = static_cast<int32_t>(e.n);
           deps(e.xoff, e.n, sg.dep0, sg.dep1);
-          const int64_t r0 = y - e.yoff;
-          const size_t base = arena.size();
-          arena.resize(base + static_cast<size_t>(2 * h * e.n));
-          double* dst = arena.data() + base;
-          for (int64_t c = 0; c < e.n; ++c)
-            for (int i = 0; i < h; ++i) {
-              const int64_t r = r0 + i;
-              const double* src = e.tr ? e.data + 2 * (c + r * e.ld) : e.data + 2 * (r + c * e.ld);
-              dst[2 * (c * h + i)] = src[0];
-              dst[2 * (c * h + i) + 1] = src[1];
-            }
+          jobs.push_back({arena_len, e.raw, h, static_cast<int32_t>(e.n), static_cast<int32_t>(e.ld),
+                          static_cast<int32_t>(y - e.yoff), e.tr ? 1 : 0, 0});
+          arena_len += static_cast<int64_t>(h) * e.n;
           segs.push_back(sg);
           ++st.nseg;
           st.xcols += sg.n;
@@ -341,14 +429,15 @@ void Plan::build_direction(int d, const PlanTables& T) {
       }
     }
     stg.nstrips = static_cast<int32_t>(strips.size()) - stg.strip0;
-    stg.payload_bytes = 16 * (static_cast<int64_t>(arena.size() / 2) - stg.arena0);
+    stg.payload_bytes = 16 * (arena_len - stg.arena0);
     D.stages.push_back(stg);
   }
   if (strips.size() > 0x7ffffff0 || segs.size() > 0x7ffffff0)
     throw std::invalid_argument("factorization too large for one device plan");
+  const auto t_meta = std::chrono::steady_clock::now();
   D.nstrips = static_cast<int64_t>(strips.size());
   D.nsegs = static_cast<int64_t>(segs.size());
-  D.arena_elems = static_cast<int64_t>(arena.size() / 2);
+  D.arena_elems = arena_len;
   D.stagebuf_elems = std::max<int64_t>(bufoff, 1);
   auto up = [](void** dptr, const void* src, size_t bytes, const char* what) {
     cuda_check(cudaMalloc(dptr, std::max<size_t>(bytes, 16)), what);
@@ -356,7 +445,18 @@ void Plan::build_direction(int d, const PlanTables& T) {
   };
   up(reinterpret_cast<void**>(&D.d_strips), strips.data(), strips.size() * sizeof(Strip), "upload strips");
   up(reinterpret_cast<void**>(&D.d_segs), segs.data(), segs.size() * sizeof(Seg), "upload segs");
-  up(reinterpret_cast<void**>(&D.d_arena), arena.data(), arena.size() * sizeof(double), "upload arena");
+  // panels cut out of the raw payload on the device (K0)
+  cuda_check(cudaMalloc(&D.d_arena, std::max<int64_t>(arena_len, 1) * sizeof(double2)), "cudaMalloc arena");
+  if (!jobs.empty()) {
+    PanelJob* d_jobs = nullptr;
+    up(reinterpret_cast<void**>(&d_jobs), jobs.data(), jobs.size() * sizeof(PanelJob), "upload panel jobs");
+    const int64_t nj = static_cast<int64_t>(jobs.size());
+    k0_repack<<<static_cast<unsigned>((nj * 32 + 255) / 256), 256>>>(d_jobs, nj, d_raw, D.d_arena);
+    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e2 = e == cudaSuccess ? cudaDeviceSynchronize() : e;
+    cudaFree(d_jobs);
+    cuda_check(e2, "k0_repack");
+  }
   if (D.max_seg <= kMaxSeg) {  // one self-contained metadata record per strip for k1_flow
     std::vector<StripCtx> ctxs(strips.size());
     for (size_t t = 0; t < strips.size(); ++t) {
@@ -374,9 +474,14 @@ void Plan::build_direction(int d, const PlanTables& T) {
   cuda_check(cudaMalloc(&D.d_sync, kMaxFlowCtas * sizeof(unsigned)), "cudaMalloc sync");
   cuda_check(cudaMemset(D.d_sync, 0, kMaxFlowCtas * sizeof(unsigned)), "memset sync");
   D.built = true;
+  if (std::getenv("MIDBF_PLAN_TIMING"))
+    std::fprintf(stderr, "[plan] dir %d: metadata %.1f ms, repack+uploads %.1f ms (%lld strips, %lld segs)\n", d,
+                 1e3 * std::chrono::duration<double>(t_meta - t_begin).count(),
+                 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_meta).count(),
+                 static_cast<long long>(D.nstrips), static_cast<long long>(D.nsegs));
 }
 
-Plan::Plan(const PlanTables& T, unsigned directions) {
+Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   device = require_device();
   if (const char* e = std::getenv("MIDBF_STRIP_ROWS")) {  // experiments: strip height 1..32
     const int v = std::atoi(e);
@@ -395,8 +500,35 @@ Plan::Plan(const PlanTables& T, unsigned directions) {
   cuda_check(cudaMalloc(&d_col_perm, std::max<int64_t>(1, ncols) * sizeof(int)), "cudaMalloc perm");
   cuda_check(cudaMemcpy(d_row_perm, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice), "upload perm");
   cuda_check(cudaMemcpy(d_col_perm, cp.data(), cp.size() * sizeof(int), cudaMemcpyHostToDevice), "upload perm");
-  for (int d = 0; d < 2; ++d)
-    if (directions & (1u << d)) build_direction(d, T);
+  static const bool timing = std::getenv("MIDBF_PLAN_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+  const auto t0 = now();
+  std::vector<std::vector<int64_t>> raw_off;
+  double2* d_raw = nullptr;
+  if (d_raw_in) {  // payload already on the device, blocks back to back in table order
+    d_raw = d_raw_in;
+    int64_t at = 0;
+    raw_off.resize(T.factors.size());
+    for (size_t f = 0; f < T.factors.size(); ++f)
+      for (int64_t b = 0; b < T.factors[f].nblocks; ++b) {
+        raw_off[f].push_back(at);
+        at += T.factors[f].blocks[4 * b + 2] * T.factors[f].blocks[4 * b + 3];
+      }
+  } else {
+    d_raw = upload_raw(T, raw_off);
+  }
+  const auto t1 = now();
+  try {
+    for (int d = 0; d < 2; ++d)
+      if (directions & (1u << d)) build_direction(d, T, d_raw, raw_off);
+  } catch (...) {
+    cudaFree(d_raw);
+    throw;
+  }
+  cudaFree(d_raw);
+  const auto t2 = now();
+  if (timing) std::fprintf(stderr, "[plan] raw upload %.1f ms, directions %.1f ms\n", ms(t0, t1), ms(t1, t2));
   flow_grid[0] = flow_setup<4, 3, 16384>(num_sms);
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
   flow_grid[2] = flow_setup<6, 4, 8192>(num_sms);

@@ -94,7 +94,9 @@ struct GraphEntry {
 
 class Plan {
  public:
-  Plan(const PlanTables& T, unsigned directions);
+  // d_raw: optional device copy of every block's payload back to back in
+  // table order (taken over and freed); else uploaded from T's payload pointers.
+  Plan(const PlanTables& T, unsigned directions, double2* d_raw = nullptr);
   ~Plan();
   Plan(const Plan&) = delete;
   Plan& operator=(const Plan&) = delete;
@@ -130,7 +132,8 @@ class Plan {
   void prepare_flow(int d);
 
  private:
-  void build_direction(int d, const PlanTables& T);
+  void build_direction(int d, const PlanTables& T, const double2* d_raw,
+                       const std::vector<std::vector<int64_t>>& raw_off);
   void ensure_buffers(int64_t nrhs);
   void launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);

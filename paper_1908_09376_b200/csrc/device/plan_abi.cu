@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -12,6 +13,7 @@
 
 #include "common.cuh"
 #include "plan.hpp"
+#include "pool.hpp"
 
 namespace midbf::dev {
 
@@ -95,28 +97,45 @@ std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions) {
       total += blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
       ++nblocks_all;
     }
-  std::vector<double> payload(static_cast<size_t>(2 * total));
-  f.read(reinterpret_cast<char*>(payload.data()), static_cast<std::streamsize>(16 * total));
-  need(bool(f), "truncated payload");
-  f.peek();
-  need(f.eof(), "trailing bytes after payload");
-  const double* p = payload.data();
-  std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(T.nfactors));
+  // payload: contiguous in block order = the plan's raw layout; stream it
+  // through the pinned staging pool straight into device memory
+  double2* d_raw = nullptr;
+  cuda_check(cudaMalloc(&d_raw, std::max<int64_t>(total, 1) * sizeof(double2)), "cudaMalloc raw payload");
+  try {
+    PinnedPool& P = pinned_pool();
+    std::lock_guard<std::mutex> lock(P.mu);
+    P.ensure();
+    const int64_t cap = static_cast<int64_t>(PinnedPool::kBytes / sizeof(double2));
+    int buf = 0, used = 0;
+    for (int64_t at = 0; at < total; at += cap) {
+      const int64_t n = std::min(cap, total - at);
+      if (used >= 2) cuda_check(cudaEventSynchronize(P.ev[buf]), "payload buffer reuse");
+      f.read(P.h[buf], static_cast<std::streamsize>(16 * n));
+      need(bool(f), "truncated payload");
+      cuda_check(cudaMemcpyAsync(d_raw + at, P.h[buf], n * sizeof(double2), cudaMemcpyHostToDevice, nullptr),
+                 "payload H2D");
+      cuda_check(cudaEventRecord(P.ev[buf], nullptr), "event");
+      buf ^= 1;
+      ++used;
+    }
+    cuda_check(cudaDeviceSynchronize(), "payload upload");
+    f.peek();
+    need(f.eof(), "trailing bytes after payload");
+  } catch (...) {
+    cudaDeviceSynchronize();
+    cudaFree(d_raw);
+    throw;
+  }
   for (int64_t i = 0; i < T.nfactors; ++i) {
     FactorView& F = T.factors[static_cast<size_t>(i)];
     F.blocks = blocks[i].data();
     F.groups = groups[i].data();
-    for (int64_t b = 0; b < F.nblocks; ++b) {
-      ptrs[i].push_back(p);
-      p += 2 * blocks[i][4 * b + 2] * blocks[i][4 * b + 3];
-    }
-    F.payload = ptrs[i].data();
   }
   T.row_perm = rp.data();
   T.col_perm = cp.data();
   T.total_nnz = total;
   T.total_blocks = nblocks_all;
-  return std::make_unique<Plan>(T, directions);
+  return std::make_unique<Plan>(T, directions, d_raw);
 }
 
 int require_device() {
@@ -144,49 +163,81 @@ struct midbf_plan_s {
   std::unique_ptr<Plan> p;
 };
 
+namespace {
+
+// Shared body of midbf_plan_create / midbf_plan_create_blocks: payload(i, b)
+// returns block b of factor i (column-major complex, rows x cols).
+template <typename PayloadAt>
+midbf_plan_t create_plan(int64_t nrows, int64_t ncols, const int64_t* row_perm, const int64_t* col_perm,
+                         int64_t nfactors, const int64_t* factor_shape, const int64_t* blocks,
+                         const int64_t* groups, PayloadAt payload, unsigned directions) {
+  midbf::dev::PlanTables T;
+  T.nrows = nrows;
+  T.ncols = ncols;
+  T.row_perm = row_perm;
+  T.col_perm = col_perm;
+  T.nfactors = nfactors;
+  T.factors.resize(static_cast<size_t>(nfactors));
+  std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(nfactors));
+  const int64_t* bp = blocks;
+  const int64_t* gp = groups;
+  int64_t flat = 0;
+  for (int64_t i = 0; i < nfactors; ++i) {
+    auto& F = T.factors[static_cast<size_t>(i)];
+    F.rows = factor_shape[4 * i];
+    F.cols = factor_shape[4 * i + 1];
+    F.nblocks = factor_shape[4 * i + 2];
+    F.ngroups = factor_shape[4 * i + 3];
+    F.blocks = bp;
+    F.groups = gp;
+    for (int64_t b = 0; b < F.nblocks; ++b, ++flat) {
+      const int64_t m = bp[4 * b + 2], n = bp[4 * b + 3];
+      if (m < 0 || n < 0 || bp[4 * b] < 0 || bp[4 * b + 1] < 0 || bp[4 * b] + m > F.rows ||
+          bp[4 * b + 1] + n > F.cols)
+        throw std::invalid_argument("block outside its factor");
+      const double* pb = payload(flat, m * n);
+      if (!pb && m * n > 0) throw std::invalid_argument("null block payload");
+      ptrs[i].push_back(pb);
+      T.total_nnz += m * n;
+      ++T.total_blocks;
+    }
+    for (int64_t g = 0; g < F.ngroups; ++g)
+      if (gp[2 * g] < 0 || gp[2 * g] > gp[2 * g + 1] || gp[2 * g + 1] > F.nblocks)
+        throw std::invalid_argument("group outside block table");
+    F.payload = ptrs[i].data();
+    bp += 4 * F.nblocks;
+    gp += 2 * F.ngroups;
+  }
+  return new midbf_plan_s{std::make_unique<Plan>(T, directions)};
+}
+
+}  // namespace
+
 extern "C" int midbf_plan_create(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int64_t* row_perm,
                                  const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
                                  const int64_t* blocks, const int64_t* groups, const double* payload,
                                  unsigned directions) {
   return guard([&] {
     if (!out) throw std::invalid_argument("null output handle");
-    midbf::dev::PlanTables T;
-    T.nrows = nrows;
-    T.ncols = ncols;
-    T.row_perm = row_perm;
-    T.col_perm = col_perm;
-    T.nfactors = nfactors;
-    T.factors.resize(static_cast<size_t>(nfactors));
-    std::vector<std::vector<const double*>> ptrs(static_cast<size_t>(nfactors));
-    const int64_t* bp = blocks;
-    const int64_t* gp = groups;
     const double* pp = payload;
-    for (int64_t i = 0; i < nfactors; ++i) {
-      auto& F = T.factors[static_cast<size_t>(i)];
-      F.rows = factor_shape[4 * i];
-      F.cols = factor_shape[4 * i + 1];
-      F.nblocks = factor_shape[4 * i + 2];
-      F.ngroups = factor_shape[4 * i + 3];
-      F.blocks = bp;
-      F.groups = gp;
-      for (int64_t b = 0; b < F.nblocks; ++b) {
-        const int64_t m = bp[4 * b + 2], n = bp[4 * b + 3];
-        if (m < 0 || n < 0 || bp[4 * b] < 0 || bp[4 * b + 1] < 0 || bp[4 * b] + m > F.rows ||
-            bp[4 * b + 1] + n > F.cols)
-          throw std::invalid_argument("block outside its factor");
-        ptrs[i].push_back(pp);
-        pp += 2 * m * n;
-        T.total_nnz += m * n;
-        ++T.total_blocks;
-      }
-      for (int64_t g = 0; g < F.ngroups; ++g)
-        if (gp[2 * g] < 0 || gp[2 * g] > gp[2 * g + 1] || gp[2 * g + 1] > F.nblocks)
-          throw std::invalid_argument("group outside block table");
-      F.payload = ptrs[i].data();
-      bp += 4 * F.nblocks;
-      gp += 2 * F.ngroups;
-    }
-    *out = new midbf_plan_s{std::make_unique<Plan>(T, directions)};
+    *out = create_plan(nrows, ncols, row_perm, col_perm, nfactors, factor_shape, blocks, groups,
+                       [&pp](int64_t, int64_t mn) {
+                         const double* p = pp;
+                         pp += 2 * mn;
+                         return p;
+                       },
+                       directions);
+  });
+}
+
+extern "C" int midbf_plan_create_blocks(midbf_plan_t* out, int64_t nrows, int64_t ncols, const int64_t* row_perm,
+                                        const int64_t* col_perm, int64_t nfactors, const int64_t* factor_shape,
+                                        const int64_t* blocks, const int64_t* groups,
+                                        const double* const* block_payloads, unsigned directions) {
+  return guard([&] {
+    if (!out || !block_payloads) throw std::invalid_argument("null argument");
+    *out = create_plan(nrows, ncols, row_perm, col_perm, nfactors, factor_shape, blocks, groups,
+                       [block_payloads](int64_t flat, int64_t) { return block_payloads[flat]; }, directions);
   });
 }
 

@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "k5_id.cuh"
+#include "pool.hpp"
 #include "sample.hpp"
 
 namespace midbf::dev {
@@ -238,21 +239,14 @@ IdPool& id_pool() {
   return *p;
 }
 
-// Double-buffered device output / pinned staging of sample_blocks, also
-// process-wide (allocated on first use; held under `mu` for a whole call).
+// Double-buffered device output of sample_blocks (process-wide, allocated on
+// first use); the pinned side is the shared staging pool (pool.hpp).
 struct ChunkPool {
-  static constexpr int64_t kChunk = int64_t{4} << 20;  // complex entries per chunk (64 MB)
-  std::mutex mu;
+  static constexpr int64_t kChunk = static_cast<int64_t>(PinnedPool::kBytes / sizeof(double2));  // 4M entries
   double2* d_out[2] = {nullptr, nullptr};
-  double2* h_pin[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
   void ensure() {
     if (d_out[0]) return;
-    for (int b = 0; b < 2; ++b) {
-      cuda_check(cudaMalloc(&d_out[b], kChunk * sizeof(double2)), "cudaMalloc sample buffer");
-      cuda_check(cudaMallocHost(&h_pin[b], kChunk * sizeof(double2)), "cudaMallocHost sample buffer");
-      cuda_check(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming), "event");
-    }
+    for (int b = 0; b < 2; ++b) cuda_check(cudaMalloc(&d_out[b], kChunk * sizeof(double2)), "cudaMalloc sample buffer");
   }
 };
 ChunkPool& chunk_pool() {
@@ -417,7 +411,9 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   chunk_begin.push_back(nsub);
   I.ensure_stream();
   ChunkPool& CP = chunk_pool();
-  std::lock_guard<std::mutex> lock(CP.mu);
+  PinnedPool& PP = pinned_pool();
+  std::lock_guard<std::mutex> lock(PP.mu);
+  PP.ensure();
   CP.ensure();
   int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
   int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
@@ -425,8 +421,8 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   const int64_t nchunks = static_cast<int64_t>(chunk_entries.size());
   auto scatter = [&](int64_t c) {
     const int b = static_cast<int>(c & 1);
-    cuda_check(cudaEventSynchronize(CP.done[b]), "sample chunk");
-    const double2* src = CP.h_pin[b];
+    cuda_check(cudaEventSynchronize(PP.ev[b]), "sample chunk");
+    const double2* src = reinterpret_cast<double2*>(PP.h[b]);
     const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t t = t0; t < t1; ++t) {
@@ -437,17 +433,17 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
   try {
     for (int64_t c = 0; c < nchunks; ++c) {
       const int b = static_cast<int>(c & 1);
-      if (c >= 2) cuda_check(cudaEventSynchronize(CP.done[b]), "sample buffer reuse");
+      if (c >= 2) cuda_check(cudaEventSynchronize(PP.ev[b]), "sample buffer reuse");
       const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
       if (chunk_entries[static_cast<size_t>(c)] > 0) {
         k3_sample<<<static_cast<unsigned>(t1 - t0), 256, 0, I.stream>>>(I.k, d_tasks + 5 * t0, d_rid, d_cid,
                                                                          CP.d_out[b]);
         cuda_check(cudaGetLastError(), "k3_sample launch");
-        cuda_check(cudaMemcpyAsync(CP.h_pin[b], CP.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
+        cuda_check(cudaMemcpyAsync(reinterpret_cast<double2*>(PP.h[b]), CP.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
                                    cudaMemcpyDeviceToHost, I.stream),
                    "sample D2H");
       }
-      cuda_check(cudaEventRecord(CP.done[b], I.stream), "event record");
+      cuda_check(cudaEventRecord(PP.ev[b], I.stream), "event record");
       if (c >= 1) scatter(c - 1);
       I.launched_entries += chunk_entries[static_cast<size_t>(c)];
     }

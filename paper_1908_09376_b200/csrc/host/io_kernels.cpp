@@ -136,27 +136,22 @@ midbf_plan_t device_plan(const Factorization& F, unsigned directions) {
   const unsigned want = directions | (F.device ? F.device->directions : 0u);
   F.device.reset();
   std::vector<std::int64_t> shape, blocks, groups;
-  Index total = 0;
   for (const Factor& fc : F.factors) {
     shape.insert(shape.end(), {fc.rows, fc.cols, static_cast<std::int64_t>(fc.blocks.size()),
                                static_cast<std::int64_t>(fc.groups.size())});
     for (const FactorBlock& b : fc.blocks) {
       blocks.insert(blocks.end(), {b.row_off, b.col_off, b.M.rows(), b.M.cols()});
-      total += b.M.size();
     }
     for (const auto& g : fc.groups) groups.insert(groups.end(), {g.first, g.second});
   }
-  std::vector<double> payload(static_cast<size_t>(2 * total));
-  size_t at = 0;
+  std::vector<const double*> ptrs;  // per block, no repacking on the host
+  ptrs.reserve(static_cast<size_t>(blocks.size() / 4));
   for (const Factor& fc : F.factors)
-    for (const FactorBlock& b : fc.blocks) {
-      std::memcpy(payload.data() + at, b.M.data(), static_cast<size_t>(16 * b.M.size()));
-      at += static_cast<size_t>(2 * b.M.size());
-    }
+    for (const FactorBlock& b : fc.blocks) ptrs.push_back(reinterpret_cast<const double*>(b.M.data()));
   auto cache = std::make_shared<DevicePlanCache>();
-  detail::rethrow(midbf_plan_create(&cache->plan, F.nrows, F.ncols, F.row_perm.data(), F.col_perm.data(),
-                                    static_cast<std::int64_t>(F.factors.size()), shape.data(), blocks.data(),
-                                    groups.data(), payload.data(), want));
+  detail::rethrow(midbf_plan_create_blocks(&cache->plan, F.nrows, F.ncols, F.row_perm.data(), F.col_perm.data(),
+                                           static_cast<std::int64_t>(F.factors.size()), shape.data(), blocks.data(),
+                                           groups.data(), ptrs.data(), want));
   cache->directions = want;
   F.device = cache;
   return cache->plan;
