@@ -30,13 +30,4 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Streaming 128-bit load: read once, evict first (factor payload).
-__device__ __forceinline__ double2 ld_stream(const double2* p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p));
-  return v;
-}
-
 }  // namespace midbf::dev

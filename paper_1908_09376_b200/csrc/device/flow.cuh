@@ -132,12 +132,6 @@ __device__ __forceinline__ double2 ld_cg(const double2* p) {
   asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
-// input index of the strip's flattened staged column kk
-__device__ __forceinline__ int x_index(const StripCtx& c, int kk) {
-  int j = 0;
-  while (kk >= c.g[j].n) kk -= c.g[j++].n;
-  return c.g[j].x0 + kk;
-}
 // Gather cnt entries from x0 (stage 0 through xperm, never polled: user f),
 // polling intermediate buffers until every loaded entry is valid.
 __device__ __forceinline__ void gather_range(const double2* x, const int* xperm, int x0, int cnt, double2* dst,
