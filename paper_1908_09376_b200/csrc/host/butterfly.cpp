@@ -197,8 +197,13 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
       if (sys[a * nB + b].col.cells.size() != sys[b].col.cells.size())
         throw std::logic_error("column unit layout differs between sibling systems");
 
+  static const bool timing = std::getenv("MIDBF_FACT_TIMING") != nullptr;
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  const auto t_a = tnow();
   // column samples, one per system (:434-441)
   std::vector<IndexVec> csamp(static_cast<size_t>(ns));
+  const bool par = cfg.exec == Exec::Parallel;
+#pragma omp parallel for schedule(dynamic) if (par && ns > 1)
   for (Index s = 0; s < ns; ++s) {
     IndexVec pool;
     pool.reserve(static_cast<size_t>(sys[s].col.size));
@@ -207,6 +212,7 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
     csamp[s] = pick(pool, Om, want, rng);
   }
 
+  const auto t_b = tnow();
   // row pass: fill all blocks K(cell ids, csamp[s]) at once, then the IDs
   std::vector<std::vector<Skel>> rsk(static_cast<size_t>(ns));
   std::vector<std::pair<Index, Index>> rjobs;
@@ -252,13 +258,16 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
     mid_rows += static_cast<Index>(rhat[s].size());
   }
 
+  const auto t_c = tnow();
   // row samples for the column pass (:486-491)
   std::vector<IndexVec> rsamp(static_cast<size_t>(ns));
+#pragma omp parallel for schedule(dynamic) if (par && ns > 1)
   for (Index s = 0; s < ns; ++s) {
     std::mt19937_64 rng(mix(mix(salt ^ mix(0x73726f77ull)) ^ mix(static_cast<std::uint64_t>(s))));
     rsamp[s] = pick(rhat[s], X, want, rng);
   }
 
+  const auto t_d = tnow();
   // column pass (:493-519)
   std::vector<std::vector<Skel>> csk(static_cast<size_t>(ns));
   std::vector<std::pair<Index, Index>> cjobs;
@@ -304,6 +313,7 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
     mid_cols += static_cast<Index>(chat[s].size());
   }
 
+  const auto t_e = tnow();
   SweepOut R;
   R.mid_rows = mid_rows;
   R.mid_cols = mid_cols;
@@ -381,6 +391,11 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
           nx.col = b.span;
         }
     }
+  }
+  if (timing) {
+    auto ms = [](auto a, auto b) { return 1e3 * std::chrono::duration<double>(b - a).count(); };
+    std::fprintf(stderr, "[sweep %d] systems %lld: col samples %.1f ms, row IDs %.1f, row samples %.1f, col IDs %.1f, assemble %.1f\n",
+                 level, static_cast<long long>(ns), ms(t_a, t_b), ms(t_b, t_c), ms(t_c, t_d), ms(t_d, t_e), ms(t_e, tnow()));
   }
   return R;
 }

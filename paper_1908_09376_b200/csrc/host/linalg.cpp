@@ -203,26 +203,63 @@ IndexVec mock_chebyshev_points(const MatXd& P, Index s, std::mt19937_64& rng) {
   Index nodes = 1;
   for (Index a = 0; a < d; ++a) nodes *= c;
   std::vector<char> taken(static_cast<size_t>(n), 0);
-  std::vector<double> node(static_cast<size_t>(d));
+  // Node coordinates (last axis varies fastest), as the reference builds them.
+  std::vector<double> nodec(static_cast<size_t>(nodes * d));
   for (Index t = 0; t < nodes; ++t) {
     Index rem = t;
-    for (Index a = d - 1; a >= 0; --a) {  // last axis varies fastest
+    for (Index a = d - 1; a >= 0; --a) {
       const Index j = rem % c;
       rem /= c;
-      node[a] = mid[a] + half[a] * std::cos((2.0 * j + 1.0) * kPi / (2.0 * c));
+      nodec[static_cast<size_t>(t * d + a)] = mid[a] + half[a] * std::cos((2.0 * j + 1.0) * kPi / (2.0 * c));
     }
-    Index best = -1;
-    double bd = std::numeric_limits<double>::infinity();
+  }
+  auto dist_to = [&](Index i, Index t) {
+    double dist = 0.0;
+    for (Index a = 0; a < d; ++a) {
+      const double e = P(i, a) - nodec[static_cast<size_t>(t * d + a)];
+      dist += e * e;
+    }
+    return dist;
+  };
+  // Each node's kCand nearest points by (distance, index), independent of the
+  // picks, in parallel; then the picks in node order take the first untaken
+  // candidate -- the reference's "nearest unused point, first on ties" --
+  // and fall back to a full scan when every candidate is already taken.
+  constexpr Index kCand = 8;
+  std::vector<Index> cand(static_cast<size_t>(nodes * kCand), -1);
+  std::vector<double> cdist(static_cast<size_t>(nodes * kCand), std::numeric_limits<double>::infinity());
+#pragma omp parallel for schedule(dynamic) if (n * nodes >= (Index{1} << 20))
+  for (Index t = 0; t < nodes; ++t) {
+    Index* ci = cand.data() + t * kCand;
+    double* cd = cdist.data() + t * kCand;
     for (Index i = 0; i < n; ++i) {
-      if (taken[i]) continue;
-      double dist = 0.0;
-      for (Index a = 0; a < d; ++a) {
-        const double e = P(i, a) - node[a];
-        dist += e * e;
+      const double dist = dist_to(i, t);
+      if (!(dist < cd[kCand - 1])) continue;  // ties keep the earlier index
+      Index q = kCand - 1;
+      while (q > 0 && dist < cd[q - 1]) {
+        cd[q] = cd[q - 1];
+        ci[q] = ci[q - 1];
+        --q;
       }
-      if (dist < bd) {
-        bd = dist;
-        best = i;
+      cd[q] = dist;
+      ci[q] = i;
+    }
+  }
+  for (Index t = 0; t < nodes; ++t) {
+    Index best = -1;
+    for (Index q = 0; q < kCand && best < 0; ++q) {
+      const Index i = cand[static_cast<size_t>(t * kCand + q)];
+      if (i >= 0 && !taken[i]) best = i;
+    }
+    if (best < 0) {  // all candidates taken: full scan over the untaken points
+      double bd = std::numeric_limits<double>::infinity();
+      for (Index i = 0; i < n; ++i) {
+        if (taken[i]) continue;
+        const double dist = dist_to(i, t);
+        if (dist < bd) {
+          bd = dist;
+          best = i;
+        }
       }
     }
     taken[best] = 1;
