@@ -557,12 +557,14 @@ int Plan::flow_variant(int d) const {
   return bytes > (int64_t{512} << 20) ? 1 : 0;
 }
 
+// Up to kFlowColumns right-hand sides run k1_flow once per column: at cfg1 a
+// column costs ~66 us, a 64-RHS DMMA slice (k2_flow) ~395 us whatever its width.
 bool Plan::flow_ok(int d, int64_t nrhs) const {
-  return nrhs == 1 && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
+  return nrhs >= 1 && nrhs <= kFlowColumns && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
 }
 
 int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
-  if (flow_ok(d, nrhs)) return 1;
+  if (flow_ok(d, nrhs)) return nrhs;
   if (k2flow_ok(d, nrhs)) return (nrhs + kK2Rhs - 1) / kK2Rhs;
   if (k2_ok(d, nrhs)) {
     int64_t n = 0;
@@ -765,9 +767,10 @@ bool Plan::k2_ok(int d, int64_t nrhs) const {
 }
 
 void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
-  if (flow_ok(d, nrhs))
-    launch_flow(d, in, out, stream);
-  else if (k2flow_ok(d, nrhs))
+  if (flow_ok(d, nrhs)) {
+    const int64_t in_ld = d == 0 ? ncols : nrows, out_ld = d == 0 ? nrows : ncols;
+    for (int64_t c = 0; c < nrhs; ++c) launch_flow(d, in + c * in_ld, out + c * out_ld, stream);
+  } else if (k2flow_ok(d, nrhs))
     launch_k2flow(d, in, out, nrhs, stream);
   else if (k2_ok(d, nrhs))
     launch_k2(d, in, out, nrhs, stream);
