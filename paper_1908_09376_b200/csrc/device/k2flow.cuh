@@ -53,12 +53,25 @@ constexpr int kK2FConsumers = 8;                      // consumer warps
 constexpr int kK2FThreads = (kK2FConsumers + 2) * 32;  // + producer and publisher warps
 constexpr int kK2FSlots = 4;                           // ring depth
 constexpr int kK2FDone = 8;                            // strip-completion barrier ring
-constexpr size_t kK2FSmem = size_t(kK2FSlots) * (kK2PBuf + kK2XBuf) * 16 + kK2FSlots * (16 + 16) + kK2FDone * 8;
+
+// Tile width W = 16 NCB right-hand sides (2 warp halves x NCB column blocks of
+// 8); X slot / stage-buffer row stride W + 2 (== 2 mod 8 in 16-byte units:
+// conflict-free B fragments).  The host picks the narrowest W covering a slice.
+// Narrower tiles have smaller X slots, so the same ~100 KB holds a deeper
+// ring (8 / 6 / 4 slots at W = 16 / 32 / 64).
+template <int NCB>
+struct K2FCfg {
+  static constexpr int W = 16 * NCB;
+  static constexpr int XS = W + 2;
+  static constexpr int XBUF = kK2Kc * XS;
+  static constexpr int SLOTS = NCB == 1 ? 8 : (NCB == 2 ? 6 : kK2FSlots);
+  static constexpr size_t kSmem = size_t(SLOTS) * (kK2PBuf + XBUF) * 16 + SLOTS * (16 + 16) + kK2FDone * 8;
+};
 
 struct K2FStage {
   const double2* x;  // input (stage 0: user operand, gathered through xperm)
   double2* y;        // output (last stage: user operand, scattered through yperm)
-  int64_t xld, yld;  // user operands: column-major ld; stage buffers: row-major, row stride kK2Xs
+  int64_t xld, yld;  // user operands: column-major ld; stage buffers: row-major, row stride W + 2
   const int* xperm;
   const int* yperm;
 };
@@ -71,7 +84,7 @@ struct K2FParams {
   unsigned* epoch;  // per CTA: launches completed
   int nstrips;
   int nstages;
-  int ncv;     // valid RHS of this slice (<= 64)
+  int ncv;     // valid RHS of this slice (<= W)
   // timing experiments only (flag bits 14-15), results invalid: 1 skip the
   // dependency waits, 2 stream only (no math), 3 math only (no loads)
   int mode;
@@ -94,24 +107,27 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 
 }  // namespace k2fdev
 
+template <int NCB>
 __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant__ K2FParams P) {
+  using Cfg = K2FCfg<NCB>;
+  constexpr int kW = Cfg::W, kXs = Cfg::XS, kXBuf = Cfg::XBUF, kSlots = Cfg::SLOTS;
   using namespace k2dev;
   using namespace k2fdev;
   using flowdev::mbar_arrive;
   using flowdev::mbar_init;
   using flowdev::mbar_wait;
   extern __shared__ __align__(16) double2 k2smem[];
-  double2* const Pb = k2smem;                        // kK2FSlots panel buffers
-  double2* const Xb = k2smem + kK2FSlots * kK2PBuf;  // kK2FSlots X buffers
-  uint64_t* const full = reinterpret_cast<uint64_t*>(Xb + kK2FSlots * kK2XBuf);
-  uint64_t* const empty = full + kK2FSlots;
-  int4* const meta = reinterpret_cast<int4*>(empty + kK2FSlots);  // per slot: {y0, h, stage | A stride, K}
-  uint64_t* const done = reinterpret_cast<uint64_t*>(meta + kK2FSlots);
+  double2* const Pb = k2smem;                        // kSlots panel buffers
+  double2* const Xb = k2smem + kSlots * kK2PBuf;  // kSlots X buffers
+  uint64_t* const full = reinterpret_cast<uint64_t*>(Xb + kSlots * kXBuf);
+  uint64_t* const empty = full + kSlots;
+  int4* const meta = reinterpret_cast<int4*>(empty + kSlots);  // per slot: {y0, h, stage | A stride, K}
+  uint64_t* const done = reinterpret_cast<uint64_t*>(meta + kSlots);
   __shared__ unsigned s_epoch;
   __shared__ int s_pub;  // strips of this CTA published so far
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
-    for (int i = 0; i < kK2FSlots; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       mbar_init(&full[i], 33);  // 32 cp.async arrivals + the meta writer
       mbar_init(&empty[i], kK2FConsumers);
     }
@@ -149,7 +165,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
       const int nq = K > 0 ? (K + kK2Kc - 1) / kK2Kc : 1;
       bool deps = st.stage == 0 || P.mode != 0;
       for (int q = 0; q < nq; ++q, ++gc) {
-        const int slot = gc % kK2FSlots, use = gc / kK2FSlots;
+        const int slot = gc % kSlots, use = gc / kSlots;
         if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1);
         // lane resolves K column c = lane & 15 of the chunk
         const int c = lane & (kK2Kc - 1);
@@ -171,10 +187,10 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int prev = __shfl_up_sync(0xffffffffu, sidx, 1);
         unsigned runs = __ballot_sync(0xffffffffu, ok && lane < kK2Kc && (c == 0 || prev != sidx));
         double2* pd = Pb + slot * kK2PBuf;
-        double2* xd = Xb + slot * kK2XBuf;
+        double2* xd = Xb + slot * kXBuf;
         if (lane == 0) {
           meta[slot] = make_int4(st.y0, h, st.stage | (pst << 8), K);
-          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : kK2Xs)) : 0u;
+          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : kXs)) : 0u;
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(flowdev::smem_u32(&full[slot])),
                        "r"(bytes)
                        : "memory");
@@ -207,7 +223,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
           if (gather) {  // stage 0: lane & 15 = k, RHS (lane >> 4) + 2 i
             if (ok) {
               const double2* xs = io.x + __ldg(io.xperm + xi);
-              double2* xk = xd + c * kK2Xs;
+              double2* xk = xd + c * kXs;
 #pragma unroll 4
               for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xk + rhs, xs + rhs * io.xld);
             }
@@ -216,8 +232,8 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
               const int r0 = __ffs(runs) - 1;
               runs &= runs - 1;
               const int r1 = runs ? __ffs(runs) - 1 : kval;
-              const int64_t src = static_cast<int64_t>(__shfl_sync(0xffffffffu, xi, r0)) * kK2Xs;
-              if (lane == 0) flowdev::bulk_g2s(xd + r0 * kK2Xs, io.x + src, (r1 - r0) * kK2Xs * 16u, &full[slot]);
+              const int64_t src = static_cast<int64_t>(__shfl_sync(0xffffffffu, xi, r0)) * kXs;
+              if (lane == 0) flowdev::bulk_g2s(xd + r0 * kXs, io.x + src, (r1 - r0) * kXs * 16u, &full[slot]);
             }
           }
         }
@@ -241,16 +257,16 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
     const int row = 8 * rb + g;
     int gc = 0, nit = 0;
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
-      double acc[4][2][2];
+      double acc[NCB][2][2];
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb)
+      for (int cb = 0; cb < NCB; ++cb)
 #pragma unroll
         for (int r = 0; r < 2; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
       int4 m = make_int4(0, 0, 0, 0);
       int nq = 1;
       for (int q = 0; q < nq; ++q, ++gc) {
-        const int slot = gc % kK2FSlots;
-        mbar_wait(&full[slot], (gc / kK2FSlots) & 1);
+        const int slot = gc % kSlots;
+        mbar_wait(&full[slot], (gc / kSlots) & 1);
         if (q == 0) {
           m = meta[slot];
           nq = m.w > 0 ? (m.w + kK2Kc - 1) / kK2Kc : 1;
@@ -259,25 +275,25 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int kfull = krem & ~3;
         const int pst = m.z >> 8;
         const double2* Ps = Pb + slot * kK2PBuf + 8 * rb + g;
-        const double2* Xs = Xb + slot * kK2XBuf + t * kK2Xs + ch * 32 + g;
+        const double2* Xs = Xb + slot * kXBuf + t * kXs + ch * (kW / 2) + g;
         auto step = [&](int kk, bool live) {
           double2 a = Ps[(kk + t) * pst];
-          double2 bv[4];
+          double2 bv[NCB];
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) bv[cb] = Xs[kk * kK2Xs + cb * 8];
+          for (int cb = 0; cb < NCB; ++cb) bv[cb] = Xs[kk * kXs + cb * 8];
           if (!live) {  // K tail: stale slot contents must not reach the sums
             a = make_double2(0, 0);
 #pragma unroll
-            for (int cb = 0; cb < 4; ++cb) bv[cb] = make_double2(0, 0);
+            for (int cb = 0; cb < NCB; ++cb) bv[cb] = make_double2(0, 0);
           }
           const double naim = -a.y;
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cb = 0; cb < NCB; ++cb) {
             dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
             dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
           }
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cb = 0; cb < NCB; ++cb) {
             dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
             dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
           }
@@ -293,7 +309,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
-      // D fragment: row 8*rb + g, RHS 32*ch + cb*8 + 2t + {0,1}
+      // D fragment: row 8*rb + g, RHS (W/2)*ch + cb*8 + 2t + {0,1}
       const int stage = m.z & 255;
       const K2FStage io = P.st[stage];
       const bool last = stage + 1 == P.nstages;
@@ -301,10 +317,10 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         int idx = m.x + row;
         if (io.yperm) idx = __ldg(io.yperm + idx);
 #pragma unroll
-        for (int cb = 0; cb < 4; ++cb)
+        for (int cb = 0; cb < NCB; ++cb)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int rhs = 32 * ch + cb * 8 + 2 * t + i;
+            const int rhs = (kW / 2) * ch + cb * 8 + 2 * t + i;
             if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : idx * io.yld + rhs] =
                 make_double2(acc[cb][0][i], acc[cb][1][i]);
           }

@@ -158,6 +158,16 @@ int flow_setup(int num_sms) {
   return std::min(per_sm * num_sms, kMaxFlowCtas);
 }
 
+template <int NCB>
+int k2flow_setup(int num_sms) {
+  const size_t smem = K2FCfg<NCB>::kSmem;
+  cuda_check(cudaFuncSetAttribute(k2_flow<NCB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+             "k2_flow smem attribute");
+  int per_sm = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_flow<NCB>, kK2FThreads, smem), "occupancy");
+  return std::min(per_sm * num_sms, kMaxFlowCtas);  // 0: unavailable
+}
+
 template <int FW, int FS, int SLOT>
 void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
   P.nwarps = grid * FW;
@@ -501,11 +511,13 @@ Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   flow_grid[3] = flow_grid[0];  // unused: variant 3 resolves per direction (flow_variant)
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
-  cuda_check(cudaFuncSetAttribute(k2_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2FSmem)),
-             "k2_flow smem attribute");
-  int per_sm = 0;
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_flow, kK2FThreads, kK2FSmem), "occupancy");
-  k2flow_grid = std::min(per_sm * num_sms, kMaxFlowCtas);  // 0: k2_flow unavailable
+  k2flow_grid[0] = k2flow_setup<1>(num_sms);  // 16-wide tiles
+  k2flow_grid[1] = k2flow_setup<2>(num_sms);  // 32
+  k2flow_grid[2] = k2flow_setup<4>(num_sms);  // 64
+  // one grid for every width: the per-CTA launch epochs (k2flow.cuh) assume
+  // every launch runs the same set of CTAs
+  const int g = std::min({k2flow_grid[0], k2flow_grid[1], k2flow_grid[2]});
+  for (int& v : k2flow_grid) v = g;
 }
 
 Plan::~Plan() {
@@ -558,7 +570,7 @@ int Plan::flow_variant(int d) const {
 }
 
 // Up to kFlowColumns right-hand sides run k1_flow once per column: at cfg1 a
-// column costs ~66 us, a 64-RHS DMMA slice (k2_flow) ~395 us whatever its width.
+// column costs ~66 us, the narrowest DMMA slice (16 wide) ~200 us.
 bool Plan::flow_ok(int d, int64_t nrhs) const {
   return nrhs >= 1 && nrhs <= kFlowColumns && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
 }
@@ -693,7 +705,7 @@ void Plan::launch_k2(int d, const double2* in, double2* out, int64_t nrhs, cudaS
 }
 
 bool Plan::k2flow_ok(int d, int64_t nrhs) const {
-  return k2_ok(d, nrhs) && !(flags & 8192u) && k2flow_grid > 0;
+  return k2_ok(d, nrhs) && !(flags & 8192u) && k2flow_grid[0] > 0 && k2flow_grid[1] > 0 && k2flow_grid[2] > 0;
 }
 
 void Plan::ensure_k2flow(int d) {
@@ -723,9 +735,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   P.nstages = ns;
   P.mode = static_cast<int>((flags >> 14) & 3u);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(k2flow_grid), 1, 1);
   cfg.blockDim = dim3(kK2FThreads, 1, 1);
-  cfg.dynamicSmemBytes = kK2FSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // CTAs wait on each other's strips
@@ -734,6 +744,9 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   cfg.numAttrs = 1;
   for (int64_t c0 = 0; c0 < nrhs; c0 += kK2Rhs) {
     P.ncv = static_cast<int>(std::min<int64_t>(kK2Rhs, nrhs - c0));
+    const int wi = P.ncv <= 16 ? 0 : (P.ncv <= 32 ? 1 : 2);  // narrowest tile covering the slice
+    const int64_t xs = (16 << wi) + 2;                      // its X / stage-row stride
+    cfg.gridDim = dim3(static_cast<unsigned>(k2flow_grid[wi]), 1, 1);
     int64_t off = 0;
     for (int s = 0; s < ns; ++s) {
       K2FStage& io = P.st[s];
@@ -752,13 +765,25 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         io.yld = out_ld;
         io.yperm = d == 0 ? d_row_perm : d_col_perm;
       } else {
-        io.y = D.d_k2buf + off * kK2Xs;
-        io.yld = kK2Xs;  // row-major, RHS fastest, rows padded to the smem slot stride
+        io.y = D.d_k2buf + off * xs;
+        io.yld = xs;  // row-major, RHS fastest, rows padded to the smem slot stride
         io.yperm = nullptr;
         off += len;
       }
     }
-    cuda_check(cudaLaunchKernelEx(&cfg, k2_flow, P), "k2_flow launch");
+    switch (wi) {
+      case 0:
+        cfg.dynamicSmemBytes = K2FCfg<1>::kSmem;
+        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<1>, P), "k2_flow launch");
+        break;
+      case 1:
+        cfg.dynamicSmemBytes = K2FCfg<2>::kSmem;
+        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<2>, P), "k2_flow launch");
+        break;
+      default:
+        cfg.dynamicSmemBytes = K2FCfg<4>::kSmem;
+        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<4>, P), "k2_flow launch");
+    }
   }
 }
 

@@ -12,7 +12,7 @@ namespace midbf::dev {
 
 constexpr int kMaxStages = 64;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
-constexpr int kFlowColumns = 5;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
+constexpr int kFlowColumns = 3;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 
 // Output strip of <= 32 rows of one stage; one warp computes it.
 struct Strip {
@@ -128,7 +128,7 @@ class Plan {
   int flow_variant(int d) const;
   bool k2_ok(int d, int64_t nrhs) const;
   bool k2flow_ok(int d, int64_t nrhs) const;
-  int k2flow_grid = 0;
+  int k2flow_grid[3] = {0, 0, 0};  // persistent CTAs of k2_flow<1 | 2 | 4> (16 / 32 / 64-wide tiles)
   int last_grid[2] = {-1, -1};
   void prepare_flow(int d);
 
