@@ -50,7 +50,7 @@
 namespace midbf::dev {
 
 constexpr int kK2FConsumers = 8;                      // consumer warps
-constexpr int kK2FThreads = (kK2FConsumers + 2) * 32;  // + producer and publisher warps
+constexpr int kK2FThreads = (kK2FConsumers + 3) * 32;  // + panel / input producer warps and a publisher warp
 constexpr int kK2FSlots = 4;                           // ring depth
 constexpr int kK2FDone = 8;                            // strip-completion barrier ring
 
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
-      mbar_init(&full[i], 33);  // 32 cp.async arrivals + the meta writer
+      mbar_init(&full[i], 34);  // panel-producer lane 0 + input-producer lane 0 + its 32 cp.async arrivals
       mbar_init(&empty[i], kK2FConsumers);
     }
     for (int i = 0; i < kK2FDone; ++i) mbar_init(&done[i], kK2FConsumers);
@@ -139,8 +139,9 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
   __syncthreads();
   const unsigned target = s_epoch;
 
-  if (w == kK2FConsumers) {
-    // ------------------------------ producer -------------------------------
+  if (w == kK2FConsumers || w == kK2FConsumers + 1) {
+    // ---------------- producers: panels (no waits) | inputs (dependencies) -------
+    const bool xrole = w == kK2FConsumers + 1;
     int gc = 0;  // chunks issued
     int started = 0;  // this CTA's strips started
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
@@ -188,28 +189,36 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         unsigned runs = __ballot_sync(0xffffffffu, ok && lane < kK2Kc && (c == 0 || prev != sidx));
         double2* pd = Pb + slot * kK2PBuf;
         double2* xd = Xb + slot * kXBuf;
-        if (lane == 0) {
-          meta[slot] = make_int4(st.y0, h, st.stage | (pst << 8), K);
-          const unsigned bytes = load ? kval * 16u * (h + (gather ? 0 : kXs)) : 0u;
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(flowdev::smem_u32(&full[slot])),
-                       "r"(bytes)
-                       : "memory");
-        }
-        __syncwarp();
-        if (load) {
-          if (!prun) {
-            if (ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
-          } else {
-            unsigned r = runs;
-            while (r) {
-              const int r0 = __ffs(r) - 1;
-              r &= r - 1;
-              const int r1 = r ? __ffs(r) - 1 : kval;
-              const int64_t src = __shfl_sync(0xffffffffu, psrc, r0);
-              if (lane == 0) flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
+        if (!xrole) {  // panels: plan constants, never wait on other strips
+          if (lane == 0) {
+            meta[slot] = make_int4(st.y0, h, st.stage | (pst << 8), K);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             flowdev::smem_u32(&full[slot])),
+                         "r"(load ? kval * 16u * h : 0u)
+                         : "memory");
+          }
+          __syncwarp();
+          if (load) {
+            if (!prun) {
+              if (ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
+            } else {
+              unsigned r = runs;
+              while (r) {
+                const int r0 = __ffs(r) - 1;
+                r &= r - 1;
+                const int r1 = r ? __ffs(r) - 1 : kval;
+                const int64_t src = __shfl_sync(0xffffffffu, psrc, r0);
+                if (lane == 0) flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
+              }
             }
           }
+          continue;
         }
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(flowdev::smem_u32(&full[slot])),
+                       "r"(load && !gather ? kval * 16u * kXs : 0u)
+                       : "memory");
+        __syncwarp();
         while (!deps) {  // previous-stage producers of this strip's input rows
           bool ready = true;
           for (int l = 0; l < st.nseg; ++l) {
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         cp_async_arrive_noinc(&full[slot]);
       }
     }
-  } else if (w == kK2FConsumers + 1) {
+  } else if (w == kK2FConsumers + 2) {
     // ------------------------------ publisher ------------------------------
     int n = 0;
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x, ++n) {

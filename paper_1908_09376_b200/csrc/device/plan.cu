@@ -570,7 +570,7 @@ int Plan::flow_variant(int d) const {
 }
 
 // Up to kFlowColumns right-hand sides run k1_flow once per column: at cfg1 a
-// column costs ~66 us, the narrowest DMMA slice (16 wide) ~200 us.
+// column costs ~66 us, the narrowest DMMA slice (16 wide) ~155 us.
 bool Plan::flow_ok(int d, int64_t nrhs) const {
   return nrhs >= 1 && nrhs <= kFlowColumns && (flags & 8u) && dir[d].max_seg <= kMaxSeg;
 }

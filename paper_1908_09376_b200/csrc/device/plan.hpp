@@ -12,7 +12,7 @@ namespace midbf::dev {
 
 constexpr int kMaxStages = 64;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
-constexpr int kFlowColumns = 3;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
+constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 
 // Output strip of <= 32 rows of one stage; one warp computes it.
 struct Strip {

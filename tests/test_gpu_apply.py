@@ -54,12 +54,12 @@ def test_multi_rhs_matches_oracle_and_columns(pair):
 
 @pytest.mark.parametrize("nrhs", [2, 3, 4])
 def test_few_rhs_dispatch(pair, nrhs):
-    """Up to 3 RHS run the single-RHS dataflow kernel once per column, more
+    """Up to 2 RHS run the single-RHS dataflow kernel once per column, more
     run the DMMA kernel; both match the oracle."""
     name, K, Fo, Fm, plan = pair
     X = cvec(Fo.ncols, 21, cols=nrhs)
     assert rel(plan.apply(X), Fo.apply(X)) <= TOL
-    assert plan.launches(nrhs) == (nrhs if nrhs <= 3 else 1)
+    assert plan.launches(nrhs) == (nrhs if nrhs <= 2 else 1)
 
 
 @pytest.mark.parametrize("nrhs", [64, 70, 16, 33, 100])
