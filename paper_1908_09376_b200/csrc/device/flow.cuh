@@ -19,10 +19,11 @@
 //     after the last panel writes its row (the row value is the ready signal).
 // Dependencies: a strip reads x[x0, x0+n) of each panel from the previous
 // stage's output buffer, which is armed with a sentinel bit pattern before the
-// apply; the consumer polls exactly the entries it needs until none is a
-// sentinel (the data is its own ready signal: no flags, no fences).  The next
-// strip's entries are loaded into registers before the current strip is
-// computed and validated after it, so x usually arrives for free.
+// apply; an x stager polls exactly the entries a strip needs until none is a
+// sentinel (the data is its own ready signal: no flags, no fences) and stages
+// them in shared memory up to two strips ahead of the consumer (x_full /
+// x_empty mbarriers).  The stager is a dedicated warp per pair when the
+// register file allows (<= 4 pairs), else the producer warp's lanes 1..31.
 // Strip metadata (strip + up to kMaxSeg panels) is loaded once per claim into
 // a per-warp shared-memory context ring, so the hot loop issues no
 // dependent global loads besides x.
@@ -31,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "plan.hpp"
 
@@ -206,6 +208,48 @@ __device__ __forceinline__ void store_x_regs(const StripCtx& c, const double2* v
     if (lane + 32 * i < c.s.xcols) dst[lane + 32 * i] = v[i];
 }
 
+// A strip's x window is staged into shared memory by a stager: a dedicated
+// warp per pair (flow_sep) or the producer warp's lanes 1..31.  Each lane
+// gathers its entries (lane-strided over the flattened panel columns) and
+// polls until none is a sentinel; no warp-collective ops inside, so the
+// producer's lane 0 can run the TMA issue loop concurrently.
+template <int NS>  // stager lanes
+__device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst, int sl) {
+  constexpr int kPer = (kXWin + NS - 1) / NS;
+  int idx[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) idx[i] = -1;
+  int cb = 0;
+  for (int j = 0; j < c.s.nseg; ++j) {
+    const int n = c.g[j].n, x0 = c.g[j].x0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int kk = sl + NS * i - cb;
+      if (kk >= 0 && kk < n) idx[i] = x0 + kk;
+    }
+    cb += n;
+  }
+  double2 v[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i)
+    if (idx[i] >= 0) v[i] = xperm ? __ldg(x + __ldg(xperm + idx[i])) : ld_cg(x + idx[i]);
+  if (!xperm) {
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i)
+        if (idx[i] >= 0 && is_sentinel(v[i])) {
+          v[i] = ld_cg(x + idx[i]);
+          ok = false;
+        }
+    } while (!ok);
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i)
+    if (idx[i] >= 0) dst[sl + NS * i] = v[i];
+}
+
 __host__ __device__ constexpr int chunk_cols_for(int h, int slot_bytes) {
   int c = 64;
   while (c > 1 && h * c * 16 > slot_bytes) c >>= 1;
@@ -229,14 +273,26 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
 
 }  // namespace flowdev
 
+// Up to 4 pairs per CTA a dedicated x-stager warp per pair fits the register
+// file (3 x 4 x 32 threads x 160 registers); with more pairs the producer
+// warp's idle lanes 1..31 stage x instead.
+template <int FW>
+__host__ __device__ constexpr bool flow_sep() {
+  return FW <= 4;
+}
+template <int FW>
+__host__ __device__ constexpr int flow_threads() {
+  return (flow_sep<FW>() ? 3 : 2) * FW * 32;
+}
+
 // Shared-memory layout of one CTA: FW (producer, consumer) warp pairs.
 template <int FW, int FS, int SLOT>
 struct FlowCfg {
   static constexpr size_t kSlotArea = size_t(FW) * FS * SLOT;
   static constexpr size_t kXArea = size_t(FW) * 2 * kXWin * 16;
   static constexpr size_t kCtxArea = size_t(FW) * kQN * sizeof(StripCtx);
-  // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN]
-  static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN) * 8;
+  // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2]
+  static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 4) * 8;
   static constexpr size_t kSmem = kSlotArea + kXArea + kCtxArea + kBarArea;
 };
 
@@ -250,24 +306,28 @@ struct FlowCfg {
 // PROF: per-warp clock64 phase timers (experiment builds only), written to
 // P.prof[(blockIdx.x * 2*FW + warp) * 16 + phase].
 template <int FW, int FS, int SLOT, bool PROF = false>
-__global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant__ FlowParams P) {
+__global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_constant__ FlowParams P) {
   using namespace flowdev;
   using Cfg = FlowCfg<FW, FS, SLOT>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool producer = warp >= FW;
-  const int c = producer ? warp - FW : warp;  // pair index
+  constexpr bool kSep = flow_sep<FW>();
+  const bool producer = warp >= FW && warp < 2 * FW;
+  const bool stager_warp = kSep && warp >= 2 * FW;
+  const int c = warp % FW;  // pair index
   unsigned char* slots = smem + size_t(c) * FS * SLOT;
   double2* xb = reinterpret_cast<double2*>(smem + Cfg::kSlotArea) + c * 2 * kXWin;
   StripCtx* ctx = reinterpret_cast<StripCtx*>(smem + Cfg::kSlotArea + Cfg::kXArea) + c * kQN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kCtxArea) +
-                   c * (2 * FS + 2 * kQN);
+                   c * (2 * FS + 2 * kQN + 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + FS;
   uint64_t* cfull = bars + 2 * FS;
   uint64_t* cempty = bars + 2 * FS + kQN;
+  uint64_t* xfull = bars + 2 * FS + 2 * kQN;      // x window of strip k staged (buffer k & 1)
+  uint64_t* xempty = bars + 2 * FS + 2 * kQN + 2;  // buffer k & 1 released by the consumer
   if (producer && lane == 0) {
-    for (int s = 0; s < 2 * FS + 2 * kQN; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < 2 * FS + 2 * kQN + 4; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -303,6 +363,25 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
       __VA_ARGS__;                              \
     }                                           \
   } while (0)
+
+  // x stager: stages the x window of each of the pair's strips, up to two
+  // strips ahead of the consumer (double buffer xb[k & 1])
+  auto stager = [&](auto ns, int sl, unsigned mask, bool arriver) {
+    constexpr int NS = decltype(ns)::value;
+    const int nmine = gw < P.nstrips ? (P.nstrips - 1 - gw) / P.nwarps + 1 : 0;
+    for (int k = 0; k < nmine; ++k) {
+      const int sc = k % kQN, b = k & 1;
+      FLOW_T(3, mbar_wait(&cfull[sc], (k / kQN) & 1));
+      const StripCtx& C = ctx[sc];
+      if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
+      if (C.s.xcols <= kXWin && P.nodeps != 2) {
+        const StageIO io = P.st[C.s.stage];
+        FLOW_T(13, stage_x<NS>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
+      }
+      __syncwarp(mask);
+      if (arriver) mbar_arrive(&xfull[b]);
+    }
+  };
 
   if (producer) {
     if (lane == 0) {
@@ -358,18 +437,21 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
         }
       }
       while (kf <= nmine) prefetch(true);
+    } else if (!kSep) {
+      stager(std::integral_constant<int, 31>{}, lane - 1, 0xfffffffeu, lane == 1);  // lanes 1..31
     }
     __syncwarp();
+  } else if (stager_warp) {
+    stager(std::integral_constant<int, 32>{}, lane, 0xffffffffu, lane == 0);
   } else {
     unsigned q = 0;
-    int xsel = 0;
-    bool have_x = false;
     for (int k = 0;; ++k) {
       const int sc = k % kQN;
       FLOW_T(2, mbar_wait(&cfull[sc], (k / kQN) & 1));
       const StripCtx& C = ctx[sc];
       if (C.s.y0 < 0) break;
       if (P.nodeps == 2) {  // timing experiment: stream the payload only
+        mbar_wait(&xfull[k & 1], (k >> 1) & 1);
         const int cpc = chunk_cols_for(C.s.h, SLOT);
         for (int j = 0; j < C.s.nseg; ++j)
           for (int col0 = 0; col0 < C.g[j].n; col0 += cpc, ++q) {
@@ -377,7 +459,11 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q % FS]);
           }
-        if (lane == 0) mbar_arrive(&cempty[sc]);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&xempty[k & 1]);
+          mbar_arrive(&cempty[sc]);
+        }
         continue;
       }
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
@@ -385,24 +471,8 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
       const double2* xin = io.x + (io.x_par ? par_off : 0);
       double2* yout = io.y + (io.y_par ? par_off : 0);
       const bool fast = C.s.xcols <= kXWin;
-      double2* xcur = xb + xsel * kXWin;
-      if (fast && !have_x) {
-        FLOW_T(4, gather_x(C, xin, io.xperm, xcur, lane));
-        if (PROF) tm[11] += 1;  // strips whose x was not prefetched
-      }
-      // The next strip's x: loads issued now, validated after this strip.
-      double2 nx[kXPerLane];
-      const StripCtx* Cn = nullptr;
-      const double2* nxin = nullptr;
-      {
-        const int sn = (k + 1) % kQN;
-        if (mbar_test(&cfull[sn], ((k + 1) / kQN) & 1) && ctx[sn].s.y0 >= 0 && ctx[sn].s.xcols <= kXWin) {
-          Cn = &ctx[sn];
-          const StageIO nio = P.st[Cn->s.stage];
-          nxin = nio.x + (nio.x_par ? par_off : 0);
-          FLOW_T(6, load_x_regs(*Cn, nxin, nio.xperm, nx, lane));
-        }
-      }
+      double2* xcur = xb + (k & 1) * kXWin;
+      FLOW_T(4, mbar_wait(&xfull[k & 1], (k >> 1) & 1));  // staged by the producer warp's lanes 1..31
       // Lane mapping: strips of <= 16 rows use both half-warps (row = lane&15,
       // column parity = lane>>4, combined by one shuffle at the end), wider
       // strips one lane per row.
@@ -487,24 +557,24 @@ __global__ void __launch_bounds__(2 * FW * 32, 1) k1_flow(const __grid_constant_
       // The stored value is the readiness signal of this row: never let a
       // result alias the "not yet written" sentinel.
       FLOW_T(7, if (live && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
-      bool pref = false;
-      if (Cn) {
-        FLOW_T(5, pref = x_regs_ready(*Cn, nx, lane));
-        if (pref) {
-          store_x_regs(*Cn, nx, xb + (xsel ^ 1) * kXWin, lane);
-          __syncwarp();
-        }
-      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&cempty[sc]);  // context no longer read
-      if (pref) xsel ^= 1;
-      have_x = pref;
+      if (lane == 0) {
+        mbar_arrive(&xempty[k & 1]);  // x buffer free for strip k + 2
+        mbar_arrive(&cempty[sc]);     // context no longer read
+      }
     }
   }
   if (PROF) {
     tm[10] = clock64() - t_start;  // until this warp is done
+    long long* out = P.prof + (static_cast<int64_t>(blockIdx.x) * (flow_threads<FW>() / 32) + warp) * 16;
     if (lane == 0)
-      for (int i = 0; i < 16; ++i) P.prof[(static_cast<int64_t>(blockIdx.x) * 2 * FW + warp) * 16 + i] = tm[i];
+      for (int i = 0; i < 16; ++i) out[i] = tm[i];
+    __syncwarp();
+    if (!kSep && producer && lane == 1) {  // the in-warp x stager's timers
+      out[3] = tm[3];
+      out[12] = tm[12];
+      out[13] = tm[13];
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) = e;

@@ -152,7 +152,7 @@ int flow_setup(int num_sms) {
                                   static_cast<int>(smem)),
              "flow smem attribute");
   int per_sm = 0;
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_flow<FW, FS, SLOT>, 2 * FW * 32, smem),
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_flow<FW, FS, SLOT>, flow_threads<FW>(), smem),
              "occupancy");
   if (per_sm < 1) throw detail::CudaFailure("k1_flow does not fit on an SM");
   return std::min(per_sm * num_sms, kMaxFlowCtas);
@@ -173,7 +173,7 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
   P.nwarps = grid * FW;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
-  cfg.blockDim = dim3(2 * FW * 32, 1, 1);
+  cfg.blockDim = dim3(flow_threads<FW>(), 1, 1);
   cfg.dynamicSmemBytes = FlowCfg<FW, FS, SLOT>::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

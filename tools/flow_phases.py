@@ -14,8 +14,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_1908_09376_b200 as M  # noqa: E402
 
-NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "-", "C: x gather+poll (not prefetched)",
-         "C: next-x validate", "C: next-x load issue", "C: y store", "C: wait full slot", "C: FMA loop", "total", "strips w/o prefetched x"]
+NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "X: wait ctx", "C: wait x staged",
+         "-", "-", "C: y store", "C: wait full slot", "C: FMA loop", "total", "-",
+         "X: wait x buffer free", "X: gather+poll"]
 
 
 def main():
@@ -31,13 +32,17 @@ def main():
     torch.cuda.synchronize()
     fw = {15: 4, 31: 8, 47: 6}[flags & 63]
     grid = 148
-    n = grid * 2 * fw * 16
+    nw = (3 if fw <= 4 else 2) * fw  # warps per CTA: consumers, producers (+ x stagers when fw <= 4)
+    n = grid * nw * 16
     out = np.zeros(n, dtype=np.int64)
     M.lib().midbf_plan_flow_profile(plan._h, out.ctypes.data_as(C.POINTER(C.c_int64)), C.c_int64(n))
-    t = out.reshape(grid, 2 * fw, 16)
-    cons, prod = t[:, :fw, :].reshape(-1, 16), t[:, fw:, :].reshape(-1, 16)
+    t = out.reshape(grid, nw, 16)
+    cons, prod = t[:, :fw, :].reshape(-1, 16), t[:, fw:2 * fw, :].reshape(-1, 16)
+    roles = [("consumer", cons), ("producer", prod)]
+    if nw == 3 * fw:
+        roles.append(("x stager", t[:, 2 * fw:, :].reshape(-1, 16)))
     clk = 1.965e3  # cycles per us
-    for role, arr in (("consumer", cons), ("producer", prod)):
+    for role, arr in roles:
         print(f"== {role} warps ({len(arr)}), mean over warps, us")
         for i, name in enumerate(NAMES):
             if arr[:, i].any():
