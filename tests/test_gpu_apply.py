@@ -117,6 +117,25 @@ def test_single_rhs_kernel_variants(pair, variant):
         assert plan.launches(1) == 1
 
 
+def test_multi_rhs_runs_are_bitwise_identical(pair):
+    """k2_flow: fixed-order DMMA accumulation, no atomics on values."""
+    name, K, Fo, Fm, plan = pair
+    X = cvec(Fo.ncols, 23, cols=40)
+    a, b = plan.apply(X), plan.apply(X)
+    assert np.array_equal(a, b)
+
+
+def test_many_slices(pair):
+    """300 RHS = 4 x 64 + a 44-wide tail: five launches with alternating
+    tile widths, forward and transpose."""
+    name, K, Fo, Fm, plan = pair
+    X = cvec(Fo.ncols, 24, cols=300)
+    assert rel(plan.apply(X), Fo.apply(X)) <= TOL
+    Y = cvec(Fo.nrows, 25, cols=300)
+    assert rel(plan.apply(Y, transpose=True), Fo.apply_transpose(Y)) <= TOL
+    assert plan.launches(300) == 5
+
+
 def test_runs_are_bitwise_identical(pair):
     name, K, Fo, Fm, plan = pair
     f = cvec(Fo.ncols, 14)
