@@ -434,13 +434,30 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
     cuda_check(e2, "k0_repack");
   }
   if (D.max_seg <= kMaxSeg) {  // one self-contained metadata record per strip for k1_flow
+    // Deal order within each stage: by the last previous-stage strip the
+    // strip reads from (any order inside a stage keeps the deadlock-freedom
+    // argument: every dependency lies in an earlier stage).
+    std::vector<size_t> order(strips.size());
+    for (size_t t = 0; t < strips.size(); ++t) order[t] = t;
+    // (measured within noise of the natural order: cfg1 64.1 vs 64.2 us,
+    // cfg2 270.7 vs 272.0 us)
+    auto maxdep = [&](size_t t) {
+      int32_t m = 0;
+      for (int j = 0; j < strips[t].nseg; ++j) m = std::max(m, segs[static_cast<size_t>(strips[t].seg0 + j)].dep1);
+      return m;
+    };
+    for (const Stage& stg : D.stages) {
+      auto b = order.begin() + stg.strip0, e = b + stg.nstrips;
+      std::stable_sort(b, e, [&](size_t x, size_t y) { return maxdep(x) < maxdep(y); });
+    }
     std::vector<StripCtx> ctxs(strips.size());
     for (size_t t = 0; t < strips.size(); ++t) {
+      const size_t o = order[t];
       StripCtx& c = ctxs[t];
       std::memset(static_cast<void*>(&c), 0, sizeof(c));
-      c.s = strips[t];
-      c.s.seg0 = static_cast<int32_t>(t);
-      for (int j = 0; j < strips[t].nseg; ++j) c.g[j] = segs[static_cast<size_t>(strips[t].seg0 + j)];
+      c.s = strips[o];
+      c.s.seg0 = static_cast<int32_t>(o);
+      for (int j = 0; j < strips[o].nseg; ++j) c.g[j] = segs[static_cast<size_t>(strips[o].seg0 + j)];
     }
     up(reinterpret_cast<void**>(&D.d_ctx), ctxs.data(), ctxs.size() * sizeof(StripCtx), "upload strip records");
   }
