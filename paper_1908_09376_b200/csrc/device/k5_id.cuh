@@ -14,9 +14,12 @@
 // to the host's serial sums).  The phase fix of R's rows is skipped: it
 // cancels in R11^-1 R12 and leaves |R_ii| unchanged.
 //
-// One warp per block, rows distributed over lanes (row i -> lane i % 32,
-// register slot i / 32; m <= 32 * kIdRows), squared norms and the column
-// permutation in shared memory (n <= kIdCols).  Blocks outside those limits,
+// One CTA of kIdWarps warps per block: rows distributed over lanes (row i
+// -> lane i % 32, register slot i / 32; m <= 32 * kIdRows), squared norms,
+// the column permutation and the Householder vector in shared memory
+// (n <= kIdCols).  Per step warp 0 picks the pivot and builds the reflector,
+// then all warps update interleaved trailing columns (two CTA barriers per
+// step).  Blocks outside those limits,
 // and blocks whose first min(m,n,k_max) diagonals hit id_rank's 1e-14 tail
 // trim below the full factorization (the host's fallback case), return
 // rank -1: the caller recomputes them on the host.
@@ -31,8 +34,8 @@ namespace midbf::dev {
 constexpr int kIdRows = 8;             // register slots per lane: m <= 256
 constexpr int kIdMaxRows = 32 * kIdRows;
 constexpr int kIdCols = 512;           // n <= 512
-constexpr int kIdWarps = 4;            // warps (blocks) per CTA
-constexpr size_t kIdSmem = size_t(kIdWarps) * kIdCols * (8 + 8 + 4);
+constexpr int kIdWarps = 4;            // warps cooperating on one block
+constexpr size_t kIdSmem = size_t(kIdCols) * (8 + 8 + 4) + size_t(kIdMaxRows) * 16 + 64;
 
 struct IdTask {
   int64_t off;   // block B (m x n, column-major) in the workspace
@@ -70,24 +73,27 @@ __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws,
                                                        int* __restrict__ skel, int kcap) {
   using namespace k5dev;
   extern __shared__ __align__(16) unsigned char k5smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* cur = reinterpret_cast<double*>(k5smem) + wib * kIdCols;
-  double* ref = reinterpret_cast<double*>(k5smem) + (kIdWarps + wib) * kIdCols;
-  int* perm = reinterpret_cast<int*>(reinterpret_cast<double*>(k5smem) + 2 * kIdWarps * kIdCols) + wib * kIdCols;
-  const int t = blockIdx.x * kIdWarps + wib;
+  double* cur = reinterpret_cast<double*>(k5smem);
+  double* ref = cur + kIdCols;
+  double2* vsh = reinterpret_cast<double2*>(ref + kIdCols);  // Householder vector (rows)
+  int* perm = reinterpret_cast<int*>(vsh + kIdMaxRows);
+  __shared__ int sh_p, sh_stop, sh_rank, sh_fb;
+  __shared__ double sh_beta;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int t = blockIdx.x;
   if (t >= ntasks) return;
   const IdTask tk = tasks[t];
   const int m = tk.m, n = tk.n;
   if (m > kIdMaxRows || n > kIdCols || m <= 0 || n <= 0) {
-    if (lane == 0) ranks[t] = -1;
+    if (tid == 0) ranks[t] = -1;
     return;
   }
   double2* B = ws + tk.off;
   const int full = min(m, n);
   const int cap = kmax > 0 ? min(full, kmax) : full;
 
-  // squared column norms
-  for (int j = 0; j < n; ++j) {
+  // squared column norms (warp w: columns w, w + kIdWarps, ...)
+  for (int j = w; j < n; j += kIdWarps) {
     const double2* c = B + static_cast<int64_t>(j) * m;
     double s = 0.0;
 #pragma unroll
@@ -98,87 +104,107 @@ __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws,
     s = wsum(s);
     if (lane == 0) cur[j] = ref[j] = s;
   }
-  for (int j = lane; j < n; j += 32) perm[j] = j;
-  __syncwarp();
+  for (int j = tid; j < n; j += kIdWarps * 32) perm[j] = j;
+  __syncthreads();
 
   int k = 0;
   for (; k < cap; ++k) {
-    // pivot: largest remaining norm, lowest index on ties
-    double bv = -1.0;
-    int bp = n;
-    for (int j = k + lane; j < n; j += 32)
-      if (cur[j] > bv) bv = cur[j], bp = j;
+    if (w == 0) {  // pivot: largest remaining norm, lowest index on ties
+      double bv = -1.0;
+      int bp = n;
+      for (int j = k + lane; j < n; j += 32)
+        if (cur[j] > bv) bv = cur[j], bp = j;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+      }
+      if (lane == 0) {
+        sh_p = bp;
+        if (bp != k) {
+          const int tp = perm[k];
+          perm[k] = perm[bp];
+          perm[bp] = tp;
+          double tv = cur[k];
+          cur[k] = cur[bp];
+          cur[bp] = tv;
+          tv = ref[k];
+          ref[k] = ref[bp];
+          ref[bp] = tv;
+        }
+      }
     }
-    const int p = bp;
+    __syncthreads();
+    const int p = sh_p;
     if (p != k) {
       double2* a = B + static_cast<int64_t>(k) * m;
       double2* b = B + static_cast<int64_t>(p) * m;
-      for (int i = lane; i < m; i += 32) {
+      for (int i = tid; i < m; i += kIdWarps * 32) {
         const double2 tmp = a[i];
         a[i] = b[i];
         b[i] = tmp;
       }
-      if (lane == 0) {
-        const int tp = perm[k];
-        perm[k] = perm[p];
-        perm[p] = tp;
-        double tv = cur[k];
-        cur[k] = cur[p];
-        cur[p] = tv;
-        tv = ref[k];
-        ref[k] = ref[p];
-        ref[p] = tv;
-      }
-      __syncwarp();
     }
-    // Householder vector from column k (rows k..m-1)
+    __syncthreads();
     double2* col = B + static_cast<int64_t>(k) * m;
-    double2 x[kIdRows];
-    double xs = 0.0;
+    if (w == 0) {  // Householder vector from column k (rows k..m-1)
+      double2 x[kIdRows];
+      double xs = 0.0;
 #pragma unroll
-    for (int r = 0; r < kIdRows; ++r) {
-      const int i = lane + 32 * r;
-      x[r] = (i >= k && i < m) ? col[i] : make_double2(0, 0);
-      xs += nrm2(x[r]);
-    }
-    xs = wsum(xs);
-    const double xn = sqrt(xs);
-    if (xn == 0.0) break;
-    double2 mine = make_double2(0, 0);  // row k's entry (static register indexing)
+      for (int r = 0; r < kIdRows; ++r) {
+        const int i = lane + 32 * r;
+        x[r] = (i >= k && i < m) ? col[i] : make_double2(0, 0);
+        xs += nrm2(x[r]);
+      }
+      xs = wsum(xs);
+      const double xn = sqrt(xs);
+      if (xn == 0.0) {
+        if (lane == 0) sh_stop = 1;
+      } else {
+        double2 mine = make_double2(0, 0);  // row k's entry (static register indexing)
 #pragma unroll
-    for (int r = 0; r < kIdRows; ++r)
-      if (r == (k >> 5)) mine = x[r];
-    const double2 a0 = make_double2(__shfl_sync(0xffffffffu, mine.x, k & 31), __shfl_sync(0xffffffffu, mine.y, k & 31));
-    const double aa = sqrt(nrm2(a0));
-    const double2 ph = aa == 0.0 ? make_double2(1.0, 0.0) : make_double2(a0.x / aa, a0.y / aa);
-    const double2 v0 = make_double2(a0.x + ph.x * xn, a0.y + ph.y * xn);
-    double vs = 0.0;
+        for (int r = 0; r < kIdRows; ++r)
+          if (r == (k >> 5)) mine = x[r];
+        const double2 a0 =
+            make_double2(__shfl_sync(0xffffffffu, mine.x, k & 31), __shfl_sync(0xffffffffu, mine.y, k & 31));
+        const double aa = sqrt(nrm2(a0));
+        const double2 ph = aa == 0.0 ? make_double2(1.0, 0.0) : make_double2(a0.x / aa, a0.y / aa);
+        const double2 v0 = make_double2(a0.x + ph.x * xn, a0.y + ph.y * xn);
+        double vs = 0.0;
 #pragma unroll
-    for (int r = 0; r < kIdRows; ++r) {
-      const int i = lane + 32 * r;
-      if (i > k && i < m) {
-        x[r] = cdiv(x[r], v0);
-        vs += nrm2(x[r]);
-        col[i] = x[r];
+        for (int r = 0; r < kIdRows; ++r) {
+          const int i = lane + 32 * r;
+          if (i > k && i < m) {
+            x[r] = cdiv(x[r], v0);
+            vs += nrm2(x[r]);
+            col[i] = x[r];
+          }
+        }
+        vs = wsum(vs);
+        if (lane == (k & 31)) col[k] = make_double2(-ph.x * xn, -ph.y * xn);
+#pragma unroll
+        for (int r = 0; r < kIdRows; ++r) {
+          const int i = lane + 32 * r;
+          if (i < m) vsh[i] = i == k ? make_double2(1.0, 0.0) : (i > k ? x[r] : make_double2(0, 0));
+        }
+        if (lane == 0) {
+          sh_beta = 2.0 / (1.0 + vs);
+          sh_stop = 0;
+        }
       }
     }
-    vs = wsum(vs);
-    const double beta = 2.0 / (1.0 + vs);
-    if (lane == (k & 31)) col[k] = make_double2(-ph.x * xn, -ph.y * xn);
-    // v = [1; x(k+1:)], zero above row k
+    __syncthreads();
+    if (sh_stop) break;
+    const double beta = sh_beta;
     double2 v[kIdRows];
 #pragma unroll
     for (int r = 0; r < kIdRows; ++r) {
       const int i = lane + 32 * r;
-      v[r] = i == k ? make_double2(1.0, 0.0) : (i > k && i < m ? x[r] : make_double2(0, 0));
+      v[r] = i < m ? vsh[i] : make_double2(0, 0);
     }
-    // trailing columns: c -= beta v (v^H c); squared-norm downdate
-    for (int j = k + 1; j < n; ++j) {
+    // trailing columns (warp w: k+1+w, k+1+w+kIdWarps, ...): c -= beta v (v^H c)
+    for (int j = k + 1 + w; j < n; j += kIdWarps) {
       double2* c = B + static_cast<int64_t>(j) * m;
       double2 cv[kIdRows];
       double wr = 0.0, wi = 0.0;
@@ -214,18 +240,17 @@ __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws,
         cj = m - k > 1 ? s : 0.0;
         rj = cj;
       }
-      __syncwarp();
       if (lane == 0) cur[j] = cj, ref[j] = rj;
-      __syncwarp();
     }
+    __syncthreads();
   }
   const int steps = k;
-  __syncwarp();
+  __syncthreads();
 
   // rank (id_rank, src/linalg.cpp:249-264) on |R_ii|, i < steps
-  int rank = 0;
-  bool fallback = false;
-  if (lane == 0) {
+  if (tid == 0) {
+    int rank = 0;
+    bool fallback = false;
     const double d0 = steps > 0 ? sqrt(nrm2(B[0])) : 0.0;
     if (steps > 0 && d0 != 0.0) {
       if (steps == cap && cap < full)
@@ -242,19 +267,18 @@ __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws,
           }
       if (kmax > 0) rank = min(rank, kmax);
     }
+    sh_rank = rank;
+    sh_fb = fallback ? 1 : 0;
+    ranks[t] = fallback ? -1 : rank;
   }
-  rank = __shfl_sync(0xffffffffu, rank, 0);
-  fallback = __shfl_sync(0xffffffffu, fallback, 0);
-  if (fallback) {
-    if (lane == 0) ranks[t] = -1;
-    return;
-  }
-  if (lane == 0) ranks[t] = rank;
-  for (int i = lane; i < rank; i += 32) skel[static_cast<int64_t>(t) * kcap + i] = perm[i];
+  __syncthreads();
+  if (sh_fb) return;
+  const int rank = sh_rank;
+  for (int i = tid; i < rank; i += kIdWarps * 32) skel[static_cast<int64_t>(t) * kcap + i] = perm[i];
 
-  // V(:, perm[j]) = e_j (j < rank), else R11^-1 R(0:rank, j); lane per column
+  // V(:, perm[j]) = e_j (j < rank), else R11^-1 R(0:rank, j); thread per column
   double2* V = out + tk.ooff;
-  for (int j = lane; j < n; j += 32) {
+  for (int j = tid; j < n; j += kIdWarps * 32) {
     const int pj = perm[j];
     auto at = [&](int i) -> double2& {
       return rowid ? V[static_cast<int64_t>(i) * n + pj] : V[static_cast<int64_t>(pj) * rank + i];

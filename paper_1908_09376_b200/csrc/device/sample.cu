@@ -532,7 +532,7 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
     cuda_check(cudaGetLastError(), "k3_sample_ws launch");
     cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
                "k5 smem attribute");
-    k5_id<<<(nt + kIdWarps - 1) / kIdWarps, kIdWarps * 32, kIdSmem, I.stream>>>(
+    k5_id<<<nt, kIdWarps * 32, kIdSmem, I.stream>>>(
         P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0,
         P.d_vals, P.d_rank, P.d_skel, kcap);
     cuda_check(cudaGetLastError(), "k5_id launch");
@@ -674,7 +674,7 @@ extern "C" int midbf_cid_batch(const double* blocks, const int64_t* dims, int64_
     cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
                "k5 smem attribute");
     const unsigned nt = static_cast<unsigned>(nblocks);
-    k5_id<<<(nt + kIdWarps - 1) / kIdWarps, kIdWarps * 32, kIdSmem>>>(
+    k5_id<<<nt, kIdWarps * 32, kIdSmem>>>(
         P.d_ws, d_tk, static_cast<int>(nblocks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, 0, P.d_vals,
         P.d_rank, P.d_skel, static_cast<int>(kcap));
     const cudaError_t e = cudaGetLastError();
