@@ -445,6 +445,8 @@ def rsvd_dense(A, R0, C0, r, seed):
     a, (m, n), dt, cplx = _dense(A)
     R0 = np.ascontiguousarray(R0, dtype=np.int64)
     C0 = np.ascontiguousarray(C0, dtype=np.int64)
+    if R0.shape != C0.shape or R0.ndim != 1:  # one count crosses the ABI (src/linalg.cpp:142, equal sizes)
+        raise ValueError("rsvd: row and column samples differ in size")
     U, V, S = _out((m, r), dt), _out((n, r), dt), np.zeros(r)
     info = np.zeros(4, dtype=np.int64)
     _check(lib().midbf_rsvd_dense(_p(a), i64(m), i64(n), 1 if cplx else 0, _ip(R0), _ip(C0), i64(len(R0)), i64(r),

@@ -70,3 +70,30 @@ def test_error_classes_follow_the_reference():
         M.idbf_factorize(K, 0, sampler="host")
     with pytest.raises(RuntimeError):  # missing container (src/butterfly_io.cpp:105)
         M.load_factorization("/nonexistent/midbf.bin")
+
+
+def test_new_entry_points_fail_loudly_without_gpu():
+    """K5 batched IDs, low-rank phase sampling and eps_K need the device."""
+    if M.device_count() > 0:
+        pytest.skip("a device is visible")
+    with pytest.raises(M.MidbfCudaError):
+        M.cid_batch([np.eye(4, dtype=complex)], 2, 1e-9)
+    X = np.random.default_rng(2).random((64, 2))
+    K = M.Kernel(M.KIND_FIO2D, X=X, Omega=X)
+    with pytest.raises(M.MidbfCudaError):
+        M.lowrank_phase(K, 2, 2, seed=1)
+    with pytest.raises(M.MidbfCudaError):
+        M.eps_K(K, np.zeros((64, 1)), np.zeros((64, 1)), 8, 1)
+
+
+def test_host_linear_algebra_argument_errors():
+    """rsvd / pinv / thin_q are host-only and reject bad arguments like the
+    reference (std::invalid_argument -> ValueError)."""
+    A = np.random.default_rng(3).standard_normal((10, 8))
+    with pytest.raises(ValueError):  # sample index out of range
+        M.rsvd_dense(A, [0, 11], [0, 1], 1, 0)
+    with pytest.raises(ValueError):  # R0 / C0 of different sizes
+        M.rsvd_dense(A, [0, 1, 2], [0, 1], 1, 0)
+    P, cond = M.pinv(A)
+    assert P.shape == (8, 10) and np.isfinite(cond)
+    assert M.thin_q(A).shape == (10, 8)
