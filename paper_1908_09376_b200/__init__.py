@@ -469,9 +469,13 @@ def lowrank_phase(kernel, r, q=2, seed=0):
 
 def eps_K(kernel, U, V, nsamp=256, seed=0):
     """metrics::eps_K of a low-rank phase U V^T against the kernel (GPU entries)."""
-    r = np.shape(U)[1]
-    u, _, _, _ = _dense(np.asarray(U, dtype=np.float64))
-    v, _, _, _ = _dense(np.asarray(V, dtype=np.float64))
+    U = np.asarray(U, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    r = U.shape[1] if U.ndim == 2 else -1
+    if U.shape != (kernel.nrows, r) or V.shape != (kernel.ncols, r):
+        raise ValueError("eps_K: U must be nrows x r and V ncols x r")
+    u, _, _, _ = _dense(U)
+    v, _, _, _ = _dense(V)
     out = C.c_double()
     _check(lib().midbf_eps_K(C.byref(kernel.desc), _p(u), _p(v), i64(r), i64(nsamp), u64(seed), C.byref(out)))
     return out.value
