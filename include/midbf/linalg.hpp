@@ -1,12 +1,13 @@
 // Interpolative decompositions used by the factorization (drop-in for the ID
-// subset of the reference's proj/include/midbf/linalg.hpp:56-108).  The
-// randomized SVD / pinv / thin_q part of that header belongs to phase
-// recovery and is out of scope.
+// subset of the reference's proj/include/midbf/linalg.hpp:56-108); the
+// randomized SVD / pinv / thin_q part of that header is in midbf/lowrank.hpp.
 //
-// B200 build note: the IDs stay on the host (north_star).  The pivoted QR is
-// truncated after k_max steps and never forms Q: rows 0..k_max-1 of R and the
-// first k_max pivots are final after step k_max-1, so the skeleton, the rank
-// and the interpolation matrix equal the reference's full-QR result
+// These are the host IDs (bitwise the oracle's arithmetic); the factorization
+// runs its IDs on the GPU by default (K5, midbf_cid_batch) and falls back to
+// these for blocks the device hands back.  The pivoted QR is truncated after
+// k_max steps and never forms Q: rows 0..k_max-1 of R and the first k_max
+// pivots are final after step k_max-1, so the skeleton, the rank and the
+// interpolation matrix equal the reference's full-QR result
 // (src/linalg.cpp:23-107, 266-286).
 #pragma once
 
