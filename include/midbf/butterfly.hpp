@@ -12,7 +12,8 @@
 //   * idbf_factorize samples every kernel entry on the GPU when given a
 //     `KernelDesc` (fused exp(2*pi*i*Phi) sampler); the EntryFn overload keeps
 //     the reference's host-callback semantics for arbitrary kernels.
-//   * the interpolative decompositions stay on the host (OpenMP).
+//   * with a `KernelDesc`, the interpolative decompositions run on the GPU
+//     too (K5); the EntryFn overload runs them on the host (OpenMP).
 #pragma once
 
 #include <cstdint>
@@ -79,7 +80,9 @@ Factorization idbf_factorize(const EntryFn& K, const tree::ClusterTree& tx, cons
                              const MatXd& X, const MatXd& Omega, const Config& cfg);
 
 // B200 overload: every entry sampled on the GPU from a typed kernel
-// description (explicit 2D/3D FIO phase, low-rank A*B^T phase, x.xi).
+// description (explicit 2D/3D FIO phase, low-rank A*B^T phase, x.xi), and
+// every ID computed there (K5; blocks the device hands back are redone on
+// the host).
 Factorization idbf_factorize(const ker::KernelDesc& K, const tree::ClusterTree& tx, const tree::ClusterTree& tomega,
                              const MatXd& X, const MatXd& Omega, const Config& cfg);
 
