@@ -335,20 +335,28 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   const unsigned e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
   const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
-  {
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t di = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (!producer) {
     // stage -1: the input permutation, gathered once into the head of this
-    // apply's set (sentinel-armed; stage 0 polls it like any other stage)
+    // apply's set (sentinel-armed; stage 0 polls it like any other stage) by
+    // the consumer / stager warps while the producers start streaming panels
+    const int nw = flow_threads<FW>() / 32 - FW;  // non-producer warps per CTA
+    const int wl = warp < FW ? warp : warp - FW;   // index among them
+    const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * nw + wl) * 32 + lane;
+    const int64_t di = static_cast<int64_t>(gridDim.x) * nw * 32;
     double2* x0 = P.stagebuf + par_off;
     for (int64_t i = i0; i < P.in_len; i += di) {
       const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
       x0[i] = make_double2(unsentinel(v.x), unsentinel(v.y));
     }
-    // re-arm the other set for the next apply (nobody reads it now)
-    long long* other = reinterpret_cast<long long*>(P.stagebuf + ((e & 1u) ? 0 : P.par_elems));
-    for (int64_t i = i0; i < 2 * P.par_elems; i += di) other[i] = -1ll;
   }
+  // re-arm the other set for the next apply (nobody reads it during this
+  // one): done by the x stagers once their last window is staged
+  auto rearm = [&](int sl, int ns) {
+    long long* other = reinterpret_cast<long long*>(P.stagebuf + ((e & 1u) ? 0 : P.par_elems));
+    const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * FW + c) * ns + sl;
+    const int64_t di = static_cast<int64_t>(gridDim.x) * FW * ns;
+    for (int64_t i = i0; i < 2 * P.par_elems; i += di) other[i] = -1ll;
+  };
   long long tm[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) tm[i] = 0;
@@ -381,6 +389,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       __syncwarp(mask);
       if (arriver) mbar_arrive(&xfull[b]);
     }
+    rearm(sl, NS);
   };
 
   if (producer) {
