@@ -107,6 +107,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cmac(double& ar, double& ai, double2 m, double2 x) {
   ar = fma(m.x, x.x, ar);
@@ -310,6 +315,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   using namespace flowdev;
   using Cfg = FlowCfg<FW, FS, SLOT>;
   extern __shared__ __align__(128) unsigned char smem[];
+  const unsigned long long g_entry = PROF ? globaltimer_ns() : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr bool kSep = flow_sep<FW>();
   const bool producer = warp >= FW && warp < 2 * FW;
@@ -361,6 +367,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
 #pragma unroll
   for (int i = 0; i < 16; ++i) tm[i] = 0;
   long long t_start = PROF ? clock64() : 0;
+  const unsigned long long g_prologue = PROF ? globaltimer_ns() : 0;
 #define FLOW_T(i, ...)                          \
   do {                                          \
     if (PROF) {                                 \
@@ -575,6 +582,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   }
   if (PROF) {
     tm[10] = clock64() - t_start;  // until this warp is done
+    tm[11] = static_cast<long long>(globaltimer_ns());  // absolute ns: this warp's end
+    tm[14] = static_cast<long long>(g_entry);          // ... kernel entry
+    tm[15] = static_cast<long long>(g_prologue);       // ... after the prologue
     long long* out = P.prof + (static_cast<int64_t>(blockIdx.x) * (flow_threads<FW>() / 32) + warp) * 16;
     if (lane == 0)
       for (int i = 0; i < 16; ++i) out[i] = tm[i];

@@ -1,6 +1,6 @@
 """Phase breakdown of k1_flow at cfg1 (flag bit 12 phase timers).
 
-    python tools/flow_phases.py [flags]
+    python tools/flow_phases.py [flags] [config]
 Prints, per warp role, the mean cycles per apply spent in each phase.
 """
 import ctypes as C
@@ -21,8 +21,9 @@ NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "X: wait ctx", "C: 
 
 def main():
     flags = int(sys.argv[1]) if len(sys.argv) > 1 else 31
-    K, X, Om, fk, nrhs, desc = bench.workload("cfg1")
-    F = M.idbf_factorize(K, 64, k=30, eps=1e-9, seed=M.chain(0, 0x666163))
+    config = sys.argv[2] if len(sys.argv) > 2 else "cfg1"
+    K, X, Om, fk, nrhs, desc = bench.workload(config)
+    F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, seed=M.chain(0, 0x666163))
     plan = F.plan(1)
     M.lib().midbf_plan_set_flags(plan._h, flags | 4096)
     f = torch.randn(F.ncols, dtype=torch.complex128, device="cuda")
@@ -42,10 +43,15 @@ def main():
     if nw == 3 * fw:
         roles.append(("x stager", t[:, 2 * fw:, :].reshape(-1, 16)))
     clk = 1.965e3  # cycles per us
+    ent, pro, end = t[:, :, 14], t[:, :, 15], t[:, :, 11]
+    base = ent[ent > 0].min()
+    print(f"== launch (global timer, us from the first CTA's entry): entry spread {(ent.max() - base) / 1e3:.2f}, "
+          f"prologue done median {(np.median(pro) - base) / 1e3:.2f} max {(pro.max() - base) / 1e3:.2f}, "
+          f"warp ends median {(np.median(end) - base) / 1e3:.2f} max {(end.max() - base) / 1e3:.2f}")
     for role, arr in roles:
         print(f"== {role} warps ({len(arr)}), mean over warps, us")
         for i, name in enumerate(NAMES):
-            if arr[:, i].any():
+            if name != "-" and arr[:, i].any():
                 v = arr[:, i].mean()
                 print(f"  {name:28s} {v / clk if i != 11 else v:9.2f}   (max {arr[:, i].max() / (clk if i != 11 else 1):.2f})")
 
