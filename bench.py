@@ -234,11 +234,12 @@ def main():
     K, X, Om, fk, nrhs, desc = workload(args.config)
     t0 = time.perf_counter()
     F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="device")
-    t_fac_first = time.perf_counter() - t0  # includes one-time module loading
-    del F
-    t0 = time.perf_counter()
-    F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="device")
-    t_fac = time.perf_counter() - t0
+    t_fac_first = time.perf_counter() - t0  # includes one-time module loading and pool growth
+    for _ in range(2):  # the second call still grows process-wide staging pools; time the third
+        del F
+        t0 = time.perf_counter()
+        F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="device")
+        t_fac = time.perf_counter() - t0
     entries, sample_calls, sample_s = F.sample_stats()
     n_dev_ids, n_host_ids, id_s, _ = F.id_stats()
     plan = F.plan(1)

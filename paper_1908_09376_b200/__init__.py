@@ -242,7 +242,10 @@ class DevicePlan:
 
     def __del__(self):
         if getattr(self, "_owned", False) and getattr(self, "_h", None):
-            lib().midbf_plan_destroy(self._h)
+            try:
+                lib().midbf_plan_destroy(self._h)
+            except TypeError:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3):
@@ -308,7 +311,10 @@ class Factorization:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            lib().midbf_fact_destroy(self._h)
+            try:
+                lib().midbf_fact_destroy(self._h)
+            except TypeError:  # interpreter shutdown: module globals already gone
+                pass
             self._h = None
 
     def factor_count(self):
