@@ -535,6 +535,7 @@ Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   // every launch runs the same set of CTAs
   const int g = std::min({k2flow_grid[0], k2flow_grid[1], k2flow_grid[2]});
   for (int& v : k2flow_grid) v = g;
+  cuda_check(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming), "event");
 }
 
 Plan::~Plan() {
@@ -550,6 +551,7 @@ Plan::~Plan() {
     cudaFree(D.d_sync);
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+  if (ev_last) cudaEventDestroy(ev_last);
   if (s_h2d) {
     cudaStreamSynchronize(s_d2h);
     for (auto& a : aslots) {
@@ -836,11 +838,25 @@ void Plan::prepare_flow(int d) {
 }
 
 void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
+  std::lock_guard<std::recursive_mutex> lock(mu);
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
   ensure_buffers(nrhs);
   if (flow_ok(d, nrhs)) prepare_flow(d);
   if (dir[d].stages.empty()) return;
   if (k2flow_ok(d, nrhs)) ensure_k2flow(d);
+  // after the previous apply on this plan, whichever stream it ran on
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(stream, &cs), "capture status");
+  const bool ordered = cs == cudaStreamCaptureStatusNone;
+  if (ordered) cuda_check(cudaStreamWaitEvent(stream, ev_last, 0), "order applies");
+  struct Done {
+    Plan* p;
+    cudaStream_t s;
+    bool on;
+    ~Done() {
+      if (on) cudaEventRecord(p->ev_last, s);
+    }
+  } done{this, stream, ordered};
   if (!(flags & 4u)) {
     launch(d, in, out, nrhs, stream);
     cuda_check(cudaGetLastError(), "apply");
@@ -879,6 +895,7 @@ static bool is_device_ptr(const void* p) {
 }
 
 void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t stream) {
+  std::lock_guard<std::recursive_mutex> lock(mu);
   if (nrhs < 1) throw std::invalid_argument("nrhs must be >= 1");
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   const int d = transpose ? 1 : 0;
@@ -918,6 +935,7 @@ void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaS
 // (host-written input: it is not ordered after work on `user`), so it must
 // not change until `user` is synchronized.
 void Plan::apply_async(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t user) {
+  std::lock_guard<std::recursive_mutex> lock(mu);
   if (nrhs < 1) throw std::invalid_argument("nrhs must be >= 1");
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   const int d = transpose ? 1 : 0;

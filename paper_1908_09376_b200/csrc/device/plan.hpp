@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -153,6 +154,16 @@ class Plan {
   int64_t acount = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_user = nullptr;
+
+ public:
+  // One apply at a time per plan (the stage buffers, launch epochs and
+  // counters are per plan): `mu` serialises the host side (graph cache,
+  // staging, flags), `ev_last` orders the device work of consecutive applies
+  // across callers' streams.
+  std::recursive_mutex mu;
+
+ private:
+  cudaEvent_t ev_last = nullptr;
 };
 
 std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions);

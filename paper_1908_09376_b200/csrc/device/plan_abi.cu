@@ -307,6 +307,7 @@ extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out,
 // (stage kernels), bit2 CUDA graphs, bit3 persistent dataflow kernel.
 extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
   return guard([&] {
+    std::lock_guard<std::recursive_mutex> lock(plan->p->mu);
     Plan& p = *plan->p;
     p.flags = flags;
     if ((flags & 4096u) && !p.d_prof)  // phase-timer buffer, allocated outside any capture

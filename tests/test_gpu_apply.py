@@ -226,3 +226,48 @@ def test_pipelined_host_apply(gpu):
     for fi, go in zip(ins, outs):
         assert np.array_equal(go.numpy(), plan.apply(fi.numpy()))
         assert rel(go.numpy(), Fo.apply(fi.numpy())) <= TOL
+
+
+@pytest.mark.parametrize("route", ["default", "stages"])
+def test_concurrent_applies_on_one_plan(gpu, route):
+    """bf::apply is a const function callers may run concurrently: applies on
+    one plan from several host threads, each on its own stream, are ordered
+    by the plan and all match the oracle (the per-stage kernels share work
+    buffers between launches, so they need that ordering)."""
+    import threading
+
+    torch = pytest.importorskip("torch")
+    X = O.grid2d(32)
+    K, Fo = oracle_factorization(O.KIND_FIO2D, X, X, 64, 30, 1e-9)
+    path = saved(Fo)
+    plan = M.DevicePlan.load(path, directions=3)
+    os.unlink(path)
+    if route == "stages":
+        plan.set_flags(flow=False, dmma=False)
+    jobs = [(False, 1), (True, 1), (False, 8)]
+    inputs = [cvec(1024, 90 + i, cols=c) for i, (_, c) in enumerate(jobs)]
+    want = [Fo.apply_transpose(f) if t else Fo.apply(f) for (t, _), f in zip(jobs, inputs)]
+    errors = []
+
+    def worker(i):
+        try:
+            t, c = jobs[i]
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                fd = torch.from_numpy(np.asfortranarray(inputs[i]).reshape(-1, order="F")).cuda()
+                gd = torch.empty_like(fd)
+                for _ in range(30):
+                    plan.apply_ptr(fd.data_ptr(), gd.data_ptr(), c, t, s.cuda_stream)
+                s.synchronize()
+                got = gd.cpu().numpy().reshape((1024, c), order="F")
+            if rel(got, want[i].reshape(1024, c)) > TOL:
+                errors.append((i, rel(got, want[i].reshape(1024, c))))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(jobs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
