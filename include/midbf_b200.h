@@ -186,7 +186,10 @@ int midbf_fact_factor(midbf_fact_t fact, int64_t i, int64_t* out);
 int midbf_fact_tables(midbf_fact_t fact, int64_t i, int64_t* blocks4, int64_t* groups2);
 int midbf_fact_block(midbf_fact_t fact, int64_t i, int64_t b, double* out);
 int midbf_fact_perms(midbf_fact_t fact, int64_t* row_perm, int64_t* col_perm);
-/* Device plan owned by the factorization (built on first use). */
+/* Device plan owned by the factorization (built on first use, both
+ * directions, so the handle stays valid until midbf_fact_destroy).
+ * Applies through the factorization or its plan may come from several
+ * threads / streams at once: a plan runs one apply at a time, in call order. */
 int midbf_fact_plan(midbf_fact_t fact, unsigned directions, midbf_plan_t* out);
 /* bf::apply on the factorization's cached device plan (host or device operands). */
 int midbf_fact_apply(midbf_fact_t fact, const double* f, double* g, int64_t nrhs, int transpose, void* stream);

@@ -640,11 +640,11 @@ MatXc apply_dir(const Factorization& F, const MatXc& in, bool transpose) {
   const Index nin = transpose ? F.nrows : F.ncols;
   const Index nout = transpose ? F.ncols : F.nrows;
   if (in.rows() != nin) throw std::invalid_argument("input length does not match the factorization");
-  midbf_plan_t plan = device_plan(F, transpose ? 2u : 1u);
+  const auto cache = device_plan(F, transpose ? 2u : 1u);  // held for the duration of the apply
   MatXc out(nout, in.cols());
   if (in.cols() == 0) return out;
-  detail::rethrow(midbf_apply(plan, reinterpret_cast<const double*>(in.data()), reinterpret_cast<double*>(out.data()),
-                              in.cols(), transpose ? 1 : 0, nullptr));
+  detail::rethrow(midbf_apply(cache->plan, reinterpret_cast<const double*>(in.data()),
+                              reinterpret_cast<double*>(out.data()), in.cols(), transpose ? 1 : 0, nullptr));
   return out;
 }
 

@@ -215,13 +215,15 @@ int midbf_fact_perms(midbf_fact_t fact, int64_t* rp, int64_t* cp) {
 }
 
 int midbf_fact_plan(midbf_fact_t fact, unsigned directions, midbf_plan_t* out) {
-  return guard([&] { *out = midbf::bf::device_plan(fact->F, directions); });
+  // both directions: a cache holding both is never rebuilt, so the returned
+  // handle stays valid for the factorization's lifetime
+  return guard([&] { *out = midbf::bf::device_plan(fact->F, directions | 3u)->plan; });
 }
 
 int midbf_fact_apply(midbf_fact_t fact, const double* f, double* g, int64_t nrhs, int transpose, void* stream) {
   return guard([&] {
-    midbf_plan_t plan = midbf::bf::device_plan(fact->F, transpose ? 2u : 1u);
-    midbf::detail::rethrow(midbf_apply(plan, f, g, nrhs, transpose, stream));
+    const auto cache = midbf::bf::device_plan(fact->F, transpose ? 2u : 1u);
+    midbf::detail::rethrow(midbf_apply(cache->plan, f, g, nrhs, transpose, stream));
   });
 }
 

@@ -4,6 +4,7 @@
 // the device-plan cache and the sampled-row metric (src/metrics.cpp:26-53).
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <fstream>
 #include <numeric>
 #include <random>
@@ -131,10 +132,12 @@ DevicePlanCache::~DevicePlanCache() {
   if (plan) midbf_plan_destroy(plan);
 }
 
-midbf_plan_t device_plan(const Factorization& F, unsigned directions) {
-  if (F.device && (F.device->directions & directions) == directions) return F.device->plan;
+std::shared_ptr<DevicePlanCache> device_plan(const Factorization& F, unsigned directions) {
+  // one mutex for all factorizations: plan builds are rare and brief
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (F.device && (F.device->directions & directions) == directions) return F.device;
   const unsigned want = directions | (F.device ? F.device->directions : 0u);
-  F.device.reset();
   std::vector<std::int64_t> shape, blocks, groups;
   for (const Factor& fc : F.factors) {
     shape.insert(shape.end(), {fc.rows, fc.cols, static_cast<std::int64_t>(fc.blocks.size()),
@@ -153,8 +156,8 @@ midbf_plan_t device_plan(const Factorization& F, unsigned directions) {
                                            static_cast<std::int64_t>(F.factors.size()), shape.data(), blocks.data(),
                                            groups.data(), ptrs.data(), want));
   cache->directions = want;
-  F.device = cache;
-  return cache->plan;
+  F.device = cache;  // earlier entries live on while callers still hold them
+  return cache;
 }
 
 }  // namespace bf

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 
 #include "midbf/butterfly.hpp"
 #include "midbf_b200.h"
@@ -29,6 +30,8 @@ struct DevicePlanCache {
   unsigned directions = 0;
   ~DevicePlanCache();
 };
-midbf_plan_t device_plan(const Factorization& F, unsigned directions);
+// Returns the cache entry (not just the handle) so that a concurrent caller
+// rebuilding the cache with more directions cannot free a plan still in use.
+std::shared_ptr<DevicePlanCache> device_plan(const Factorization& F, unsigned directions);
 
 }  // namespace midbf::bf

@@ -271,3 +271,35 @@ def test_concurrent_applies_on_one_plan(gpu, route):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+def test_factorization_applies_from_threads(gpu):
+    """bf::apply / apply_transpose on ONE factorization from several threads
+    (the cached plan is built once, with a direction added concurrently)."""
+    import threading
+
+    X = O.grid2d(32)
+    K = M.Kernel(M.KIND_FIO2D, X=X, Omega=X)
+    F = M.idbf_factorize(K, 64, k=30, eps=1e-9)
+    path = saved(F)
+    Fo = O.load(path)
+    os.unlink(path)
+    f, g = cvec(1024, 31), cvec(1024, 32)
+    want_f, want_t = Fo.apply(f), Fo.apply_transpose(g)
+    errors = []
+
+    def worker(i):
+        try:
+            for _ in range(10):
+                got = F.apply_transpose(g) if i % 2 else F.apply(f)
+                if rel(got, want_t if i % 2 else want_f) > TOL:
+                    errors.append(i)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
