@@ -894,10 +894,25 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+namespace {
+// Makes the plan's device current for a call and restores the caller's.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
 void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> lock(mu);
   if (nrhs < 1) throw std::invalid_argument("nrhs must be >= 1");
-  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  const DeviceScope on_device(device);
   const int d = transpose ? 1 : 0;
   const int64_t nin = transpose ? nrows : ncols, nout = transpose ? ncols : nrows;
   const bool din = is_device_ptr(f), dout = is_device_ptr(g);
@@ -937,7 +952,7 @@ void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaS
 void Plan::apply_async(const double* f, double* g, int64_t nrhs, bool transpose, cudaStream_t user) {
   std::lock_guard<std::recursive_mutex> lock(mu);
   if (nrhs < 1) throw std::invalid_argument("nrhs must be >= 1");
-  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  const DeviceScope on_device(device);
   const int d = transpose ? 1 : 0;
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
   const int64_t nin = transpose ? nrows : ncols, nout = transpose ? ncols : nrows;
