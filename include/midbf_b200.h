@@ -207,6 +207,11 @@ int midbf_fact_id_stats(midbf_fact_t fact, int64_t* out);
  * (application order); flags bit0 = programmatic dependent launch,
  * bit1 = L2 bulk prefetch of the next stage's payload, bit2 = CUDA graphs. */
 int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap);
+/* Panel bytes the single-RHS dataflow kernel streams per stage, out[s]
+ * (application order): the factors' exact identity parts (unit rows / unit
+ * columns of the ID blocks) are gathered from x instead of streamed, unless
+ * flag bit 9 (dense panels) is set. */
+int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap);
 int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags);
 
 /* Seeded inputs of the reference experiment (src/experiment.cpp:75-81). */

@@ -248,15 +248,18 @@ class DevicePlan:
                 pass
             self._h = None
 
-    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3):
+    def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3,
+                  compress=True):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
         64-RHS slice (dmma_flow) or one launch per stage.  variant: k1_flow
         layout 0 (4 warp pairs x 3 x 16 KB), 1 (8 x 2 x 8 KB), 2 (6 x 4 x
-        8 KB), 3 chosen by the plan's size (default)."""
+        8 KB), 3 chosen by the plan's size (default).  compress: k1_flow
+        streams the identity-compressed panels (unit rows / columns of the ID
+        blocks gathered from x instead)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
-        f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4)
+        f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         _check(lib().midbf_plan_set_flags(self._h, f))
 
     def launches(self, nrhs=1, transpose=False):
@@ -269,6 +272,13 @@ class DevicePlan:
         out = np.zeros((64, 4), dtype=np.int64)
         _check(lib().midbf_plan_stages(self._h, 1 if transpose else 0, _ip(out), i64(64)))
         return [tuple(int(v) for v in r) for r in out if r[2] or r[3]]
+
+    def flow_bytes(self, transpose=False):
+        """Panel bytes k1_flow streams per stage (application order)."""
+        n = len(self.stages(transpose))
+        out = np.zeros(max(n, 1), dtype=np.int64)
+        _check(lib().midbf_plan_flow_bytes(self._h, 1 if transpose else 0, _ip(out), i64(n)))
+        return [int(v) for v in out[:n]]
 
     def apply_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
         """Raw-pointer apply (device or host pointers, cudaStream_t as int)."""

@@ -72,10 +72,40 @@ struct FlowParams {
   StageIO st[kMaxStages];
 };
 
-struct StripCtx {
-  Strip s;
-  Seg g[kMaxSeg];
+// A panel as k1_flow streams it.
+struct FlowSeg {
+  int64_t off;     // complex offset in the arena (dense part, or compressed part)
+  int32_t x0;      // first input entry of the block's column range
+  int32_t n;       // columns streamed (the kept columns of a compressed panel)
+  uint32_t urows;  // bit r: row r is a unit row of this panel (no panel row)
+  uint32_t adds;   // bit r: row r adds one staged x entry for this panel
+  int32_t hc;      // rows streamed: the strip's rows minus this panel's unit rows
+  int32_t aoff;    // this panel's first entry in StripCtx::addpos
 };
+
+// Identity compression (plan.cu, build_flow_records).  The factors' ID blocks
+// hold exact identity parts (src/linalg.cpp:278-290 writes MatXc::Identity
+// into every column ID; a row ID is its transpose), so within one panel
+//   a unit row    (its only nonzero is an exact 1 at column c) contributes
+//                 y_r += x[c] and is not streamed;
+//   a unit column (over the remaining rows, a single exact 1 at row r)
+//                 contributes y_r += x[c] and is not streamed;
+//   a zero column (over the remaining rows) is dropped.
+// A compressed strip streams hc x n' per panel; its staged x window holds the
+// kept columns (cmap) followed by `next` extra entries (xext) that only the
+// adds read; each add is a staged position (addpos), summed after the panels.
+struct StripCtx {
+  Strip s;              // s.h rows, s.xcols staged x entries, s.seg0 = strip id
+  FlowSeg g[kMaxSeg];
+  int32_t nkept;        // staged kept columns (sum of g[j].n)
+  int32_t next;         // extra staged entries after them
+  int32_t mapped;       // 1: compressed record (cmap / xext / adds valid)
+  int32_t pad_;
+  uint8_t cmap[kXWin];  // kept column (within its block) of staged entry kk
+  uint16_t xext[32];    // extra staged entry e: segment << 8 | column
+  uint8_t addpos[64];   // per panel, per add row (row order): staged position
+};
+static_assert(sizeof(StripCtx) % 16 == 0, "StripCtx is copied with cp.async.bulk");
 
 namespace flowdev {
 
@@ -225,14 +255,25 @@ __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, con
 #pragma unroll
   for (int i = 0; i < kPer; ++i) idx[i] = -1;
   int cb = 0;
+  const bool mapped = c.mapped != 0;
   for (int j = 0; j < c.s.nseg; ++j) {
     const int n = c.g[j].n, x0 = c.g[j].x0;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int kk = sl + NS * i - cb;
-      if (kk >= 0 && kk < n) idx[i] = x0 + kk;
+      if (kk >= 0 && kk < n) idx[i] = x0 + (mapped ? static_cast<int>(c.cmap[sl + NS * i]) : kk);
     }
     cb += n;
+  }
+  if (mapped) {  // extra entries: x of unit columns / dropped columns read by adds
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = sl + NS * i - cb;
+      if (e >= 0 && e < c.next) {
+        const unsigned t = c.xext[e];
+        idx[i] = c.g[t >> 8].x0 + static_cast<int>(t & 0xffu);
+      }
+    }
   }
   double2 v[kPer];
 #pragma unroll
@@ -299,6 +340,7 @@ struct FlowCfg {
   // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2]
   static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 4) * 8;
   static constexpr size_t kSmem = kSlotArea + kXArea + kCtxArea + kBarArea;
+  static_assert(kSmem <= 232448, "k1_flow exceeds the 227 KB dynamic shared memory of a CTA");
 };
 
 // Warps [0, FW) consume, warps [FW, 2*FW) produce: producer warp FW+c feeds
@@ -434,10 +476,10 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         const int sc = k % kQN;
         FLOW_T(0, mbar_wait(&cfull[sc], (k / kQN) & 1));
         const StripCtx& C = ctx[sc];
-        const int nseg = C.s.nseg, h = C.s.h;
-        const int cpc = chunk_cols_for(h, SLOT);
+        const int nseg = C.s.nseg;
         for (int j = 0; j < nseg; ++j) {
-          const int n = C.g[j].n;
+          const int n = C.g[j].n, h = C.g[j].hc;  // panel rows streamed
+          const int cpc = chunk_cols_for(h, SLOT);
           const double2* src = P.arena + C.g[j].off;
           for (int col = 0; col < n; col += cpc, ++q) {
             const int ncol = min(cpc, n - col);
@@ -468,9 +510,8 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (C.s.y0 < 0) break;
       if (P.nodeps == 2) {  // timing experiment: stream the payload only
         mbar_wait(&xfull[k & 1], (k >> 1) & 1);
-        const int cpc = chunk_cols_for(C.s.h, SLOT);
         for (int j = 0; j < C.s.nseg; ++j)
-          for (int col0 = 0; col0 < C.g[j].n; col0 += cpc, ++q) {
+          for (int col0 = 0, cpc = chunk_cols_for(C.g[j].hc, SLOT); col0 < C.g[j].n; col0 += cpc, ++q) {
             mbar_wait(&full[q % FS], (q / FS) & 1);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q % FS]);
@@ -496,14 +537,19 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       const int row = halves ? (lane & 15) : lane;
       const int cpar = halves ? (lane >> 4) : 0;
       const int cstep = halves ? 2 : 1;
-      const bool live = row < h;
-      const int cpc = chunk_cols_for(h, SLOT);
+      const unsigned below = (1u << row) - 1u;  // rows before this lane's
       int yidx = y0 + row;  // output permutation looked up now, used after the compute
-      if (io.yperm && live && cpar == 0) yidx = io.yperm[yidx];
+      if (io.yperm && row < h && cpar == 0) yidx = io.yperm[yidx];
       double ar0 = 0, ai0 = 0, ar1 = 0, ai1 = 0, ar2 = 0, ai2 = 0, ar3 = 0, ai3 = 0;
       int cb = 0;
       for (int j = 0; j < nseg; ++j) {
         const int n = C.g[j].n;
+        // compressed panels: hc rows (this panel's non-unit rows, in order)
+        const int hc = C.g[j].hc;
+        const unsigned urows = C.g[j].urows;
+        const bool live = row < h && !((urows >> row) & 1u);
+        const int prow = __popc(~urows & below);  // row within the streamed panel
+        const int cpc = chunk_cols_for(hc, SLOT);
         int win = -1;
         for (int col0 = 0; col0 < n; col0 += cpc, ++q) {
           const int ncol = min(cpc, n - col0);
@@ -533,7 +579,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
               double2 m[8], xr[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                m[i] = M[(cc + i * cstep) * h + row];
+                m[i] = M[(cc + i * cstep) * hc + prow];
                 xr[i] = xv[cc + i * cstep];
               }
               cmac(ar0, ai0, m[0], xr[0]);
@@ -546,18 +592,18 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
               cmac(ar3, ai3, m[7], xr[7]);
             }
             if (cc + 3 * cstep < ncol) {  // remainder spread over the 4 chains
-              cmac(ar0, ai0, M[cc * h + row], xv[cc]);
-              cmac(ar1, ai1, M[(cc + cstep) * h + row], xv[cc + cstep]);
-              cmac(ar2, ai2, M[(cc + 2 * cstep) * h + row], xv[cc + 2 * cstep]);
-              cmac(ar3, ai3, M[(cc + 3 * cstep) * h + row], xv[cc + 3 * cstep]);
+              cmac(ar0, ai0, M[cc * hc + prow], xv[cc]);
+              cmac(ar1, ai1, M[(cc + cstep) * hc + prow], xv[cc + cstep]);
+              cmac(ar2, ai2, M[(cc + 2 * cstep) * hc + prow], xv[cc + 2 * cstep]);
+              cmac(ar3, ai3, M[(cc + 3 * cstep) * hc + prow], xv[cc + 3 * cstep]);
               cc += 4 * cstep;
             }
             if (cc + cstep < ncol) {
-              cmac(ar0, ai0, M[cc * h + row], xv[cc]);
-              cmac(ar1, ai1, M[(cc + cstep) * h + row], xv[cc + cstep]);
+              cmac(ar0, ai0, M[cc * hc + prow], xv[cc]);
+              cmac(ar1, ai1, M[(cc + cstep) * hc + prow], xv[cc + cstep]);
               cc += 2 * cstep;
             }
-            if (cc < ncol) cmac(ar2, ai2, M[cc * h + row], xv[cc]);
+            if (cc < ncol) cmac(ar2, ai2, M[cc * hc + prow], xv[cc]);
           }
           if (PROF) tm[9] += clock64() - tc0;
           __syncwarp();
@@ -570,9 +616,19 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
+      if (C.mapped && row < h) {  // identity parts: one staged entry per (panel, add row)
+        for (int j = 0; j < nseg; ++j) {
+          const unsigned a = C.g[j].adds;
+          if ((a >> row) & 1u) {
+            const double2 t = xcur[C.addpos[C.g[j].aoff + __popc(a & below)]];
+            yr += t.x;
+            yi += t.y;
+          }
+        }
+      }
       // The stored value is the readiness signal of this row: never let a
       // result alias the "not yet written" sentinel.
-      FLOW_T(7, if (live && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
+      FLOW_T(7, if (row < h && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&xempty[k & 1]);  // x buffer free for strip k + 2

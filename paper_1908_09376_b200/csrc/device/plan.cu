@@ -213,6 +213,75 @@ __global__ void __launch_bounds__(256) k0_repack(const PanelJob* __restrict__ jo
     }
 }
 
+// K0 identity detection, one warp per strip (k1_flow-eligible strips only),
+// panel by panel: urow[seg*32 + r] = the column of row r's single nonzero in
+// this panel when it is an exact 1 (a unit row), else -1; cinfo[column] over
+// the panel's other rows = -2 (all zero), r >= 0 (a single exact 1 at row r,
+// the first such column of row r in this panel), else -1 (kept).  Exact
+// comparisons: the ID's identity parts are exact ones and zeros (reference
+// src/linalg.cpp:278-290).
+__global__ void __launch_bounds__(256) k0_units(const Strip* __restrict__ strips, int64_t nstrips,
+                                                const Seg* __restrict__ segs, const double2* __restrict__ arena,
+                                                int* __restrict__ urow, int8_t* __restrict__ cinfo) {
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nstrips) return;
+  const Strip st = strips[t];
+  if (st.xcols > kXWin || st.nseg > kMaxSeg) return;
+  const int h = st.h;
+  const bool in = lane < h;
+  for (int j = 0; j < st.nseg; ++j) {
+    const Seg g = segs[st.seg0 + j];
+    int cnt = 0, one = -1;
+    if (in)
+      for (int c = 0; c < g.n; ++c) {
+        const double2 v = arena[g.off + static_cast<int64_t>(c) * h + lane];
+        if (v.x != 0.0 || v.y != 0.0) {
+          ++cnt;
+          if (v.x == 1.0 && v.y == 0.0) one = c;
+        }
+      }
+    const bool unit = in && cnt == 1 && one >= 0;
+    urow[static_cast<int64_t>(st.seg0 + j) * 32 + lane] = unit ? one : -1;
+    unsigned used = 0;  // rows that already have a unit column in this panel
+    for (int c = 0; c < g.n; ++c) {
+      double2 v = make_double2(0.0, 0.0);
+      if (in && !unit) v = arena[g.off + static_cast<int64_t>(c) * h + lane];
+      const unsigned nz = __ballot_sync(0xffffffffu, v.x != 0.0 || v.y != 0.0);
+      const unsigned ones = __ballot_sync(0xffffffffu, v.x == 1.0 && v.y == 0.0);
+      int8_t info = -1;
+      if (nz == 0) {
+        info = -2;
+      } else if (__popc(nz) == 1 && ones == nz && !(used & nz)) {
+        info = static_cast<int8_t>(__ffs(nz) - 1);
+        used |= nz;
+      }
+      if (lane == 0) cinfo[g.pad_[0] + c] = info;
+    }
+  }
+}
+
+// One compressed panel: the kept columns (kcols) of the non-unit rows.
+struct PackJob {
+  int64_t src, dst;  // dense / compressed arena offsets (complex)
+  int32_t h, hc;
+  int32_t nkept, k0;  // kept columns kcols[k0, k0 + nkept)
+  uint32_t urows;
+  int32_t pad_;
+};
+
+__global__ void __launch_bounds__(256) k0_pack(const PackJob* __restrict__ jobs, int64_t njobs,
+                                               const uint8_t* __restrict__ kcols, double2* __restrict__ arena) {
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= njobs) return;
+  const PackJob J = jobs[j];
+  if (lane >= J.h || ((J.urows >> lane) & 1u)) return;
+  const int prow = __popc(~J.urows & ((1u << lane) - 1u));
+  for (int q = 0; q < J.nkept; ++q)
+    arena[J.dst + static_cast<int64_t>(q) * J.hc + prow] = arena[J.src + static_cast<int64_t>(kcols[J.k0 + q]) * J.h + lane];
+}
+
 // Every block's payload, factor by factor, packed back to back on the device
 // (chunks of whole blocks copied in parallel into pinned memory while the
 // previous chunk uploads).  offs[f][b] = complex offset of block b of factor f.
@@ -279,6 +348,212 @@ double2* upload_raw(const PlanTables& T, std::vector<std::vector<int64_t>>& offs
   return d_raw;
 }
 
+// k1_flow strip records: one self-contained StripCtx per strip, dealt in
+// stage order and, within a stage, by the last previous-stage strip read
+// (any order inside a stage keeps the deadlock-freedom argument: every
+// dependency lies in an earlier stage).  Two sets: dense (the panels as
+// stored) and identity-compressed (flow.cuh, StripCtx); the compressed panels
+// are appended to the arena behind the dense ones.
+void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, const std::vector<Seg>& segs) {
+  const size_t ns = strips.size();
+  std::vector<size_t> order(ns);
+  for (size_t t = 0; t < ns; ++t) order[t] = t;
+  // (measured within noise of the natural order: cfg1 64.1 vs 64.2 us,
+  // cfg2 270.7 vs 272.0 us)
+  auto maxdep = [&](size_t t) {
+    int32_t m = 0;
+    for (int j = 0; j < strips[t].nseg; ++j) m = std::max(m, segs[static_cast<size_t>(strips[t].seg0 + j)].dep1);
+    return m;
+  };
+  for (const Stage& stg : D.stages) {
+    auto b = order.begin() + stg.strip0, e = b + stg.nstrips;
+    std::stable_sort(b, e, [&](size_t x, size_t y) { return maxdep(x) < maxdep(y); });
+  }
+  std::vector<StripCtx> dense(ns);
+  for (size_t t = 0; t < ns; ++t) {
+    StripCtx& c = dense[t];
+    std::memset(static_cast<void*>(&c), 0, sizeof(c));
+    const Strip& st = strips[order[t]];
+    c.s = st;
+    c.s.seg0 = static_cast<int32_t>(order[t]);
+    for (int j = 0; j < st.nseg; ++j) {
+      const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+      c.g[j] = FlowSeg{g.off, g.x0, g.n, 0u, 0u, st.h, 0};
+    }
+  }
+  auto up = [](void** dptr, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaMalloc(dptr, std::max<size_t>(bytes, 16)), what);
+    if (bytes) cuda_check(cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice), what);
+  };
+  up(&D.d_ctx, dense.data(), ns * sizeof(StripCtx), "upload strip records");
+  for (Stage& stg : D.stages) stg.flow_bytes = stg.payload_bytes;
+  D.farena_elems = 0;
+  if (ns == 0 || D.ncols_total > INT32_MAX) return;
+
+  // identity detection on the dense panels
+  const size_t nsg = segs.size();
+  int* d_urow = nullptr;
+  int8_t* d_cinfo = nullptr;
+  cuda_check(cudaMalloc(&d_urow, std::max<size_t>(nsg, 1) * 32 * sizeof(int)), "cudaMalloc unit rows");
+  cuda_check(cudaMalloc(&d_cinfo, std::max<int64_t>(D.ncols_total, 1)), "cudaMalloc unit columns");
+  std::vector<int> urow(nsg * 32);
+  std::vector<int8_t> cinfo(static_cast<size_t>(D.ncols_total));
+  cudaError_t err = cudaMemset(d_cinfo, -1, std::max<int64_t>(D.ncols_total, 1));
+  if (err == cudaSuccess) err = cudaMemset(d_urow, 0xff, std::max<size_t>(nsg, 1) * 32 * sizeof(int));
+  if (err == cudaSuccess) {
+    k0_units<<<static_cast<unsigned>((ns * 32 + 255) / 256), 256>>>(D.d_strips, static_cast<int64_t>(ns), D.d_segs,
+                                                                     D.d_arena, d_urow, d_cinfo);
+    err = cudaGetLastError();
+  }
+  if (err == cudaSuccess && nsg) err = cudaMemcpy(urow.data(), d_urow, nsg * 32 * sizeof(int), cudaMemcpyDeviceToHost);
+  if (err == cudaSuccess && D.ncols_total)
+    err = cudaMemcpy(cinfo.data(), d_cinfo, static_cast<size_t>(D.ncols_total), cudaMemcpyDeviceToHost);
+  cudaFree(d_urow);
+  cudaFree(d_cinfo);
+  cuda_check(err, "k0_units");
+
+  // compressed records (same deal order), panels appended behind the dense arena
+  std::vector<StripCtx> comp(dense);
+  std::vector<PackJob> jobs;
+  std::vector<uint8_t> kcols;
+  int64_t at = D.arena_elems;  // next compressed panel (complex offset)
+  auto align = [](int64_t v) { return (v + 7) & ~int64_t(7); };
+  for (Stage& stg : D.stages) stg.flow_bytes = 0;
+  std::vector<int> kpos;  // staged position of each dense column of the strip (-1: dropped)
+  for (size_t t = 0; t < ns; ++t) {
+    const size_t o = order[t];
+    const Strip& st = strips[o];
+    const int h = st.h;
+    Stage& stg = D.stages[static_cast<size_t>(st.stage)];
+    const int64_t dense_elems = static_cast<int64_t>(h) * st.xcols;
+    if (st.xcols > kXWin || st.nseg > kMaxSeg) {
+      stg.flow_bytes += 16 * dense_elems;
+      continue;
+    }
+    StripCtx c = dense[t];
+    kpos.assign(static_cast<size_t>(st.xcols), -1);
+    // kept columns, panel by panel
+    int nkept = 0, cb = 0;
+    for (int j = 0; j < st.nseg; ++j) {
+      const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+      int nk = 0;
+      for (int q = 0; q < g.n; ++q)
+        if (cinfo[static_cast<size_t>(g.pad_[0] + q)] == -1) {
+          kpos[static_cast<size_t>(cb + q)] = nkept;
+          c.cmap[nkept++] = static_cast<uint8_t>(q);
+          ++nk;
+        }
+      c.g[j].n = nk;
+      cb += g.n;
+    }
+    // adds: unit rows (reuse the kept column's staged entry when there is one)
+    // and unit columns (an extra staged entry)
+    std::vector<uint16_t> ext;
+    std::vector<uint8_t> addpos;
+    bool ok = true;
+    int64_t comp_elems = 0;
+    cb = 0;
+    auto extra = [&](int j, int q) {
+      const uint16_t key = static_cast<uint16_t>(j << 8 | q);
+      for (size_t e = 0; e < ext.size(); ++e)
+        if (ext[e] == key) return static_cast<int>(e);
+      ext.push_back(key);
+      return static_cast<int>(ext.size()) - 1;
+    };
+    std::vector<std::pair<int, int>> rowadd;  // (row, staged position)
+    for (int j = 0; j < st.nseg && ok; ++j) {
+      const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+      uint32_t um = 0;
+      int ucol[32];
+      for (int r = 0; r < 32; ++r) ucol[r] = -1;
+      for (int q = 0; q < g.n; ++q) {
+        const int8_t ci = cinfo[static_cast<size_t>(g.pad_[0] + q)];
+        if (ci >= 0) ucol[ci] = q;
+      }
+      rowadd.clear();
+      for (int r = 0; r < h; ++r) {
+        const int q = urow[static_cast<size_t>(st.seg0 + j) * 32 + static_cast<size_t>(r)];
+        if (q >= 0) {
+          um |= 1u << r;
+          const int kp = kpos[static_cast<size_t>(cb + q)];
+          rowadd.push_back({r, kp >= 0 ? kp : nkept + extra(j, q)});
+        } else if (ucol[r] >= 0) {
+          rowadd.push_back({r, nkept + extra(j, ucol[r])});
+        }
+      }
+      const int hc = h - __builtin_popcount(um);
+      c.g[j].hc = hc;
+      c.g[j].urows = um;
+      c.g[j].adds = 0;
+      c.g[j].aoff = static_cast<int32_t>(addpos.size());
+      for (const auto& ra : rowadd) {
+        c.g[j].adds |= 1u << ra.first;
+        addpos.push_back(static_cast<uint8_t>(std::min(ra.second, 255)));
+      }
+      comp_elems += static_cast<int64_t>(hc) * c.g[j].n;
+      cb += g.n;
+      ok = addpos.size() <= 64 && ext.size() <= 32;
+    }
+    ok = ok && nkept + static_cast<int>(ext.size()) <= kXWin && comp_elems < dense_elems;
+    if (!ok) {  // stays dense
+      stg.flow_bytes += 16 * dense_elems;
+      continue;
+    }
+    c.nkept = nkept;
+    c.next = static_cast<int32_t>(ext.size());
+    c.mapped = 1;
+    c.s.xcols = nkept + c.next;
+    for (size_t e = 0; e < ext.size(); ++e) c.xext[e] = ext[e];
+    for (size_t e = 0; e < addpos.size(); ++e) c.addpos[e] = addpos[e];
+    // compressed panels
+    size_t k0 = 0;
+    for (int j = 0; j < st.nseg; ++j) {
+      const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+      const int nk = c.g[j].n, hc = c.g[j].hc;
+      at = align(at);
+      c.g[j].off = at;
+      if (hc > 0 && nk > 0) {
+        jobs.push_back({g.off, at, h, hc, nk, static_cast<int32_t>(kcols.size()), c.g[j].urows, 0});
+        for (int q = 0; q < nk; ++q) kcols.push_back(c.cmap[k0 + static_cast<size_t>(q)]);
+        at += static_cast<int64_t>(hc) * nk;
+      }
+      k0 += static_cast<size_t>(nk);  // (hc == 0: every column is dropped, nk == 0)
+    }
+    comp[t] = c;
+    stg.flow_bytes += 16 * comp_elems;
+  }
+  D.farena_elems = at - D.arena_elems;
+  if (jobs.empty()) {  // nothing to compress: the dense records serve both
+    D.d_fctx = nullptr;
+    return;
+  }
+  // arena = [dense panels | compressed panels]
+  double2* arena = nullptr;
+  cuda_check(cudaMalloc(&arena, std::max<int64_t>(at, 1) * sizeof(double2)), "cudaMalloc flow arena");
+  PackJob* d_jobs = nullptr;
+  uint8_t* d_kcols = nullptr;
+  err = cudaMemcpy(arena, D.d_arena, D.arena_elems * sizeof(double2), cudaMemcpyDeviceToDevice);
+  if (err == cudaSuccess) err = cudaMalloc(&d_jobs, jobs.size() * sizeof(PackJob));
+  if (err == cudaSuccess) err = cudaMalloc(&d_kcols, std::max<size_t>(kcols.size(), 1));
+  if (err == cudaSuccess) err = cudaMemcpy(d_jobs, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMemcpy(d_kcols, kcols.data(), kcols.size(), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) {
+    const int64_t nj = static_cast<int64_t>(jobs.size());
+    k0_pack<<<static_cast<unsigned>((nj * 32 + 255) / 256), 256>>>(d_jobs, nj, d_kcols, arena);
+    err = cudaGetLastError();
+  }
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  cudaFree(d_jobs);
+  cudaFree(d_kcols);
+  if (err != cudaSuccess) {
+    cudaFree(arena);
+    cuda_check(err, "k0_pack");
+  }
+  cudaFree(D.d_arena);
+  D.d_arena = arena;
+  up(&D.d_fctx, comp.data(), ns * sizeof(StripCtx), "upload compressed strip records");
+}
+
 // Build one direction (forward or transpose) of the plan on the host and
 // upload it.  Strip construction is general (ragged, overlapping and
 // uncovered rows): breakpoints at every block edge, active blocks in the
@@ -290,6 +565,7 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
   const int64_t nf = T.nfactors;
   if (nf > kMaxStages) throw std::invalid_argument("too many factors for one device plan");
   D.stages.clear();
+  D.ncols_total = 0;
   std::vector<Strip> strips;
   std::vector<Seg> segs;
   std::vector<PanelJob> jobs;
@@ -392,6 +668,8 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
           sg.off = arena_len;
           sg.x0 = static_cast<int32_t>(e.xoff);
           sg.n = static_cast<int32_t>(e.n);
+          sg.pad_[0] = static_cast<int32_t>(std::min<int64_t>(D.ncols_total, INT32_MAX));  // column base (k0_units)
+          D.ncols_total += e.n;
           deps(e.xoff, e.n, sg.dep0, sg.dep1);
           jobs.push_back({arena_len, e.raw, h, static_cast<int32_t>(e.n), static_cast<int32_t>(e.ld),
                           static_cast<int32_t>(y - e.yoff), e.tr ? 1 : 0, 0});
@@ -433,34 +711,7 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
     cudaFree(d_jobs);
     cuda_check(e2, "k0_repack");
   }
-  if (D.max_seg <= kMaxSeg) {  // one self-contained metadata record per strip for k1_flow
-    // Deal order within each stage: by the last previous-stage strip the
-    // strip reads from (any order inside a stage keeps the deadlock-freedom
-    // argument: every dependency lies in an earlier stage).
-    std::vector<size_t> order(strips.size());
-    for (size_t t = 0; t < strips.size(); ++t) order[t] = t;
-    // (measured within noise of the natural order: cfg1 64.1 vs 64.2 us,
-    // cfg2 270.7 vs 272.0 us)
-    auto maxdep = [&](size_t t) {
-      int32_t m = 0;
-      for (int j = 0; j < strips[t].nseg; ++j) m = std::max(m, segs[static_cast<size_t>(strips[t].seg0 + j)].dep1);
-      return m;
-    };
-    for (const Stage& stg : D.stages) {
-      auto b = order.begin() + stg.strip0, e = b + stg.nstrips;
-      std::stable_sort(b, e, [&](size_t x, size_t y) { return maxdep(x) < maxdep(y); });
-    }
-    std::vector<StripCtx> ctxs(strips.size());
-    for (size_t t = 0; t < strips.size(); ++t) {
-      const size_t o = order[t];
-      StripCtx& c = ctxs[t];
-      std::memset(static_cast<void*>(&c), 0, sizeof(c));
-      c.s = strips[o];
-      c.s.seg0 = static_cast<int32_t>(o);
-      for (int j = 0; j < strips[o].nseg; ++j) c.g[j] = segs[static_cast<size_t>(strips[o].seg0 + j)];
-    }
-    up(reinterpret_cast<void**>(&D.d_ctx), ctxs.data(), ctxs.size() * sizeof(StripCtx), "upload strip records");
-  }
+  if (D.max_seg <= kMaxSeg) build_flow_records(D, strips, segs);
   // two parity sets, armed with the all-ones sentinel (k1_flow's ready signal)
   cuda_check(cudaMalloc(&D.d_stagebuf, 2 * D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
   cuda_check(cudaMemset(D.d_stagebuf, 0xff, 2 * D.stagebuf_elems * sizeof(double2)), "arm stage buffers");
@@ -524,7 +775,7 @@ Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   if (timing) std::fprintf(stderr, "[plan] raw upload %.1f ms, directions %.1f ms\n", ms(t0, t1), ms(t1, t2));
   flow_grid[0] = flow_setup<4, 3, 16384>(num_sms);
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
-  flow_grid[2] = flow_setup<6, 4, 8192>(num_sms);
+  flow_grid[2] = flow_setup<6, 3, 8192>(num_sms);
   flow_grid[3] = flow_grid[0];  // unused: variant 3 resolves per direction (flow_variant)
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
@@ -544,6 +795,7 @@ Plan::~Plan() {
     cudaFree(D.d_segs);
     cudaFree(D.d_arena);
     cudaFree(D.d_ctx);
+    cudaFree(D.d_fctx);
     cudaFree(D.d_k2buf);
     cudaFree(D.d_k2done);
     cudaFree(D.d_k2epoch);
@@ -584,7 +836,8 @@ int Plan::flow_variant(int d) const {
   const int v = static_cast<int>((flags >> 4) & 3u);
   if (v != 3) return v;
   int64_t bytes = 0;
-  for (const auto& st : dir[d].stages) bytes += st.payload_bytes;
+  const bool dense = !dir[d].d_fctx || (flags & 512u);
+  for (const auto& st : dir[d].stages) bytes += dense ? st.payload_bytes : st.flow_bytes;
   return bytes > (int64_t{512} << 20) ? 1 : 0;
 }
 
@@ -623,7 +876,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   Direction& D = dir[d];
   const int variant = flow_variant(d);
   FlowParams P{};
-  P.ctxs = static_cast<const StripCtx*>(D.d_ctx);
+  // bit 9: dense panels (identity compression off, A/B experiments)
+  P.ctxs = static_cast<const StripCtx*>((D.d_fctx && !(flags & 512u)) ? D.d_fctx : D.d_ctx);
   P.strips = D.d_strips;
   P.segs = D.d_segs;
   P.arena = D.d_arena;
@@ -651,7 +905,7 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
       flow_launch<8, 2, 8192>(P, flow_grid[1], stream);
       break;
     case 2:
-      flow_launch<6, 4, 8192>(P, flow_grid[2], stream);
+      flow_launch<6, 3, 8192>(P, flow_grid[2], stream);
       break;
     default:
       flow_launch<4, 3, 16384>(P, flow_grid[0], stream);

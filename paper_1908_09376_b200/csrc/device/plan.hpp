@@ -56,6 +56,7 @@ struct Stage {
   int32_t strip0 = 0, nstrips = 0;
   int64_t arena0 = 0, payload_bytes = 0;
   int64_t buf_off = 0;  // offset of this stage's output in the stage buffer
+  int64_t flow_bytes = 0;  // panel bytes k1_flow streams (identity-compressed)
 };
 
 struct Direction {
@@ -64,7 +65,10 @@ struct Direction {
   Strip* d_strips = nullptr;
   Seg* d_segs = nullptr;
   double2* d_arena = nullptr;
-  void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh)
+  void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh), dense panels
+  void* d_fctx = nullptr;         // ... identity-compressed panels (null: nothing to compress)
+  int64_t farena_elems = 0;       // compressed panels, stored behind the dense ones in d_arena
+  int64_t ncols_total = 0;        // panel columns over all segments (plan build)
   double2* d_stagebuf = nullptr;  // outputs of every stage but the last, two parity sets
   unsigned* d_sync = nullptr;     // per-CTA apply epochs (kMaxFlowCtas)
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
@@ -116,7 +120,8 @@ class Plan {
   // bit0 PDL + bit1 L2 prefetch (stage kernels), bit2 CUDA graphs,
   // bit3 persistent dataflow kernel for single-RHS applies,
   // bits4-5 k1_flow variant (warps per CTA / ring slots / slot size),
-  // bits6-10 timing experiments (flow.cuh), bit11 disable K2 (DMMA multi-RHS),
+  // bits6-8 timing experiments (flow.cuh), bit9 dense k1_flow panels (identity
+  // compression off), bit11 disable K2 (DMMA multi-RHS),
   // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel,
   // bits14-15 k2_flow timing experiments (k2flow.cuh, results invalid).
   unsigned flags = 0x3F;  // default: k1_flow variant chosen by size (flow_variant), graphs, PDL, prefetch
@@ -136,6 +141,7 @@ class Plan {
  private:
   void build_direction(int d, const PlanTables& T, const double2* d_raw,
                        const std::vector<std::vector<int64_t>>& raw_off);
+  void build_flow_records(Direction& D, const std::vector<Strip>& strips, const std::vector<Seg>& segs);
   void ensure_buffers(int64_t nrhs);
   void launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);

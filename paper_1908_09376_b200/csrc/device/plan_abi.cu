@@ -303,6 +303,21 @@ extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out,
   });
 }
 
+// Panel bytes k1_flow streams per stage (identity-compressed unless flag bit
+// 9 is set): out[s], application order.
+extern "C" int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap) {
+  return guard([&] {
+    const Plan& p = *plan->p;
+    const auto& D = p.dir[transpose ? 1 : 0];
+    const bool dense = !D.d_fctx || (p.flags & 512u);
+    int64_t s = 0;
+    for (const auto& st : D.stages) {
+      if (s >= cap) break;
+      out[s++] = dense ? st.payload_bytes : st.flow_bytes;
+    }
+  });
+}
+
 // Tuning switches (bench / profiling): bit0 PDL, bit1 L2 bulk prefetch
 // (stage kernels), bit2 CUDA graphs, bit3 persistent dataflow kernel.
 extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {

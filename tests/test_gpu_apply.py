@@ -117,6 +117,32 @@ def test_single_rhs_kernel_variants(pair, variant):
         assert plan.launches(1) == 1
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_identity_compression(pair, variant):
+    """k1_flow streams the ID blocks without their exact identity parts
+    (unit rows / unit columns gathered from x, flow.cuh StripCtx): fewer
+    bytes than the stored factor whenever an ID block has any, and the same
+    result as the dense panels and the oracle, both directions."""
+    name, K, Fo, Fm, plan = pair
+    stored = sum(s[1] for s in plan.stages())
+    streamed = sum(plan.flow_bytes())
+    assert 0 < streamed <= stored
+    if Fo.L >= 1:  # factors with ID blocks
+        assert streamed < stored
+    f, g = cvec(Fo.ncols, 24), cvec(Fo.nrows, 25)
+    try:
+        plan.set_flags(variant=variant)
+        a, b = plan.apply(f), plan.apply(g, transpose=True)
+        plan.set_flags(variant=variant, compress=False)
+        assert sum(plan.flow_bytes()) == stored
+        a0, b0 = plan.apply(f), plan.apply(g, transpose=True)
+    finally:
+        plan.set_flags()
+    assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14
+    assert rel(a, Fo.apply(f)) <= TOL
+    assert rel(b, Fo.apply_transpose(g)) <= TOL
+
+
 def test_multi_rhs_runs_are_bitwise_identical(pair):
     """k2_flow: fixed-order DMMA accumulation, no atomics on values."""
     name, K, Fo, Fm, plan = pair
