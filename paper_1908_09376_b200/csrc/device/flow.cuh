@@ -41,6 +41,10 @@ namespace midbf::dev {
 constexpr int kMaxSeg = 8;  // panels per strip supported by k1_flow
 constexpr int kQN = 4;      // claimed-strip context ring per warp
 constexpr int kXWin = 128;  // staged x entries per buffer (two per warp)
+// PROF builds: per-warp phase timers in the first kProfStripBase entries of
+// FlowParams::prof, then 3 timestamps per strip (up to kProfStrips strips)
+constexpr int64_t kProfStripBase = int64_t(1024) * 64 * 16;
+constexpr int kProfStrips = 1 << 18;
 
 struct StageIO {
   const double2* x;  // parity-0 address for stage buffers
@@ -529,7 +533,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       double2* yout = io.y + (io.y_par ? par_off : 0);
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + (k & 1) * kXWin;
+      const unsigned long long g_ctx = PROF ? globaltimer_ns() : 0;
       FLOW_T(4, mbar_wait(&xfull[k & 1], (k >> 1) & 1));  // staged by the producer warp's lanes 1..31
+      const unsigned long long g_x = PROF ? globaltimer_ns() : 0;
       // Lane mapping: strips of <= 16 rows use both half-warps (row = lane&15,
       // column parity = lane>>4, combined by one shuffle at the end), wider
       // strips one lane per row.
@@ -629,6 +635,12 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       // The stored value is the readiness signal of this row: never let a
       // result alias the "not yet written" sentinel.
       FLOW_T(7, if (row < h && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
+      if (PROF && lane == 0 && C.s.seg0 < kProfStrips) {  // per-strip timeline (ns): ctx ready, x staged, stored
+        long long* ts = P.prof + kProfStripBase + 3 * static_cast<int64_t>(C.s.seg0);
+        ts[0] = static_cast<long long>(g_ctx);
+        ts[1] = static_cast<long long>(g_x);
+        ts[2] = static_cast<long long>(globaltimer_ns());
+      }
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&xempty[k & 1]);  // x buffer free for strip k + 2

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "flow.cuh"
 #include "plan.hpp"
 #include "pool.hpp"
 
@@ -326,7 +327,9 @@ extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
     Plan& p = *plan->p;
     p.flags = flags;
     if ((flags & 4096u) && !p.d_prof)  // phase-timer buffer, allocated outside any capture
-      midbf::dev::cuda_check(cudaMalloc(&p.d_prof, size_t(1024) * 64 * 16 * sizeof(long long)), "prof buffer");
+      midbf::dev::cuda_check(
+          cudaMalloc(&p.d_prof, (midbf::dev::kProfStripBase + 3 * size_t(midbf::dev::kProfStrips)) * sizeof(long long)),
+          "prof buffer");
   });
 }
 
@@ -342,7 +345,9 @@ extern "C" int midbf_plan_flow_profile(midbf_plan_t plan, int64_t* out, int64_t 
     Plan& p = *plan->p;
     if (!p.d_prof) throw std::logic_error("no profiled k1_flow launch");
     midbf::dev::cuda_check(cudaDeviceSynchronize(), "sync");
-    const size_t bytes = std::min<size_t>(static_cast<size_t>(n), size_t(1024) * 64 * 16) * sizeof(long long);
+    const size_t bytes =
+        std::min<size_t>(static_cast<size_t>(n), midbf::dev::kProfStripBase + 3 * size_t(midbf::dev::kProfStrips)) *
+        sizeof(long long);
     midbf::dev::cuda_check(cudaMemcpy(out, p.d_prof, bytes, cudaMemcpyDeviceToHost), "prof D2H");
   });
 }
