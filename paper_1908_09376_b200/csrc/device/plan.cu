@@ -420,6 +420,7 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
   auto align = [](int64_t v) { return (v + 7) & ~int64_t(7); };
   for (Stage& stg : D.stages) stg.flow_bytes = 0;
   std::vector<int> kpos;  // staged position of each dense column of the strip (-1: dropped)
+  bool any = false;       // some strip compressed (possibly to no panel at all: permutation blocks)
   for (size_t t = 0; t < ns; ++t) {
     const size_t o = order[t];
     const Strip& st = strips[o];
@@ -520,11 +521,17 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
       k0 += static_cast<size_t>(nk);  // (hc == 0: every column is dropped, nk == 0)
     }
     comp[t] = c;
+    any = true;
     stg.flow_bytes += 16 * comp_elems;
   }
   D.farena_elems = at - D.arena_elems;
-  if (jobs.empty()) {  // nothing to compress: the dense records serve both
+  if (!any) {  // nothing to compress: the dense records serve both
+    for (Stage& stg : D.stages) stg.flow_bytes = stg.payload_bytes;
     D.d_fctx = nullptr;
+    return;
+  }
+  if (jobs.empty()) {  // compressed strips stream no panel at all (permutation blocks)
+    up(&D.d_fctx, comp.data(), ns * sizeof(StripCtx), "upload compressed strip records");
     return;
   }
   // arena = [dense panels | compressed panels]

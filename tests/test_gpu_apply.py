@@ -127,7 +127,7 @@ def test_identity_compression(pair, variant):
     stored = sum(s[1] for s in plan.stages())
     streamed = sum(plan.flow_bytes())
     assert 0 < streamed <= stored
-    if Fo.L >= 1 and name != "fio3d_n8":  # ID blocks in strips of <= 128 staged columns
+    if Fo.L >= 1:  # factors with ID blocks
         assert streamed < stored
     f, g = cvec(Fo.ncols, 24), cvec(Fo.nrows, 25)
     try:
