@@ -73,6 +73,7 @@ struct FlowParams {
   // FMA loop.
   int nodeps;
   long long* prof;  // phase timers of the PROF instantiation
+  const int* wmap;  // wide compressed strips: kept columns, then add columns (StripCtx::wbase)
   StageIO st[kMaxStages];
 };
 
@@ -103,8 +104,9 @@ struct StripCtx {
   FlowSeg g[kMaxSeg];
   int32_t nkept;        // staged kept columns (sum of g[j].n)
   int32_t next;         // extra staged entries after them
-  int32_t mapped;       // 1: compressed record (cmap / xext / adds valid)
-  int32_t pad_;
+  int32_t mapped;       // 1: compressed record (cmap / xext / adds valid); 2: wide compressed
+                        //    strip (kept / add columns in FlowParams::wmap at wbase)
+  int32_t wbase;
   uint8_t cmap[kXWin];  // kept column (within its block) of staged entry kk
   uint16_t xext[32];    // extra staged entry e: segment << 8 | column
   uint8_t addpos[64];   // per panel, per add row (row order): staged position
@@ -203,6 +205,35 @@ __device__ __forceinline__ void gather_range(const double2* x, const int* xperm,
       const int kk = base + lane + 32 * i;
       if (kk < cnt) dst[kk] = v[i];
     }
+  }
+}
+// Wide compressed strips: gather cnt kept columns x[x0 + map[kk]], polling.
+__device__ __forceinline__ void gather_mapped(const double2* x, int x0, const int* map, int cnt, double2* dst,
+                                              int lane) {
+  for (int base = 0; base < cnt; base += 32 * 4) {
+    double2 v[4];
+    int idx[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = base + lane + 32 * i;
+      idx[i] = kk < cnt ? x0 + __ldg(map + kk) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (idx[i] >= 0) v[i] = ld_cg(x + idx[i]);
+    bool ok;
+    do {
+      ok = true;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (idx[i] >= 0 && is_sentinel(v[i])) {
+          v[i] = ld_cg(x + idx[i]);
+          ok = false;
+        }
+    } while (!ok);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (idx[i] >= 0) dst[base + lane + 32 * i] = v[i];
   }
 }
 __device__ __forceinline__ void gather_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst,
@@ -567,7 +598,10 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             if (w0 != win) {
               __syncwarp();
               const int cnt = min(kXWin, n - w0 * kXWin);
-              gather_range(xin, io.xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
+              if (C.mapped == 2)
+                gather_mapped(xin, C.g[j].x0, P.wmap + C.wbase + cb + w0 * kXWin, cnt, xcur, lane);
+              else
+                gather_range(xin, io.xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
               __syncwarp();
               win = w0;
             }
@@ -622,11 +656,22 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
-      if (C.mapped && row < h) {  // identity parts: one staged entry per (panel, add row)
+      if (C.mapped == 1 && row < h) {  // identity parts: one staged entry per (panel, add row)
         for (int j = 0; j < nseg; ++j) {
           const unsigned a = C.g[j].adds;
           if ((a >> row) & 1u) {
             const double2 t = xcur[C.addpos[C.g[j].aoff + __popc(a & below)]];
+            yr += t.x;
+            yi += t.y;
+          }
+        }
+      } else if (C.mapped == 2 && row < h && cpar == 0) {  // wide strips: read (and poll) the entry itself
+        for (int j = 0; j < nseg; ++j) {
+          const unsigned a = C.g[j].adds;
+          if ((a >> row) & 1u) {
+            const int xi = C.g[j].x0 + __ldg(P.wmap + C.wbase + C.nkept + C.g[j].aoff + __popc(a & below));
+            double2 t = ld_cg(xin + xi);
+            while (is_sentinel(t)) t = ld_cg(xin + xi);
             yr += t.x;
             yi += t.y;
           }

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(256) k0_units(const Strip* __restrict__ strips
   const int lane = threadIdx.x & 31;
   if (t >= nstrips) return;
   const Strip st = strips[t];
-  if (st.xcols > kXWin || st.nseg > kMaxSeg) return;
+  if (st.nseg > kMaxSeg) return;
   const int h = st.h;
   const bool in = lane < h;
   for (int j = 0; j < st.nseg; ++j) {
@@ -271,7 +271,7 @@ struct PackJob {
 };
 
 __global__ void __launch_bounds__(256) k0_pack(const PackJob* __restrict__ jobs, int64_t njobs,
-                                               const uint8_t* __restrict__ kcols, double2* __restrict__ arena) {
+                                               const int* __restrict__ kcols, double2* __restrict__ arena) {
   const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= njobs) return;
@@ -415,7 +415,8 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
   // compressed records (same deal order), panels appended behind the dense arena
   std::vector<StripCtx> comp(dense);
   std::vector<PackJob> jobs;
-  std::vector<uint8_t> kcols;
+  std::vector<int> kcols;
+  std::vector<int> wmap;  // wide compressed strips: kept columns, then add columns (per strip at wbase)
   int64_t at = D.arena_elems;  // next compressed panel (complex offset)
   auto align = [](int64_t v) { return (v + 7) & ~int64_t(7); };
   for (Stage& stg : D.stages) stg.flow_bytes = 0;
@@ -427,8 +428,77 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
     const int h = st.h;
     Stage& stg = D.stages[static_cast<size_t>(st.stage)];
     const int64_t dense_elems = static_cast<int64_t>(h) * st.xcols;
-    if (st.xcols > kXWin || st.nseg > kMaxSeg) {
+    if (st.nseg > kMaxSeg) {
       stg.flow_bytes += 16 * dense_elems;
+      continue;
+    }
+    if (st.xcols > kXWin) {  // wide strip: x windows over the kept columns (wmap), adds read from x itself
+      StripCtx c = dense[t];
+      const size_t wb = wmap.size();
+      int nkept = 0;
+      for (int j = 0; j < st.nseg; ++j) {
+        const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+        int nk = 0;
+        for (int q = 0; q < g.n; ++q)
+          if (cinfo[static_cast<size_t>(g.pad_[0] + q)] == -1) {
+            wmap.push_back(q);
+            ++nk;
+          }
+        c.g[j].n = nk;
+        nkept += nk;
+      }
+      std::vector<int> addcols;
+      int64_t comp_elems = 0;
+      for (int j = 0; j < st.nseg; ++j) {
+        const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+        int ucol[32];
+        for (int r = 0; r < 32; ++r) ucol[r] = -1;
+        for (int q = 0; q < g.n; ++q) {
+          const int8_t ci = cinfo[static_cast<size_t>(g.pad_[0] + q)];
+          if (ci >= 0) ucol[ci] = q;
+        }
+        uint32_t um = 0, am = 0;
+        c.g[j].aoff = static_cast<int32_t>(addcols.size());
+        for (int r = 0; r < h; ++r) {
+          const int q = urow[static_cast<size_t>(st.seg0 + j) * 32 + static_cast<size_t>(r)];
+          if (q >= 0) um |= 1u << r;
+          const int col = q >= 0 ? q : ucol[r];
+          if (col >= 0) {
+            am |= 1u << r;
+            addcols.push_back(col);
+          }
+        }
+        c.g[j].hc = h - __builtin_popcount(um);
+        c.g[j].urows = um;
+        c.g[j].adds = am;
+        if (c.g[j].hc == 0) c.g[j].n = 0;  // (every column dropped: no rows left)
+        comp_elems += static_cast<int64_t>(c.g[j].hc) * c.g[j].n;
+      }
+      if (comp_elems >= dense_elems) {  // nothing saved: stays dense
+        wmap.resize(wb);
+        stg.flow_bytes += 16 * dense_elems;
+        continue;
+      }
+      wmap.insert(wmap.end(), addcols.begin(), addcols.end());
+      c.mapped = 2;
+      c.wbase = static_cast<int32_t>(wb);
+      c.nkept = nkept;  // (s.xcols stays > kXWin: the consumer keeps the windowed path)
+      size_t k0 = wb;
+      for (int j = 0; j < st.nseg; ++j) {
+        const Seg& g = segs[static_cast<size_t>(st.seg0 + j)];
+        const int nk = c.g[j].n, hc = c.g[j].hc;
+        at = align(at);
+        c.g[j].off = at;
+        if (hc > 0 && nk > 0) {
+          jobs.push_back({g.off, at, h, hc, nk, static_cast<int32_t>(kcols.size()), c.g[j].urows, 0});
+          kcols.insert(kcols.end(), wmap.begin() + static_cast<int64_t>(k0), wmap.begin() + static_cast<int64_t>(k0) + nk);
+          at += static_cast<int64_t>(hc) * nk;
+        }
+        k0 += static_cast<size_t>(nk);
+      }
+      comp[t] = c;
+      any = true;
+      stg.flow_bytes += 16 * comp_elems;
       continue;
     }
     StripCtx c = dense[t];
@@ -530,6 +600,7 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
     D.d_fctx = nullptr;
     return;
   }
+  if (!wmap.empty()) up(reinterpret_cast<void**>(&D.d_wmap), wmap.data(), wmap.size() * sizeof(int), "upload wide maps");
   if (jobs.empty()) {  // compressed strips stream no panel at all (permutation blocks)
     up(&D.d_fctx, comp.data(), ns * sizeof(StripCtx), "upload compressed strip records");
     return;
@@ -538,12 +609,12 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
   double2* arena = nullptr;
   cuda_check(cudaMalloc(&arena, std::max<int64_t>(at, 1) * sizeof(double2)), "cudaMalloc flow arena");
   PackJob* d_jobs = nullptr;
-  uint8_t* d_kcols = nullptr;
+  int* d_kcols = nullptr;
   err = cudaMemcpy(arena, D.d_arena, D.arena_elems * sizeof(double2), cudaMemcpyDeviceToDevice);
   if (err == cudaSuccess) err = cudaMalloc(&d_jobs, jobs.size() * sizeof(PackJob));
-  if (err == cudaSuccess) err = cudaMalloc(&d_kcols, std::max<size_t>(kcols.size(), 1));
+  if (err == cudaSuccess) err = cudaMalloc(&d_kcols, std::max<size_t>(kcols.size(), 1) * sizeof(int));
   if (err == cudaSuccess) err = cudaMemcpy(d_jobs, jobs.data(), jobs.size() * sizeof(PackJob), cudaMemcpyHostToDevice);
-  if (err == cudaSuccess) err = cudaMemcpy(d_kcols, kcols.data(), kcols.size(), cudaMemcpyHostToDevice);
+  if (err == cudaSuccess) err = cudaMemcpy(d_kcols, kcols.data(), kcols.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (err == cudaSuccess) {
     const int64_t nj = static_cast<int64_t>(jobs.size());
     k0_pack<<<static_cast<unsigned>((nj * 32 + 255) / 256), 256>>>(d_jobs, nj, d_kcols, arena);
@@ -803,6 +874,7 @@ Plan::~Plan() {
     cudaFree(D.d_arena);
     cudaFree(D.d_ctx);
     cudaFree(D.d_fctx);
+    cudaFree(D.d_wmap);
     cudaFree(D.d_k2buf);
     cudaFree(D.d_k2done);
     cudaFree(D.d_k2epoch);
@@ -888,6 +960,7 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.strips = D.d_strips;
   P.segs = D.d_segs;
   P.arena = D.d_arena;
+  P.wmap = D.d_wmap;
   P.epoch = D.d_sync;
   P.stagebuf = D.d_stagebuf;
   P.par_elems = D.stagebuf_elems;

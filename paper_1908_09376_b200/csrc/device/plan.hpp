@@ -67,6 +67,7 @@ struct Direction {
   double2* d_arena = nullptr;
   void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh), dense panels
   void* d_fctx = nullptr;         // ... identity-compressed panels (null: nothing to compress)
+  int* d_wmap = nullptr;          // wide compressed strips: kept / add columns (StripCtx::wbase)
   int64_t farena_elems = 0;       // compressed panels, stored behind the dense ones in d_arena
   int64_t ncols_total = 0;        // panel columns over all segments (plan build)
   double2* d_stagebuf = nullptr;  // outputs of every stage but the last, two parity sets

@@ -9,7 +9,7 @@ import pytest
 
 import oracle as O
 import paper_1908_09376_b200 as M
-from helpers import cases, cvec, oracle_factorization, rel, saved
+from helpers import cases, cvec, integer_grid, oracle_factorization, rel, saved, unit_grid
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
@@ -141,6 +141,39 @@ def test_identity_compression(pair, variant):
     assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14
     assert rel(a, Fo.apply(f)) <= TOL
     assert rel(b, Fo.apply_transpose(g)) <= TOL
+
+
+@pytest.fixture(scope="module")
+def wide3d(gpu):
+    """3D FIO, n = 16 per dim, n0 = k = 64: cfg3's structure at N = 4096 (leaf
+    factors are permutations, V^2 blocks 64 x 512 and U^2 strips of 8 panels x
+    64 columns exceed the 128-entry x window)."""
+    X, Om = unit_grid(16, 3), integer_grid(16, 3)
+    K, Fo = oracle_factorization(O.KIND_FIO3D, X, Om, 64, 64, 1e-9)
+    path = saved(Fo)
+    plan = M.DevicePlan.load(path, directions=3)
+    os.unlink(path)
+    return Fo, plan
+
+
+def test_wide_strip_identity_compression(wide3d):
+    """Strips wider than the x window compress through the windowed path
+    (kept columns through a global map, identity adds read from x itself);
+    permutation factors stream nothing.  Every layout, both directions."""
+    Fo, plan = wide3d
+    stages, fb = plan.stages(), plan.flow_bytes()
+    assert fb[0] == 0 and fb[-1] == 0  # V^1 / U^1 are permutations
+    assert fb[1] < stages[1][1] and fb[3] < stages[3][1]  # the wide ID stages
+    assert fb[2] == stages[2][1]  # S is dense
+    f, g = cvec(Fo.ncols, 31), cvec(Fo.nrows, 32)
+    want_f, want_g = Fo.apply(f), Fo.apply_transpose(g)
+    try:
+        for variant in (0, 1, 2):
+            plan.set_flags(variant=variant)
+            assert rel(plan.apply(f), want_f) <= TOL
+            assert rel(plan.apply(g, transpose=True), want_g) <= TOL
+    finally:
+        plan.set_flags()
 
 
 def test_multi_rhs_runs_are_bitwise_identical(pair):
