@@ -212,6 +212,9 @@ int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out, int64_t ca
  * columns of the ID blocks) are gathered from x instead of streamed, unless
  * flag bit 9 (dense panels) is set. */
 int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap);
+/* Panel bytes (16 per entry) the multi-RHS DMMA kernel multiplies per apply on
+ * 32- / 64-wide tiles: unit / zero columns of V-type ID strips skipped. */
+int midbf_plan_k2_bytes(midbf_plan_t plan, int transpose, int64_t* out);
 int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags);
 
 /* Seeded inputs of the reference experiment (src/experiment.cpp:75-81). */

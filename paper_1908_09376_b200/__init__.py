@@ -280,6 +280,12 @@ class DevicePlan:
         _check(lib().midbf_plan_flow_bytes(self._h, 1 if transpose else 0, _ip(out), i64(n)))
         return [int(v) for v in out[:n]]
 
+    def k2_bytes(self, transpose=False):
+        """Panel bytes the multi-RHS DMMA kernel multiplies per apply (32/64-wide tiles)."""
+        out = i64()
+        _check(lib().midbf_plan_k2_bytes(self._h, 1 if transpose else 0, C.byref(out)))
+        return out.value
+
     def apply_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
         """Raw-pointer apply (device or host pointers, cudaStream_t as int)."""
         _check(lib().midbf_apply(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))

@@ -77,8 +77,11 @@ struct K2FStage {
 };
 
 struct K2FParams {
-  const Strip* strips;  // all stages, application order
+  const Strip* strips;  // all stages, application order; identity-compressed
+                        // strips: pad_[0] = base in xmap, pad_[1] = base in addx
   const Seg* segs;
+  const int* xmap;      // compressed strips: stage-local input row of each kept column
+  const int* addx;      // compressed strips: per output row, the input row added to it (-1: none)
   const double2* arena;
   unsigned* done;   // per strip: completions over all launches
   unsigned* epoch;  // per CTA: launches completed
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
       }
       s_k0 -= s_n;
       const int K = st.xcols, h = st.h;
+      const int xmb = st.pad_[0];  // >= 0: kept columns' input rows in P.xmap (identity-compressed strip)
       const int nq = K > 0 ? (K + kK2Kc - 1) / kK2Kc : 1;
       bool deps = st.stage == 0 || P.mode != 0;
       for (int q = 0; q < nq; ++q, ++gc) {
@@ -178,6 +182,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int kval = min(kK2Kc, K - q * kK2Kc);  // valid columns (<= 0: none)
         const int64_t psrc = __shfl_sync(0xffffffffu, s_off, sidx) + static_cast<int64_t>(cc) * h;
         int xi = __shfl_sync(0xffffffffu, s_x0, sidx) + cc;
+        if (xmb >= 0 && ok) xi = __ldg(P.xmap + xmb + kg);
         const bool gather = io.xperm != nullptr;
         const bool load = P.mode != 3 && kval > 0;
         // panel column stride in the slot: h itself when h == 2, 6 (mod 8)
@@ -186,7 +191,10 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int pst = prun ? h : kK2Ps;
         // runs of columns on one panel (consecutive panel columns and input rows)
         const int prev = __shfl_up_sync(0xffffffffu, sidx, 1);
+        const int prevx = __shfl_up_sync(0xffffffffu, xi, 1);
         unsigned runs = __ballot_sync(0xffffffffu, ok && lane < kK2Kc && (c == 0 || prev != sidx));
+        // input rows: runs also break where the kept columns skip input rows
+        unsigned xruns = __ballot_sync(0xffffffffu, ok && lane < kK2Kc && (c == 0 || prev != sidx || prevx + 1 != xi));
         double2* pd = Pb + slot * kK2PBuf;
         double2* xd = Xb + slot * kXBuf;
         if (!xrole) {  // panels: plan constants, never wait on other strips
@@ -237,10 +245,10 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
               for (int rhs = lane >> 4; rhs < P.ncv; rhs += 2) cp_async16(xk + rhs, xs + rhs * io.xld);
             }
           } else {  // stage buffers: rows padded to the slot stride, one copy per run
-            while (runs) {
-              const int r0 = __ffs(runs) - 1;
-              runs &= runs - 1;
-              const int r1 = runs ? __ffs(runs) - 1 : kval;
+            while (xruns) {
+              const int r0 = __ffs(xruns) - 1;
+              xruns &= xruns - 1;
+              const int r1 = xruns ? __ffs(xruns) - 1 : kval;
               const int64_t src = static_cast<int64_t>(__shfl_sync(0xffffffffu, xi, r0)) * kXs;
               if (lane == 0) flowdev::bulk_g2s(xd + r0 * kXs, io.x + src, (r1 - r0) * kXs * 16u, &full[slot]);
             }
@@ -322,6 +330,26 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
       const int stage = m.z & 255;
       const K2FStage io = P.st[stage];
       const bool last = stage + 1 == P.nstages;
+      const int ab = P.strips[item].pad_[1];
+      if (ab >= 0 && row < m.y) {  // identity columns: Y(row, :) += X(input row, :)
+        const int xa = __ldg(P.addx + ab + row);
+        if (xa >= 0) {
+          const K2FStage xin = P.st[stage];
+          const double2* xr = xin.xperm ? xin.x + __ldg(xin.xperm + xa) : xin.x + static_cast<int64_t>(xa) * xin.xld;
+          const int64_t rs = xin.xperm ? xin.xld : 1;  // user operand: column-major; stage buffers: row-major
+#pragma unroll
+          for (int cb = 0; cb < NCB; ++cb)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int rhs = (kW / 2) * ch + cb * 8 + 2 * t + i;
+              if (rhs < P.ncv) {
+                const double2 v = xin.xperm ? __ldg(xr + rhs * rs) : flowdev::ld_cg(xr + rhs);
+                acc[cb][0][i] += v.x;
+                acc[cb][1][i] += v.y;
+              }
+            }
+        }
+      }
       if (row < m.y) {
         int idx = m.x + row;
         if (io.yperm) idx = __ldg(io.yperm + idx);

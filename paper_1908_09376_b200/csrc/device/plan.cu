@@ -388,6 +388,8 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
   up(&D.d_ctx, dense.data(), ns * sizeof(StripCtx), "upload strip records");
   for (Stage& stg : D.stages) stg.flow_bytes = stg.payload_bytes;
   D.farena_elems = 0;
+  D.k2_elems = 0;
+  for (const Strip& st : strips) D.k2_elems += static_cast<int64_t>(st.h) * st.xcols;
   if (ns == 0 || D.ncols_total > INT32_MAX) return;
 
   // identity detection on the dense panels
@@ -595,6 +597,7 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
     stg.flow_bytes += 16 * comp_elems;
   }
   D.farena_elems = at - D.arena_elems;
+  if (any) build_k2_records(D, strips, segs, order, comp);
   if (!any) {  // nothing to compress: the dense records serve both
     for (Stage& stg : D.stages) stg.flow_bytes = stg.payload_bytes;
     D.d_fctx = nullptr;
@@ -630,6 +633,73 @@ void Plan::build_flow_records(Direction& D, const std::vector<Strip>& strips, co
   cudaFree(D.d_arena);
   D.d_arena = arena;
   up(&D.d_fctx, comp.data(), ns * sizeof(StripCtx), "upload compressed strip records");
+}
+
+// k2_flow records for the identity-compressed panels.  The DMMA tiles are 32
+// rows, so unit rows save no tensor-core work; unit / zero columns shorten K.
+// A strip qualifies when its compressed record has no unit rows and at most
+// one identity add per row (the V-type ID strips): its panels are the
+// compressed ones (h x n' per panel), its kept columns' input rows go to
+// xmap, and each row's added input row to addx.  Other strips stay dense.
+void Plan::build_k2_records(Direction& D, const std::vector<Strip>& strips, const std::vector<Seg>& segs,
+                            const std::vector<size_t>& order, const std::vector<StripCtx>& comp) {
+  const size_t ns = strips.size();
+  std::vector<size_t> pos(ns);
+  for (size_t t = 0; t < ns; ++t) pos[order[t]] = t;
+  std::vector<Strip> ks(strips);
+  std::vector<Seg> kg;
+  std::vector<int> xmap, addx;
+  bool any = false;
+  for (size_t o = 0; o < ns; ++o) {
+    const StripCtx& c = comp[pos[o]];
+    const Strip& st = strips[o];
+    bool ok = c.mapped == 1;
+    int rowadds[32] = {0};
+    for (int j = 0; ok && j < st.nseg; ++j) {
+      ok = c.g[j].urows == 0;
+      for (int r = 0; r < 32; ++r) rowadds[r] += (c.g[j].adds >> r) & 1u;
+    }
+    for (int r = 0; ok && r < 32; ++r) ok = rowadds[r] <= 1;
+    if (!ok) continue;
+    Strip& k = ks[o];
+    k.seg0 = static_cast<int32_t>(segs.size() + kg.size());  // after the dense segs (one array)
+    k.xcols = c.nkept;
+    k.pad_[0] = static_cast<int32_t>(xmap.size());
+    k.pad_[1] = static_cast<int32_t>(addx.size());
+    int kk = 0;
+    for (int j = 0; j < st.nseg; ++j) {
+      Seg g = segs[static_cast<size_t>(st.seg0 + j)];
+      g.off = c.g[j].off;
+      g.n = c.g[j].n;
+      kg.push_back(g);
+      for (int q = 0; q < c.g[j].n; ++q) xmap.push_back(g.x0 + c.cmap[kk++]);
+    }
+    int add[32];
+    for (int r = 0; r < 32; ++r) add[r] = -1;
+    for (int j = 0; j < st.nseg; ++j)
+      for (int r = 0; r < 32; ++r)
+        if ((c.g[j].adds >> r) & 1u) {
+          const int p = c.addpos[c.g[j].aoff + __builtin_popcount(c.g[j].adds & ((1u << r) - 1u))];
+          const int e = p - c.nkept;  // (no unit rows: every add is an extra entry)
+          const unsigned key = c.xext[e];
+          add[r] = c.g[key >> 8].x0 + static_cast<int>(key & 0xffu);
+        }
+    addx.insert(addx.end(), add, add + 32);
+    any = true;
+  }
+  D.k2_elems = 0;  // panel entries k2_flow multiplies (64-wide / 32-wide tiles)
+  for (size_t o = 0; o < ns; ++o) D.k2_elems += static_cast<int64_t>(strips[o].h) * (any ? ks[o].xcols : strips[o].xcols);
+  if (!any) return;
+  std::vector<Seg> allsegs(segs);
+  allsegs.insert(allsegs.end(), kg.begin(), kg.end());
+  auto up = [](void** dptr, const void* src, size_t bytes, const char* what) {
+    cuda_check(cudaMalloc(dptr, std::max<size_t>(bytes, 16)), what);
+    if (bytes) cuda_check(cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice), what);
+  };
+  up(reinterpret_cast<void**>(&D.d_k2strips), ks.data(), ks.size() * sizeof(Strip), "upload k2 strips");
+  up(reinterpret_cast<void**>(&D.d_k2segs), allsegs.data(), allsegs.size() * sizeof(Seg), "upload k2 segs");
+  up(reinterpret_cast<void**>(&D.d_k2xmap), xmap.data(), xmap.size() * sizeof(int), "upload k2 column map");
+  up(reinterpret_cast<void**>(&D.d_k2addx), addx.data(), addx.size() * sizeof(int), "upload k2 adds");
 }
 
 // Build one direction (forward or transpose) of the plan on the host and
@@ -732,6 +802,7 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
       for (int64_t y = a; y < b; y += strip_rows) {
         const int h = static_cast<int>(std::min<int64_t>(strip_rows, b - y));
         Strip st{};
+        st.pad_[0] = st.pad_[1] = -1;  // k2_flow: dense strip (no identity maps)
         st.y0 = static_cast<int32_t>(y);
         st.h = h;
         st.seg0 = static_cast<int32_t>(segs.size());
@@ -875,6 +946,10 @@ Plan::~Plan() {
     cudaFree(D.d_ctx);
     cudaFree(D.d_fctx);
     cudaFree(D.d_wmap);
+    cudaFree(D.d_k2strips);
+    cudaFree(D.d_k2segs);
+    cudaFree(D.d_k2xmap);
+    cudaFree(D.d_k2addx);
     cudaFree(D.d_k2buf);
     cudaFree(D.d_k2done);
     cudaFree(D.d_k2epoch);
@@ -1079,8 +1154,14 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   const int ns = static_cast<int>(D.stages.size());
   const int64_t in_ld = d == 0 ? ncols : nrows, out_ld = d == 0 ? nrows : ncols;
   K2FParams P{};
-  P.strips = D.d_strips;
-  P.segs = D.d_segs;
+  // identity-compressed V panels (flag bit 9: dense) on 32- and 64-wide tiles;
+  // the 16-wide tiles are latency-bound and lose more to the end-of-strip
+  // identity adds and the split input-row copies than the shorter K saves
+  // (cfg1: 16 RHS 171.6 vs 162.4 us; 24 / 48 / 64 RHS 204 / 357 / 377 vs
+  // 217 / 402 / 392 us)
+  const bool comp = D.d_k2strips && !(flags & 512u);
+  P.xmap = D.d_k2xmap;
+  P.addx = D.d_k2addx;
   P.arena = D.d_arena;
   P.done = D.d_k2done;
   P.epoch = D.d_k2epoch;
@@ -1098,6 +1179,8 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   for (int64_t c0 = 0; c0 < nrhs; c0 += kK2Rhs) {
     P.ncv = static_cast<int>(std::min<int64_t>(kK2Rhs, nrhs - c0));
     const int wi = P.ncv <= 16 ? 0 : (P.ncv <= 32 ? 1 : 2);  // narrowest tile covering the slice
+    P.strips = comp && wi > 0 ? D.d_k2strips : D.d_strips;
+    P.segs = comp && wi > 0 ? D.d_k2segs : D.d_segs;
     const int64_t xs = (16 << wi) + 2;                      // its X / stage-row stride
     cfg.gridDim = dim3(static_cast<unsigned>(k2flow_grid[wi]), 1, 1);
     int64_t off = 0;

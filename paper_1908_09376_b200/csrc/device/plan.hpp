@@ -11,6 +11,8 @@
 
 namespace midbf::dev {
 
+struct StripCtx;
+
 constexpr int kMaxStages = 64;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
@@ -68,6 +70,12 @@ struct Direction {
   void* d_ctx = nullptr;          // k1_flow strip records (StripCtx, flow.cuh), dense panels
   void* d_fctx = nullptr;         // ... identity-compressed panels (null: nothing to compress)
   int* d_wmap = nullptr;          // wide compressed strips: kept / add columns (StripCtx::wbase)
+  // k2_flow on identity-compressed V-type strips (build_k2_records); null: all dense
+  Strip* d_k2strips = nullptr;
+  Seg* d_k2segs = nullptr;  // the dense segs followed by the compressed strips' segs
+  int* d_k2xmap = nullptr;
+  int* d_k2addx = nullptr;
+  int64_t k2_elems = 0;  // panel entries k2_flow multiplies on 32 / 64-wide tiles
   int64_t farena_elems = 0;       // compressed panels, stored behind the dense ones in d_arena
   int64_t ncols_total = 0;        // panel columns over all segments (plan build)
   double2* d_stagebuf = nullptr;  // outputs of every stage but the last, two parity sets
@@ -143,6 +151,8 @@ class Plan {
   void build_direction(int d, const PlanTables& T, const double2* d_raw,
                        const std::vector<std::vector<int64_t>>& raw_off);
   void build_flow_records(Direction& D, const std::vector<Strip>& strips, const std::vector<Seg>& segs);
+  void build_k2_records(Direction& D, const std::vector<Strip>& strips, const std::vector<Seg>& segs,
+                        const std::vector<size_t>& order, const std::vector<StripCtx>& comp);
   void ensure_buffers(int64_t nrhs);
   void launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);
   void launch_stages(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream);

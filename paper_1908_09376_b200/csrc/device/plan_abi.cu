@@ -319,6 +319,18 @@ extern "C" int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* 
   });
 }
 
+// Panel entries x 16 bytes the multi-RHS DMMA kernel multiplies per apply on
+// 32- / 64-wide tiles (identity-compressed V-type strips unless flag bit 9).
+extern "C" int midbf_plan_k2_bytes(midbf_plan_t plan, int transpose, int64_t* out) {
+  return guard([&] {
+    const Plan& p = *plan->p;
+    const auto& D = p.dir[transpose ? 1 : 0];
+    int64_t dense = 0;
+    for (const auto& st : D.stages) dense += st.payload_bytes;
+    *out = (D.d_k2strips && !(p.flags & 512u)) ? 16 * D.k2_elems : dense;
+  });
+}
+
 // Tuning switches (bench / profiling): bit0 PDL, bit1 L2 bulk prefetch
 // (stage kernels), bit2 CUDA graphs, bit3 persistent dataflow kernel.
 extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {

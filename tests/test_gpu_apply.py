@@ -130,17 +130,19 @@ def test_identity_compression(pair, variant):
     if Fo.L >= 1:  # factors with ID blocks
         assert streamed < stored
     f, g = cvec(Fo.ncols, 24), cvec(Fo.nrows, 25)
+    F48 = cvec(Fo.ncols, 26, cols=48)  # k2_flow on a 64-wide tile: compressed V-type strips
     try:
         plan.set_flags(variant=variant)
-        a, b = plan.apply(f), plan.apply(g, transpose=True)
+        a, b, c = plan.apply(f), plan.apply(g, transpose=True), plan.apply(F48)
         plan.set_flags(variant=variant, compress=False)
         assert sum(plan.flow_bytes()) == stored
-        a0, b0 = plan.apply(f), plan.apply(g, transpose=True)
+        a0, b0, c0 = plan.apply(f), plan.apply(g, transpose=True), plan.apply(F48)
     finally:
         plan.set_flags()
-    assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14
+    assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14 and rel(c, c0) <= 1e-14
     assert rel(a, Fo.apply(f)) <= TOL
     assert rel(b, Fo.apply_transpose(g)) <= TOL
+    assert rel(c, Fo.apply(F48)) <= TOL
 
 
 @pytest.fixture(scope="module")

@@ -24,20 +24,21 @@ def main():
     ap.add_argument("--rounds", type=int, default=15)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--transpose", action="store_true")
+    ap.add_argument("--nrhs", type=int, default=1)
     a = ap.parse_args()
     K, X, Om, fk, nrhs, desc = bench.workload(a.config)
     F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, seed=M.chain(0, 0x666163))
     plan = F.plan(3)
     nin, nout = (F.nrows, F.ncols) if a.transpose else (F.ncols, F.nrows)
-    f = torch.randn(nin, dtype=torch.complex128, device="cuda")
-    g = torch.empty(nout, dtype=torch.complex128, device="cuda")
+    f = torch.randn(nin * a.nrhs, dtype=torch.complex128, device="cuda")
+    g = torch.empty(nout * a.nrhs, dtype=torch.complex128, device="cuda")
     s = torch.cuda.current_stream()
     ref = None
     times = {fl: [] for fl in a.flags}
     for fl in a.flags:  # warm every graph / variant once, check agreement
         M.lib().midbf_plan_set_flags(plan._h, fl)
         for _ in range(3):
-            plan.apply_ptr(f.data_ptr(), g.data_ptr(), 1, a.transpose, s.cuda_stream)
+            plan.apply_ptr(f.data_ptr(), g.data_ptr(), a.nrhs, a.transpose, s.cuda_stream)
         torch.cuda.synchronize()
         if ref is None:
             ref = g.clone()
@@ -47,11 +48,11 @@ def main():
     for _ in range(a.rounds):
         for fl in a.flags:
             M.lib().midbf_plan_set_flags(plan._h, fl)
-            plan.apply_ptr(f.data_ptr(), g.data_ptr(), 1, a.transpose, s.cuda_stream)
+            plan.apply_ptr(f.data_ptr(), g.data_ptr(), a.nrhs, a.transpose, s.cuda_stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             for _ in range(a.reps):
-                plan.apply_ptr(f.data_ptr(), g.data_ptr(), 1, a.transpose, s.cuda_stream)
+                plan.apply_ptr(f.data_ptr(), g.data_ptr(), a.nrhs, a.transpose, s.cuda_stream)
             e1.record(s)
             torch.cuda.synchronize()
             times[fl].append(e0.elapsed_time(e1) * 1e3 / a.reps)
