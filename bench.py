@@ -325,27 +325,33 @@ def main():
     launches = plan.launches(nrhs)
     traffic = measured_traffic(args.config, launches)
     if nrhs == 1:
-        # k1_flow streams the identity-compressed panels: the ID blocks'
-        # exact unit rows / columns are gathered from x, not read from HBM
+        # algorithmic bytes = the factor as stored (16*total_nnz)
+        # + vectors.  k1_flow streams fewer: the ID blocks' exact unit rows /
+        # columns are gathered from x (midbf_plan_flow_bytes); the HBM
+        # efficiency on the bytes actually streamed is reported beside it.
         streamed = sum(flow_bytes) + vec_bytes
-        ach = streamed / (ms_step * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                    "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_apply": streamed,
-                    "factor_bytes_per_apply": alg_bytes, "factor_equivalent_gbs": achieved,
-                    "note": "achieved = (panel bytes k1_flow streams (identity-compressed, midbf_plan_flow_bytes) "
-                            "+ 16*(N_in+N_out)) / apply time; factor_equivalent_gbs = (16*total_nnz + vectors) / "
-                            f"apply time; one apply = {launches} k1_flow launch in one CUDA graph"}
+        sgbs = streamed / (ms_step * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                    "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_apply": alg_bytes,
+                    "streamed_bytes_per_apply": streamed, "streamed_gbs": sgbs, "streamed_frac": sgbs / hbm,
+                    "note": "achieved = (16*total_nnz + 16*(N_in+N_out)) / apply time (SURVEY.md 8(d)); k1_flow "
+                            "streams only the identity-compressed panels (streamed_*; traffic = ncu DRAM bytes "
+                            f"of that launch); one apply = {launches} k1_flow launch in one CUDA graph"}
     else:
-        # k2_flow skips the exact identity columns of V-type ID strips on 32/64-wide tiles
-        flops = 8.0 * (plan.k2_bytes() / 16) * nrhs
+        # algorithmic flops = 8 * nrhs * total_nnz; k2_flow skips
+        # the exact identity columns of V-type ID strips on 32/64-wide tiles
+        flops = 8.0 * F.total_nnz * nrhs
+        executed = 8.0 * (plan.k2_bytes() / 16) * nrhs
         tf = flops / (ms_step * 1e-3) / 1e12
+        etf = executed / (ms_step * 1e-3) / 1e12
         roofline = {"bound": "tensor", "achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                     "frac": tf / FP64_DMMA_TFLOPS, "peak_kind": "measured (tools/fp64_probe.cu, DMMA m8n8k4)",
                     "traffic": traffic, "algorithmic_flops_per_apply": flops,
-                    "factor_flops_per_apply": 8.0 * F.total_nnz * nrhs,
-                    "factor_equivalent_tflops": 8.0 * F.total_nnz * nrhs / (ms_step * 1e-3) / 1e12,
+                    "executed_flops_per_apply": executed, "executed_tflops": etf,
+                    "executed_frac": etf / FP64_DMMA_TFLOPS,
                     "hbm_gbs": achieved, "hbm_frac": achieved / hbm,
-                    "note": "algorithmic flops = 8 x panel entries k2_flow multiplies (midbf_plan_k2_bytes / 16) x nrhs; "
+                    "note": "achieved = 8*nrhs*total_nnz / apply time (SURVEY.md 8(d)); executed_* = the entries "
+                            "k2_flow multiplies (identity columns of V-type strips skipped, midbf_plan_k2_bytes); "
                             f"FP64 tensor-core (DMMA) k2_flow: {launches} cooperative dataflow launch(es) per "
                             "apply (one per 64-RHS slice) in one graph; traffic = DRAM bytes per launch"}
     line = {
