@@ -371,10 +371,11 @@ template <int FW, int FS, int SLOT>
 struct FlowCfg {
   static constexpr size_t kSlotArea = size_t(FW) * FS * SLOT;
   static constexpr size_t kXArea = size_t(FW) * 2 * kXWin * 16;
+  static constexpr size_t kAddArea = size_t(FW) * 2 * 32 * 16;  // per-row identity sums (stager -> consumer)
   static constexpr size_t kCtxArea = size_t(FW) * kQN * sizeof(StripCtx);
   // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2]
   static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 4) * 8;
-  static constexpr size_t kSmem = kSlotArea + kXArea + kCtxArea + kBarArea;
+  static constexpr size_t kSmem = kSlotArea + kXArea + kAddArea + kCtxArea + kBarArea;
   static_assert(kSmem <= 232448, "k1_flow exceeds the 227 KB dynamic shared memory of a CTA");
 };
 
@@ -400,9 +401,11 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   const int c = warp % FW;  // pair index
   unsigned char* slots = smem + size_t(c) * FS * SLOT;
   double2* xb = reinterpret_cast<double2*>(smem + Cfg::kSlotArea) + c * 2 * kXWin;
-  StripCtx* ctx = reinterpret_cast<StripCtx*>(smem + Cfg::kSlotArea + Cfg::kXArea) + c * kQN;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kCtxArea) +
-                   c * (2 * FS + 2 * kQN + 4);
+  double2* asum = reinterpret_cast<double2*>(smem + Cfg::kSlotArea + Cfg::kXArea) + c * 2 * 32;
+  StripCtx* ctx = reinterpret_cast<StripCtx*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kAddArea) + c * kQN;
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kAddArea + Cfg::kCtxArea) +
+      c * (2 * FS + 2 * kQN + 4);
   uint64_t* full = bars;
   uint64_t* empty = bars + FS;
   uint64_t* cfull = bars + 2 * FS;
@@ -469,6 +472,23 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
         FLOW_T(13, stage_x<NS>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
+        if (C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
+          __syncwarp(mask);
+          const double2* xs = xb + b * kXWin;
+          for (int r = sl; r < C.s.h; r += NS) {
+            const unsigned below = (1u << r) - 1u;
+            double ar = 0.0, ai = 0.0;
+            for (int j = 0; j < C.s.nseg; ++j) {
+              const unsigned a = C.g[j].adds;
+              if ((a >> r) & 1u) {
+                const double2 t = xs[C.addpos[C.g[j].aoff + __popc(a & below)]];
+                ar += t.x;
+                ai += t.y;
+              }
+            }
+            asum[b * 32 + r] = make_double2(ar, ai);
+          }
+        }
       }
       __syncwarp(mask);
       if (arriver) mbar_arrive(&xfull[b]);
@@ -656,15 +676,10 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
-      if (C.mapped == 1 && row < h) {  // identity parts: one staged entry per (panel, add row)
-        for (int j = 0; j < nseg; ++j) {
-          const unsigned a = C.g[j].adds;
-          if ((a >> row) & 1u) {
-            const double2 t = xcur[C.addpos[C.g[j].aoff + __popc(a & below)]];
-            yr += t.x;
-            yi += t.y;
-          }
-        }
+      if (C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
+        const double2 t = asum[(k & 1) * 32 + row];
+        yr += t.x;
+        yi += t.y;
       } else if (C.mapped == 2 && row < h && cpar == 0) {  // wide strips: read (and poll) the entry itself
         for (int j = 0; j < nseg; ++j) {
           const unsigned a = C.g[j].adds;

@@ -860,12 +860,12 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
     cudaFree(d_jobs);
     cuda_check(e2, "k0_repack");
   }
-  if (D.max_seg <= kMaxSeg) build_flow_records(D, strips, segs);
   // two parity sets, armed with the all-ones sentinel (k1_flow's ready signal)
   cuda_check(cudaMalloc(&D.d_stagebuf, 2 * D.stagebuf_elems * sizeof(double2)), "cudaMalloc stage buffer");
   cuda_check(cudaMemset(D.d_stagebuf, 0xff, 2 * D.stagebuf_elems * sizeof(double2)), "arm stage buffers");
   cuda_check(cudaMalloc(&D.d_sync, kMaxFlowCtas * sizeof(unsigned)), "cudaMalloc sync");
   cuda_check(cudaMemset(D.d_sync, 0, kMaxFlowCtas * sizeof(unsigned)), "memset sync");
+  if (D.max_seg <= kMaxSeg) build_flow_records(D, strips, segs);
   D.built = true;
   if (std::getenv("MIDBF_PLAN_TIMING"))
     std::fprintf(stderr, "[plan] dir %d: metadata %.1f ms, repack+uploads %.1f ms (%lld strips, %lld segs)\n", d,
