@@ -201,6 +201,12 @@ int midbf_fact_stats(midbf_fact_t fact, int64_t* out);
  * out[2] nanoseconds in the device ID batches (K3 + K5 + copies), out[3]
  * nanoseconds for the whole factorize (sampler 0 / 2). */
 int midbf_fact_id_stats(midbf_fact_t fact, int64_t* out);
+/* Device time of the factorize's kernels, CUDA events on the sampler stream:
+ * out[0] K3 entry-sampling launches, out[1] entries they evaluated, out[2]
+ * their nanoseconds; out[3] K5 ID launches, out[4] their nanoseconds (all 0
+ * for host-sampled factorizations).  Not a reference interface: the
+ * reference has no device kernels to time. */
+int midbf_fact_kernel_stats(midbf_fact_t fact, int64_t* out);
 
 /* Plan introspection / tuning (benchmarks, profiling):
  * stage table out[s*4 + 0..3] = strips, payload bytes, in_len, out_len

@@ -254,8 +254,8 @@ class DevicePlan:
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
         64-RHS slice (dmma_flow) or one launch per stage.  variant: k1_flow
-        layout 0 (4 warp pairs x 3 x 16 KB), 1 (8 x 2 x 8 KB), 2 (6 x 4 x
-        8 KB), 3 chosen by the plan's size (default).  compress: k1_flow
+        layout 0 (4 warp pairs x 3 x 16 KB), 1 (8 x 2 x 8 KB), 3 chosen
+        by the plan's size (default); 2 is retired and runs 1.  compress: k1_flow
         streams the identity-compressed panels (unit rows / columns of the ID
         blocks gathered from x instead)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
@@ -351,6 +351,14 @@ class Factorization:
         o = np.zeros(4, dtype=np.int64)
         _check(lib().midbf_fact_id_stats(self._h, _ip(o)))
         return int(o[0]), int(o[1]), o[2] * 1e-9, o[3] * 1e-9
+
+    def kernel_stats(self):
+        """Device time of the factorize's kernels (CUDA events): dict with
+        K3 launches / entries / seconds and K5 launches / seconds."""
+        o = np.zeros(5, dtype=np.int64)
+        _check(lib().midbf_fact_kernel_stats(self._h, _ip(o)))
+        return {"k3_launches": int(o[0]), "k3_entries": int(o[1]), "k3_seconds": o[2] * 1e-9,
+                "k5_launches": int(o[3]), "k5_seconds": o[4] * 1e-9}
 
     def perms(self):
         rp = np.empty(self.nrows, dtype=np.int64)

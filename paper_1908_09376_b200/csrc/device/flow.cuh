@@ -316,7 +316,13 @@ __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, con
     if (idx[i] >= 0) v[i] = xperm ? __ldg(x + __ldg(xperm + idx[i])) : ld_cg(x + idx[i]);
   if (!xperm) {
     bool ok;
+    bool first = true;
     do {
+      // The in-warp stager (NS < 32) shares its warp with the TMA-issuing
+      // lane 0: back off between polls so that spinning lanes never starve
+      // it (variant 2 deadlocked at cfg3 without this).
+      if (NS < 32 && !first) __nanosleep(64);
+      first = false;
       ok = true;
 #pragma unroll
       for (int i = 0; i < kPer; ++i)
@@ -413,7 +419,12 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   uint64_t* xfull = bars + 2 * FS + 2 * kQN;      // x window of strip k staged (buffer k & 1)
   uint64_t* xempty = bars + 2 * FS + 2 * kQN + 2;  // buffer k & 1 released by the consumer
   if (producer && lane == 0) {
-    for (int s = 0; s < 2 * FS + 2 * kQN + 4; ++s) mbar_init(&bars[s], 1);
+    // xfull: one arrival from a separate stager warp (after its warp
+    // barrier), or one per lane of the producer warp's in-warp stager, which
+    // must not use warp barriers while lane 0 runs the TMA loop (FW > 4 hung
+    // at cfg3 with them)
+    for (int s = 0; s < 2 * FS + 2 * kQN + 4; ++s)
+      mbar_init(&bars[s], (!kSep && s >= 2 * FS + 2 * kQN && s < 2 * FS + 2 * kQN + 2) ? 31 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -472,7 +483,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
         FLOW_T(13, stage_x<NS>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
-        if (C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
+        if (kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
+          // (separate stager warps only; with the in-warp stager of FW > 4
+          // the consumers sum in place)
           __syncwarp(mask);
           const double2* xs = xb + b * kXWin;
           for (int r = sl; r < C.s.h; r += NS) {
@@ -490,8 +503,12 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
           }
         }
       }
-      __syncwarp(mask);
-      if (arriver) mbar_arrive(&xfull[b]);
+      if (kSep) {
+        __syncwarp(mask);
+        if (arriver) mbar_arrive(&xfull[b]);
+      } else {
+        mbar_arrive(&xfull[b]);  // each lane's own entries (release)
+      }
     }
     rearm(sl, NS);
   };
@@ -676,10 +693,19 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
-      if (C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
+      if (kSep && C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
         const double2 t = asum[(k & 1) * 32 + row];
         yr += t.x;
         yi += t.y;
+      } else if (C.mapped == 1 && row < h) {  // identity parts: one staged entry per (panel, add row)
+        for (int j = 0; j < nseg; ++j) {
+          const unsigned a = C.g[j].adds;
+          if ((a >> row) & 1u) {
+            const double2 t = xcur[C.addpos[C.g[j].aoff + __popc(a & below)]];
+            yr += t.x;
+            yi += t.y;
+          }
+        }
       } else if (C.mapped == 2 && row < h && cpar == 0) {  // wide strips: read (and poll) the entry itself
         for (int j = 0; j < nseg; ++j) {
           const unsigned a = C.g[j].adds;

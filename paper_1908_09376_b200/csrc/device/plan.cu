@@ -924,7 +924,7 @@ Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   if (timing) std::fprintf(stderr, "[plan] raw upload %.1f ms, directions %.1f ms\n", ms(t0, t1), ms(t1, t2));
   flow_grid[0] = flow_setup<4, 3, 16384>(num_sms);
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
-  flow_grid[2] = flow_setup<6, 3, 8192>(num_sms);
+  flow_grid[2] = flow_grid[1];  // variant 2 (6 pairs x 3 x 8 KB) retired: it deadlocked at cfg3
   flow_grid[3] = flow_grid[0];  // unused: variant 3 resolves per direction (flow_variant)
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
@@ -982,7 +982,7 @@ Plan::~Plan() {
 }
 
 // k1_flow variant: flags bits 4-5 (0: 4 pairs x 3 x 16 KB, 1: 8 x 2 x 8 KB,
-// 2: 6 x 4 x 8 KB), 3 = by size: measured at cfg1 (358 MB of panels) variant
+// 2: retired -- 6 x 3 x 8 KB never won and hung at cfg3 -- runs 1), 3 = by size: measured at cfg1 (358 MB of panels) variant
 // 0 is fastest (66.5 vs 74.7 us), at cfg3 / cfg2 (872 / 1726 MB) variant 1
 // (135.7 vs 140.6, 275.1 vs 287.2 us) -- more warps pay off once every
 // warp streams enough panels to amortise its pipeline start and stage waits.
@@ -1057,10 +1057,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.in_len = D.in_len;
   switch (variant) {
     case 1:
+    case 2:  // retired variant: runs variant 1
       flow_launch<8, 2, 8192>(P, flow_grid[1], stream);
-      break;
-    case 2:
-      flow_launch<6, 3, 8192>(P, flow_grid[2], stream);
       break;
     default:
       flow_launch<4, 3, 16384>(P, flow_grid[0], stream);

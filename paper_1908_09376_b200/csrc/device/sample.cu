@@ -151,6 +151,243 @@ __global__ void __launch_bounds__(256) k3_sample_ws(DevK k, const int4* __restri
   }
 }
 
+// ---- staged sampling (K3 / K4) ---------------------------------------------
+// Every phase kernel is a function of per-row operands R (depending on x_i
+// only) and per-column operands C (depending on xi_j only).  A block's
+// operands are staged once in shared memory (structure of arrays, stride
+// `rs` / `cs` between operand q and q+1), so the entry loop issues no
+// dependent global loads: it is the FP64 arithmetic of Phi plus sincos.
+// Staged values are the reference's own intermediate values (c_k*c_k is the
+// first multiply of c_k*c_k*xi*xi, src/kernels.cpp:22), so results stay
+// bitwise those of phase_of().
+template <int KIND>
+struct Ops;
+
+template <>
+struct Ops<MIDBF_KERNEL_FIO2D> {
+  __device__ static int rw(const DevK&) { return 4; }
+  __device__ static int cw(const DevK&) { return 2; }
+  __device__ static void row(const DevK& k, int64_t i, double* o, int s) {
+    const double c1 = k.coef[3 * i], c2 = k.coef[3 * i + 1];
+    o[0] = k.X[2 * i];
+    o[s] = k.X[2 * i + 1];
+    o[2 * s] = __dmul_rn(c1, c1);
+    o[3 * s] = __dmul_rn(c2, c2);
+  }
+  __device__ static void col(const DevK& k, int64_t j, double* o, int s) {
+    o[0] = k.Om[2 * j];
+    o[s] = k.Om[2 * j + 1];
+  }
+  __device__ static double phase(const DevK&, const double* R, int rs, const double* C, int cs) {
+    const double w0 = C[0], w1 = C[cs];
+    const double lin = __dadd_rn(__dmul_rn(R[0], w0), __dmul_rn(R[rs], w1));
+    const double q = __dadd_rn(__dmul_rn(__dmul_rn(R[2 * rs], w0), w0), __dmul_rn(__dmul_rn(R[3 * rs], w1), w1));
+    return __dadd_rn(lin, __dsqrt_rn(q));
+  }
+};
+
+template <>
+struct Ops<MIDBF_KERNEL_FIO3D> {
+  __device__ static int rw(const DevK&) { return 6; }
+  __device__ static int cw(const DevK&) { return 3; }
+  __device__ static void row(const DevK& k, int64_t i, double* o, int s) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double a = k.coef[3 * i + q];
+      o[q * s] = k.X[3 * i + q];
+      o[(3 + q) * s] = __dmul_rn(a, a);
+    }
+  }
+  __device__ static void col(const DevK& k, int64_t j, double* o, int s) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) o[q * s] = k.Om[3 * j + q];
+  }
+  __device__ static double phase(const DevK&, const double* R, int rs, const double* C, int cs) {
+    const double w0 = C[0], w1 = C[cs], w2 = C[2 * cs];
+    const double lin =
+        __dadd_rn(__dadd_rn(__dmul_rn(R[0], w0), __dmul_rn(R[rs], w1)), __dmul_rn(R[2 * rs], w2));
+    const double q = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(R[3 * rs], w0), w0),
+                                         __dmul_rn(__dmul_rn(R[4 * rs], w1), w1)),
+                               __dmul_rn(__dmul_rn(R[5 * rs], w2), w2));
+    return __dadd_rn(lin, __dsqrt_rn(q));
+  }
+};
+
+template <>
+struct Ops<MIDBF_KERNEL_LOWRANK> {
+  __device__ static int rw(const DevK& k) { return k.rank; }
+  __device__ static int cw(const DevK& k) { return k.rank; }
+  __device__ static void row(const DevK& k, int64_t i, double* o, int s) {
+    for (int q = 0; q < k.rank; ++q) o[q * s] = k.A[i * k.rank + q];
+  }
+  __device__ static void col(const DevK& k, int64_t j, double* o, int s) {
+    for (int q = 0; q < k.rank; ++q) o[q * s] = k.B[j * k.rank + q];
+  }
+  __device__ static double phase(const DevK& k, const double* R, int rs, const double* C, int cs) {
+    double s = 0.0;
+    if (k.rank == 8) {  // BASELINE cfg2's rank, unrolled
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s = __dadd_rn(s, __dmul_rn(R[q * rs], C[q * cs]));
+    } else {
+      for (int q = 0; q < k.rank; ++q) s = __dadd_rn(s, __dmul_rn(R[q * rs], C[q * cs]));
+    }
+    return s;
+  }
+};
+
+template <>
+struct Ops<MIDBF_KERNEL_NUFFT> {
+  __device__ static int rw(const DevK& k) { return k.dim; }
+  __device__ static int cw(const DevK& k) { return k.dim; }
+  __device__ static void row(const DevK& k, int64_t i, double* o, int s) {
+    for (int q = 0; q < k.dim; ++q) o[q * s] = k.X[i * k.dim + q];
+  }
+  __device__ static void col(const DevK& k, int64_t j, double* o, int s) {
+    for (int q = 0; q < k.dim; ++q) o[q * s] = k.Om[j * k.dim + q];
+  }
+  __device__ static double phase(const DevK& k, const double* R, int rs, const double* C, int cs) {
+    double s = 0.0;
+    for (int q = 0; q < k.dim; ++q) s = __dadd_rn(s, __dmul_rn(R[q * rs], C[q * cs]));
+    return s;
+  }
+};
+
+// Staging capacities: m-side (fast, contiguous output index) operands for up
+// to kMCap points, n-side operands in tiles of kNTile points.  Operand
+// width <= kMaxW doubles per point (FIO 3D: 6; low-rank / x.xi: r, dim).
+constexpr int kMCap = 512, kNTile = 128, kMaxW = 8;
+constexpr int64_t kTaskEntries = 8192;  // entries per CTA of k3_sample (sample_blocks sub-tasks)
+constexpr size_t kStageSmem = static_cast<size_t>(kMCap + kNTile) * kMaxW * sizeof(double);  // 40 KB
+
+__host__ __device__ inline bool stageable(int kind, int rank, int dim) {
+  switch (kind) {
+    case MIDBF_KERNEL_FIO2D:
+    case MIDBF_KERNEL_FIO3D:
+      return true;
+    case MIDBF_KERNEL_LOWRANK:
+      return rank >= 1 && rank <= kMaxW;
+    case MIDBF_KERNEL_NUFFT:
+      return dim >= 1 && dim <= kMaxW;
+    default:
+      return false;
+  }
+}
+
+// One block B (m x n, column-major, ld m) of K(rid[ro..ro+nr), cid[co..co+nc)),
+// or with TRANS of its transpose (m = nc, n = nr).  Requires m <= kMCap.
+template <int KIND, bool TRANS>
+__device__ __forceinline__ void fill_staged(const DevK& k, const int* __restrict__ rid, const int* __restrict__ cid,
+                                            int ro, int nr, int co, int nc, double2* __restrict__ B, double* sm) {
+  using O = Ops<KIND>;
+  const int m = TRANS ? nc : nr, n = TRANS ? nr : nc;
+  double* sM = sm;                 // m-side operands, stride kMCap
+  double* sN = sm + kMCap * kMaxW; // n-side operands, stride kNTile
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    if (TRANS)
+      O::col(k, cid[co + r], sM + r, kMCap);
+    else
+      O::row(k, rid[ro + r], sM + r, kMCap);
+  }
+  const int sr = static_cast<int>(blockDim.x) % m, sc = static_cast<int>(blockDim.x) / m;
+  for (int c0 = 0; c0 < n; c0 += kNTile) {
+    const int nt = min(kNTile, n - c0);
+    __syncthreads();  // previous tile consumed (and, first time, m-side staged)
+    for (int c = threadIdx.x; c < nt; c += blockDim.x) {
+      if (TRANS)
+        O::row(k, rid[ro + c0 + c], sN + c, kNTile);
+      else
+        O::col(k, cid[co + c0 + c], sN + c, kNTile);
+    }
+    __syncthreads();
+    double2* out = B + static_cast<int64_t>(c0) * m;
+    int r = threadIdx.x % m, c = threadIdx.x / m;
+    for (int e = threadIdx.x; c < nt; e += blockDim.x) {
+      const double phi = TRANS ? O::phase(k, sN + c, kNTile, sM + r, kMCap) : O::phase(k, sM + r, kMCap, sN + c, kNTile);
+      out[e] = polar1(phi);
+      r += sr;
+      c += sc;
+      if (r >= m) {
+        r -= m;
+        ++c;
+      }
+    }
+  }
+}
+
+// Generic (unstaged) fill: kernels without a phase, or blocks taller than
+// the staging capacity.
+template <bool TRANS>
+__device__ __forceinline__ void fill_generic(const DevK& k, const int* __restrict__ rid, const int* __restrict__ cid,
+                                             int ro, int nr, int co, int nc, double2* __restrict__ B) {
+  const int m = TRANS ? nc : nr;
+  const int total = nr * nc;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int c = e / m, r = e - c * m;
+    B[e] = TRANS ? entry(k, rid[ro + c], cid[co + r]) : entry(k, rid[ro + r], cid[co + c]);
+  }
+}
+
+template <int KIND, bool TRANS>
+__device__ __forceinline__ void fill_block(const DevK& k, const int* __restrict__ rid, const int* __restrict__ cid,
+                                           int ro, int nr, int co, int nc, double2* __restrict__ B, double* sm) {
+  if ((TRANS ? nc : nr) <= kMCap)
+    fill_staged<KIND, TRANS>(k, rid, cid, ro, nr, co, nc, B, sm);
+  else
+    fill_generic<TRANS>(k, rid, cid, ro, nr, co, nc, B);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k3_sample_s(DevK k, const int* __restrict__ tasks, const int* __restrict__ rid,
+                                                   const int* __restrict__ cid, double2* __restrict__ out) {
+  extern __shared__ double sm[];
+  const int* tk = tasks + 5 * blockIdx.x;
+  fill_block<KIND, false>(k, rid, cid, tk[0], tk[1], tk[2], tk[3], out + tk[4], sm);
+}
+
+template <int KIND, bool TRANS>
+__global__ void __launch_bounds__(256) k3_sample_ws_s(DevK k, const int4* __restrict__ rc,
+                                                      const IdTask* __restrict__ tasks, const int* __restrict__ rid,
+                                                      const int* __restrict__ cid, double2* __restrict__ ws) {
+  extern __shared__ double sm[];
+  const int4 q = rc[blockIdx.x];
+  fill_block<KIND, TRANS>(k, rid, cid, q.x, q.y, q.z, q.w, ws + tasks[blockIdx.x].off, sm);
+}
+
+// Direct sum, staged: the CTA's 256 rows and each 256-column tile of
+// operands (plus f) in shared memory.
+template <int KIND>
+__global__ void __launch_bounds__(256) k4_direct_s(DevK k, const int* __restrict__ rows, int nsel,
+                                                   const double2* __restrict__ f, int64_t ncols, int64_t cps,
+                                                   double2* __restrict__ partial) {
+  using O = Ops<KIND>;
+  constexpr int kT = 256;
+  __shared__ double sR[kMaxW * kT];
+  __shared__ double sC[kMaxW * kT];
+  __shared__ double2 fs[kT];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c0 = blockIdx.y * cps, c1 = min(ncols, c0 + cps);
+  O::row(k, r < nsel ? rows[r] : rows[0], sR + threadIdx.x, kT);
+  double ar = 0.0, ai = 0.0;
+  for (int64_t cb = c0; cb < c1; cb += kT) {
+    const int cn = static_cast<int>(c1 - cb < kT ? c1 - cb : kT);
+    __syncthreads();
+    if (threadIdx.x < cn) {
+      fs[threadIdx.x] = f[cb + threadIdx.x];
+      O::col(k, cb + threadIdx.x, sC + threadIdx.x, kT);
+    }
+    __syncthreads();
+    if (r < nsel) {
+      for (int q = 0; q < cn; ++q) {
+        const double2 e = polar1(O::phase(k, sR + threadIdx.x, kT, sC + q, kT));
+        const double2 x = fs[q];
+        ar = __dadd_rn(ar, __dsub_rn(__dmul_rn(e.x, x.x), __dmul_rn(e.y, x.y)));
+        ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(e.x, x.y), __dmul_rn(e.y, x.x)));
+      }
+    }
+  }
+  if (r < nsel) partial[static_cast<int64_t>(blockIdx.y) * nsel + r] = make_double2(ar, ai);
+}
+
 // Direct sum: blockIdx.x covers 256 selected rows (one per thread),
 // blockIdx.y a contiguous column split.  Column data staged in shared memory.
 constexpr int kTile = 256;
@@ -194,6 +431,75 @@ __global__ void k4_reduce(const double2* __restrict__ partial, int nsel, int nsp
     ai += p.y;
   }
   g[r] = make_double2(ar, ai);
+}
+
+// Launchers: the staged kernels for kernels with a phase (and operands that
+// fit the staging width), the generic ones otherwise.
+void launch_k3(const DevK& k, unsigned grid, cudaStream_t st, const int* tasks, const int* rid, const int* cid,
+               double2* out) {
+  if (!stageable(k.kind, k.rank, k.dim)) {
+    k3_sample<<<grid, 256, 0, st>>>(k, tasks, rid, cid, out);
+    return;
+  }
+  switch (k.kind) {
+    case MIDBF_KERNEL_FIO2D:
+      k3_sample_s<MIDBF_KERNEL_FIO2D><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      break;
+    case MIDBF_KERNEL_FIO3D:
+      k3_sample_s<MIDBF_KERNEL_FIO3D><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      break;
+    case MIDBF_KERNEL_LOWRANK:
+      k3_sample_s<MIDBF_KERNEL_LOWRANK><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      break;
+    default:
+      k3_sample_s<MIDBF_KERNEL_NUFFT><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      break;
+  }
+}
+
+template <bool TRANS>
+void launch_k3_ws(const DevK& k, unsigned grid, cudaStream_t st, const int4* rc, const IdTask* tk, const int* rid,
+                  const int* cid, double2* ws) {
+  if (!stageable(k.kind, k.rank, k.dim)) {
+    k3_sample_ws<TRANS><<<grid, 256, 0, st>>>(k, rc, tk, rid, cid, ws);
+    return;
+  }
+  switch (k.kind) {
+    case MIDBF_KERNEL_FIO2D:
+      k3_sample_ws_s<MIDBF_KERNEL_FIO2D, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      break;
+    case MIDBF_KERNEL_FIO3D:
+      k3_sample_ws_s<MIDBF_KERNEL_FIO3D, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      break;
+    case MIDBF_KERNEL_LOWRANK:
+      k3_sample_ws_s<MIDBF_KERNEL_LOWRANK, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      break;
+    default:
+      k3_sample_ws_s<MIDBF_KERNEL_NUFFT, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      break;
+  }
+}
+
+void launch_k4(const DevK& k, dim3 grid, cudaStream_t st, const int* rows, int nsel, const double2* f, int64_t ncols,
+               int64_t cps, double2* part) {
+  if (!stageable(k.kind, k.rank, k.dim)) {
+    k4_direct<<<grid, 256, 0, st>>>(k, rows, nsel, f, ncols, cps, part);
+    return;
+  }
+  switch (k.kind) {
+    case MIDBF_KERNEL_FIO2D:
+      k4_direct_s<MIDBF_KERNEL_FIO2D><<<grid, 256, 0, st>>>(k, rows, nsel, f, ncols, cps, part);
+      break;
+    case MIDBF_KERNEL_FIO3D:
+      k4_direct_s<MIDBF_KERNEL_FIO3D><<<grid, 256, 0, st>>>(k, rows, nsel, f, ncols, cps, part);
+      break;
+    case MIDBF_KERNEL_LOWRANK:
+      k4_direct_s<MIDBF_KERNEL_LOWRANK><<<grid, 256, 0, st>>>(k, rows, nsel, f, ncols, cps, part);
+      break;
+    default:
+      k4_direct_s<MIDBF_KERNEL_NUFFT><<<grid, 256, 0, st>>>(k, rows, nsel, f, ncols, cps, part);
+      break;
+  }
 }
 
 template <class T>
@@ -259,6 +565,41 @@ struct EntrySampler::Impl {
   std::vector<void*> owned;
   int64_t nrows = 0, ncols = 0;
   int64_t launched_entries = 0;
+  // Device time of the K3 / K5 launches (CUDA events on the sampler's
+  // stream), collected at the synchronisation points of each call.
+  struct Timed {
+    cudaEvent_t a, b;
+    int kind;  // 3: K3, 5: K5
+    int64_t entries;
+  };
+  std::vector<Timed> pend;
+  KernelTimes times;
+  void begin(int kind, int64_t entries) {
+    Timed t{nullptr, nullptr, kind, entries};
+    cuda_check(cudaEventCreate(&t.a), "event");
+    cuda_check(cudaEventCreate(&t.b), "event");
+    cuda_check(cudaEventRecord(t.a, stream), "event record");
+    pend.push_back(t);
+  }
+  void end() { cuda_check(cudaEventRecord(pend.back().b, stream), "event record"); }
+  void collect() {  // after the stream has been synchronised
+    for (Timed& t : pend) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+        if (t.kind == 3) {
+          times.k3_seconds += 1e-3 * ms;
+          times.k3_launches += 1;
+          times.k3_entries += t.entries;
+        } else {
+          times.k5_seconds += 1e-3 * ms;
+          times.k5_launches += 1;
+        }
+      }
+      cudaEventDestroy(t.a);
+      cudaEventDestroy(t.b);
+    }
+    pend.clear();
+  }
   static constexpr int64_t kChunk = ChunkPool::kChunk;
   cudaStream_t stream = nullptr;
   void ensure_stream() {
@@ -337,6 +678,7 @@ EntrySampler::~EntrySampler() {
 }
 
 int64_t EntrySampler::entries_evaluated() const { return impl_->launched_entries; }
+EntrySampler::KernelTimes EntrySampler::kernel_times() const { return impl_->times; }
 
 void EntrySampler::sample(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
                           const int64_t* col_ids, int64_t n_col_ids, double* out, int64_t out_len) {
@@ -367,7 +709,7 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
     if (col_ids[q] < 0 || col_ids[q] >= I.ncols) throw std::invalid_argument("column id out of range");
     cid[q] = static_cast<int>(col_ids[q]);
   }
-  // Sub-tasks: a block larger than one chunk is split into column ranges;
+  // Sub-tasks: a block larger than kTaskEntries is split into column ranges;
   // chunks = consecutive sub-tasks with <= kChunk entries.
   struct Sub {
     int ro, nr, co, nc;
@@ -380,7 +722,9 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
     if (tk[1] < 0 || tk[3] < 0 || tk[0] < 0 || tk[2] < 0 || tk[0] + tk[1] > n_row_ids || tk[2] + tk[3] > n_col_ids)
       throw std::invalid_argument("sample task outside its id lists");
     if (tk[1] == 0 || tk[3] == 0) continue;
-    const int64_t cols_per = std::max<int64_t>(1, Impl::kChunk / tk[1]);
+    // sub-tasks of <= kTaskEntries entries (one CTA each): a few large
+    // blocks (3D S blocks, 512 x 512) must still fill all 148 SMs
+    const int64_t cols_per = std::max<int64_t>(1, std::min(Impl::kChunk, kTaskEntries) / tk[1]);
     if (tk[1] > Impl::kChunk) throw std::invalid_argument("sample block taller than the sampler chunk");
     for (int64_t c0 = 0; c0 < tk[3]; c0 += cols_per)
       subs.push_back({static_cast<int>(tk[0]), static_cast<int>(tk[1]), static_cast<int>(tk[2] + c0),
@@ -436,9 +780,10 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
       if (c >= 2) cuda_check(cudaEventSynchronize(PP.ev[b]), "sample buffer reuse");
       const int64_t t0 = chunk_begin[static_cast<size_t>(c)], t1 = chunk_begin[static_cast<size_t>(c + 1)];
       if (chunk_entries[static_cast<size_t>(c)] > 0) {
-        k3_sample<<<static_cast<unsigned>(t1 - t0), 256, 0, I.stream>>>(I.k, d_tasks + 5 * t0, d_rid, d_cid,
-                                                                         CP.d_out[b]);
+        I.begin(3, chunk_entries[static_cast<size_t>(c)]);
+        launch_k3(I.k, static_cast<unsigned>(t1 - t0), I.stream, d_tasks + 5 * t0, d_rid, d_cid, CP.d_out[b]);
         cuda_check(cudaGetLastError(), "k3_sample launch");
+        I.end();
         cuda_check(cudaMemcpyAsync(reinterpret_cast<double2*>(PP.h[b]), CP.d_out[b], chunk_entries[static_cast<size_t>(c)] * sizeof(double2),
                                    cudaMemcpyDeviceToHost, I.stream),
                    "sample D2H");
@@ -448,8 +793,11 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
       I.launched_entries += chunk_entries[static_cast<size_t>(c)];
     }
     scatter(nchunks - 1);
+    cuda_check(cudaStreamSynchronize(I.stream), "sampler");
+    I.collect();
   } catch (...) {
     cudaStreamSynchronize(I.stream);
+    I.collect();
     cudaFree(d_rid);
     cudaFree(d_cid);
     cudaFree(d_tasks);
@@ -525,17 +873,21 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   };
   try {
     const unsigned nt = static_cast<unsigned>(ntasks);
+    I.begin(3, ws);
     if (rowid)
-      k3_sample_ws<true><<<nt, 256, 0, I.stream>>>(I.k, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+      launch_k3_ws<true>(I.k, nt, I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
     else
-      k3_sample_ws<false><<<nt, 256, 0, I.stream>>>(I.k, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+      launch_k3_ws<false>(I.k, nt, I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
     cuda_check(cudaGetLastError(), "k3_sample_ws launch");
+    I.end();
     cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
                "k5 smem attribute");
+    I.begin(5, 0);
     k5_id<<<nt, kIdWarps * 32, kIdSmem, I.stream>>>(
         P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0,
         P.d_vals, P.d_rank, P.d_skel, kcap);
     cuda_check(cudaGetLastError(), "k5_id launch");
+    I.end();
     if (timing) cuda_check(cudaStreamSynchronize(I.stream), "ID kernels");
     const auto t_k = now();
     if (timing)
@@ -551,11 +903,13 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
         cudaMemcpyAsync(out.skel.data(), P.d_skel, ntasks * kcap * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
         "ID skeletons D2H");
     cuda_check(cudaStreamSynchronize(I.stream), "ID batch");
+    I.collect();
     if (timing)
       std::fprintf(stderr, "[id] D2H %.2f ms (%lld MB)\n", 1e3 * std::chrono::duration<double>(now() - t_k).count(),
                    static_cast<long long>(vals * 16 >> 20));
   } catch (...) {
     cudaStreamSynchronize(I.stream);
+    I.collect();
     cleanup();
     throw;
   }
@@ -626,8 +980,7 @@ void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel
   double2 *d_part = nullptr, *d_g = nullptr;
   cuda_check(cudaMalloc(&d_part, nsplit * nsel * sizeof(double2)), "cudaMalloc partial");
   cuda_check(cudaMalloc(&d_g, nsel * sizeof(double2)), "cudaMalloc g");
-  k4_direct<<<dim3(rb, static_cast<unsigned>(nsplit)), 256>>>(I.k, d_rows, static_cast<int>(nsel), d_f, I.ncols, cps,
-                                                              d_part);
+  launch_k4(I.k, dim3(rb, static_cast<unsigned>(nsplit)), 0, d_rows, static_cast<int>(nsel), d_f, I.ncols, cps, d_part);
   cuda_check(cudaGetLastError(), "k4_direct launch");
   k4_reduce<<<rb, 256>>>(d_part, static_cast<int>(nsel), static_cast<int>(nsplit), d_g);
   cuda_check(cudaGetLastError(), "k4_reduce launch");

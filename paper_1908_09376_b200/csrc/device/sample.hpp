@@ -45,6 +45,12 @@ class EntrySampler {
   void phase_block(int64_t nr, const int64_t* rows, int64_t nc, const int64_t* cols, double* out);
   void direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g);
   int64_t entries_evaluated() const;
+  // Device time of this sampler's kernel launches (CUDA events).
+  struct KernelTimes {
+    int64_t k3_launches = 0, k3_entries = 0, k5_launches = 0;
+    double k3_seconds = 0, k5_seconds = 0;
+  };
+  KernelTimes kernel_times() const;
 
  private:
   struct Impl;

@@ -622,6 +622,12 @@ Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::Cluster
   Factorization F = factorize(fill, ids, tx, to, X, Om, cfg);
   if (stats) {
     stats->entries = smp.entries_evaluated();
+    const dev::EntrySampler::KernelTimes kt = smp.kernel_times();
+    stats->k3_launches = kt.k3_launches;
+    stats->k3_entries = kt.k3_entries;
+    stats->k3_seconds = kt.k3_seconds;
+    stats->k5_launches = kt.k5_launches;
+    stats->k5_seconds = kt.k5_seconds;
     stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   return F;

@@ -171,6 +171,16 @@ int midbf_fact_id_stats(midbf_fact_t fact, int64_t* o) {
   });
 }
 
+int midbf_fact_kernel_stats(midbf_fact_t fact, int64_t* o) {
+  return guard([&] {
+    o[0] = fact->stats.k3_launches;
+    o[1] = fact->stats.k3_entries;
+    o[2] = static_cast<int64_t>(fact->stats.k3_seconds * 1e9);  // ns
+    o[3] = fact->stats.k5_launches;
+    o[4] = static_cast<int64_t>(fact->stats.k5_seconds * 1e9);  // ns
+  });
+}
+
 int midbf_fact_factor(midbf_fact_t fact, int64_t i, int64_t* o) {
   return guard([&] {
     if (i < 0 || i >= fact->F.factor_count()) throw std::invalid_argument("factor index out of range");

@@ -17,6 +17,9 @@ struct FactorizeStats {
   std::int64_t id_fallbacks = 0;  // IDs the device handed back to the host
   double id_seconds = 0;          // wall time inside K3 + K5 ID batches (incl. copies)
   double seconds = 0;             // whole factorization
+  // device time of the sampler's kernels (CUDA events): K3 entry sampling, K5 IDs
+  std::int64_t k3_launches = 0, k3_entries = 0, k5_launches = 0;
+  double k3_seconds = 0, k5_seconds = 0;
 };
 
 Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::ClusterTree& tx,

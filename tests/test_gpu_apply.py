@@ -97,7 +97,7 @@ def test_multi_rhs_fallback_paths(pair, path):
     assert rel(default, want) <= TOL
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, "stages"])
+@pytest.mark.parametrize("variant", [0, 1, "stages"])
 def test_single_rhs_kernel_variants(pair, variant):
     """Every k1_flow layout (the size-based default picks 0 or 1) and the
     per-stage fallback (k1_stage) match the oracle, both directions."""
@@ -117,7 +117,7 @@ def test_single_rhs_kernel_variants(pair, variant):
         assert plan.launches(1) == 1
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1])
 def test_identity_compression(pair, variant):
     """k1_flow streams the ID blocks without their exact identity parts
     (unit rows / unit columns gathered from x, flow.cuh StripCtx): fewer
@@ -170,7 +170,7 @@ def test_wide_strip_identity_compression(wide3d):
     f, g = cvec(Fo.ncols, 31), cvec(Fo.nrows, 32)
     want_f, want_g = Fo.apply(f), Fo.apply_transpose(g)
     try:
-        for variant in (0, 1, 2):
+        for variant in (0, 1):
             plan.set_flags(variant=variant)
             assert rel(plan.apply(f), want_f) <= TOL
             assert rel(plan.apply(g, transpose=True), want_g) <= TOL

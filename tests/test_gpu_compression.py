@@ -129,7 +129,7 @@ def test_streams_less_than_stored(adversarial):
     assert fb[4] == stored[4]  # dense
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("nrhs", [1, 16, 48])
 def test_matches_dense_product(adversarial, variant, nrhs):
     plan, A, _ = adversarial

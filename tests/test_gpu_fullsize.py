@@ -97,3 +97,8 @@ def test_cfg3_apply_matches_oracle(gpu):
     os.unlink(path)
     f = cvec(32768, 9)
     assert rel(F.apply(f), Fo.apply(f)) <= 1e-12
+    # consecutive applies alternate k1_flow's two sentinel-armed stage-buffer
+    # sets (a single apply never re-arms); cfg3 runs the 8-pair variant
+    for s in (10, 11, 12):
+        f = cvec(32768, s)
+        assert rel(F.apply(f), Fo.apply(f)) <= 1e-12

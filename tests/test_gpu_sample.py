@@ -101,3 +101,43 @@ def test_sampler_splits_blocks_larger_than_a_chunk(gpu):
         rr, cc = np.meshgrid(r, c, indexing="ij")
         ref = Ko.entries(rr.ravel(), cc.ravel()).reshape(len(r), len(c))
         assert np.abs(Bk - ref).max() <= 4e-15
+
+
+@pytest.mark.parametrize("name,kind,kw", list(_kernels())[:5], ids=lambda x: x if isinstance(x, str) else "")
+def test_staged_and_generic_sampling_bitwise_equal(gpu, name, kind, kw):
+    """Blocks with <= 512 rows go through the shared-memory staged sampler
+    (operands per row / per column staged once, columns in 128-wide tiles);
+    taller blocks through the generic one.  The staged operands are the
+    reference's own intermediates, so both paths give the same bits."""
+    Ko, Km = O.Kernel(kind, **kw), M.Kernel(kind, **kw)
+    rng = np.random.default_rng(21)
+    rows = rng.choice(Ko.nrows, 600, replace=False)
+    cols = rng.choice(Ko.ncols, 300, replace=False)
+    tall, top, bottom = Km.sample([rows, rows[:300], rows[300:]], [cols, cols, cols])
+    assert np.array_equal(tall[:300], top) and np.array_equal(tall[300:], bottom)
+    rr, cc = np.meshgrid(rows, cols, indexing="ij")
+    ref = Ko.entries(rr.ravel(), cc.ravel()).reshape(len(rows), len(cols))
+    assert np.abs(tall - ref).max() <= 4e-15
+
+
+def test_lowrank_wider_than_staging(gpu):
+    """Rank 12 > the staging width (8): the generic sampler and direct sum."""
+    rng = np.random.default_rng(22)
+    A, B = rng.standard_normal((2048, 12)), rng.standard_normal((2048, 12)) * 4
+    Ko, Km = O.Kernel(O.KIND_LOWRANK, A=A, B=B), M.Kernel(M.KIND_LOWRANK, A=A, B=B)
+    rows, cols = rng.choice(2048, 70, replace=False), rng.choice(2048, 90, replace=False)
+    (Bk,) = Km.sample([rows], [cols])
+    rr, cc = np.meshgrid(rows, cols, indexing="ij")
+    assert np.abs(Bk - Ko.entries(rr.ravel(), cc.ravel()).reshape(70, 90)).max() <= 4e-15
+    f = cvec(2048, 23)
+    sel = rng.choice(2048, 300, replace=False)
+    assert rel(Km.direct_sum(f, sel), Ko.direct_sum(f, sel)) <= 1e-12
+
+
+def test_factorize_reports_kernel_times(gpu):
+    X = O.grid2d(32)
+    Km = M.Kernel(M.KIND_FIO2D, X=X, Omega=integer_grid(32))
+    F = M.idbf_factorize(Km, 64, k=20, eps=1e-9, sampler="device")
+    ks = F.kernel_stats()
+    assert ks["k3_launches"] >= 3 and ks["k3_entries"] == F.sample_stats()[0]
+    assert ks["k3_seconds"] > 0 and ks["k5_launches"] >= 1 and ks["k5_seconds"] > 0
