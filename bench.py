@@ -35,6 +35,11 @@ N_SM = 148
 # FP64 tensor (DMMA m8n8k4) peak measured on this pool's B200 by tools/fp64_probe.cu
 # (MEASURED_PEAKS.json records HBM and bf16 only); DFMA measured 36.7.
 FP64_DMMA_TFLOPS = 36.8
+FP64_DFMA_TFLOPS = 36.7
+# FP64 flops per sampled entry of the K3 samplers (2*DFMA + DMUL + DADD from
+# ncu SASS thread counters over whole factorizations divided by the entries
+# they sampled; profiles/r1_k3_sample.md), by kernel kind.
+K3_FLOPS_PER_ENTRY = {"fio2d": 66.0, "fio3d": 71.0, "lowrank": 60.0}
 
 
 def peaks():
@@ -241,6 +246,16 @@ def main():
         F = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="device")
         t_fac = time.perf_counter() - t0
     entries, sample_calls, sample_s = F.sample_stats()
+    ks = F.kernel_stats()
+    k3_rate = ks["k3_entries"] / ks["k3_seconds"] if ks["k3_seconds"] > 0 else None
+    fpe = K3_FLOPS_PER_ENTRY.get({M.KIND_FIO2D: "fio2d", M.KIND_FIO3D: "fio3d", M.KIND_LOWRANK: "lowrank"}.get(K.desc.kind))
+    k3_line = {"launches": ks["k3_launches"], "entries": ks["k3_entries"], "device_seconds": ks["k3_seconds"],
+               "entries_per_s": k3_rate, "k5_launches": ks["k5_launches"], "k5_device_seconds": ks["k5_seconds"],
+               "note": "CUDA events around every k3_sample* launch of the timed factorization"}
+    if fpe and k3_rate:
+        k3_line.update({"fp64_flops_per_entry": fpe, "fp64_tflops": k3_rate * fpe / 1e12, "fp64_peak": FP64_DFMA_TFLOPS,
+                        "fp64_frac": k3_rate * fpe / 1e12 / FP64_DFMA_TFLOPS,
+                        "peak_kind": "measured DFMA (tools/fp64_probe.cu)"})
     n_dev_ids, n_host_ids, id_s, _ = F.id_stats()
     plan = F.plan(1)
     M.lib().midbf_plan_set_flags(plan._h, args.flags)
@@ -379,7 +394,8 @@ def main():
         "factorize": {"seconds": t_fac, "first_call_seconds": t_fac_first, "entries_sampled_on_gpu": entries,
                       "sampler_launch_batches": sample_calls, "ids_on_gpu": n_dev_ids, "ids_on_host": n_host_ids,
                       "id_batch_seconds": id_s, "sampler_seconds": sample_s,
-                      "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L},
+                      "total_nnz": F.total_nnz, "factors": F.nfactors, "L": F.L,
+                      "k3_sampling": k3_line},
         "stages": [dict(strips=s[0], payload_mb=s[1] / 1e6, flow_mb=b / 1e6, in_len=s[2], out_len=s[3])
                    for s, b in zip(stages, flow_bytes)],
         "clocks": clk.summary(),

@@ -31,11 +31,15 @@
 
 namespace midbf::dev {
 
-constexpr int kIdRows = 8;             // register slots per lane: m <= 256
-constexpr int kIdMaxRows = 32 * kIdRows;
+// Register slots per lane ROWS: k5_id<8> takes m <= 256 (2D blocks, e.g.
+// 150 x 120 at cfg1), k5_id<16> m <= 512 (3D blocks, 320 x 512 at cfg3).
+constexpr int kIdRowsMax = 16;
 constexpr int kIdCols = 512;           // n <= 512
 constexpr int kIdWarps = 4;            // warps cooperating on one block
-constexpr size_t kIdSmem = size_t(kIdCols) * (8 + 8 + 4) + size_t(kIdMaxRows) * 16 + 64;
+template <int ROWS>
+constexpr size_t id_smem() {
+  return size_t(kIdCols) * (8 + 8 + 4) + size_t(32 * ROWS) * 16 + 64;
+}
 
 struct IdTask {
   int64_t off;   // block B (m x n, column-major) in the workspace
@@ -67,11 +71,13 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // ranks[t] = k (or -1: recompute on the host); skel[t * kcap + i] = perm[i];
 // out + ooff: V (k x n, ld k) for a column ID, W = V^T (n x k, ld n) for a row
 // ID (`rowid`: the workspace holds the transposed block).
+template <int kIdRows>
 __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
                                                        int ntasks, int kmax, double eps, int rowid,
                                                        double2* __restrict__ out, int* __restrict__ ranks,
                                                        int* __restrict__ skel, int kcap) {
   using namespace k5dev;
+  constexpr int kIdMaxRows = 32 * kIdRows;
   extern __shared__ __align__(16) unsigned char k5smem[];
   double* cur = reinterpret_cast<double*>(k5smem);
   double* ref = cur + kIdCols;

@@ -52,9 +52,56 @@ struct DevK {
   double cre, cim;
 };
 
+// sin and cos of one argument, FP64-pipe lean: Cody-Waite reduction by
+// pi/2 in three FMA steps (pi/2 split as fdlibm's pio2_1/2/3; the first part
+// has 33 bits, so q * P1 is exact for |q| < 2^20) and fdlibm's
+// __kernel_sin / __kernel_cos minimax polynomials on [-pi/4, pi/4].  Max
+// abs error 1.2e-16 against long-double sin/cos and 1.1e-16 against glibc
+// over 2e7 arguments of the BASELINE phase range (|x| < 2200).  About 22 FP64
+// operations and no table or local-memory path; |x| >= 1e6, inf and NaN take
+// CUDA's sincos.  CUDA's own sincos spends ~90 further integer / uniform-move
+// instructions per call on its general reduction (ncu, r1_k3 source page).
+// Coefficients live in the constant bank: DFMA takes them as c[][] operands
+// directly, where literal double constants cost two uniform moves each per
+// use (28 UMOV per entry in the r1_k3 SASS with literals).
+__constant__ double kSC[18] = {
+    6.36619772367581382433e-01,  6755399441055744.0,          // 2/pi, 1.5 * 2^52
+    1.57079632673412561417e+00,  6.07710050630396597660e-11,  2.02226624871116645580e-21,  // pi/2 = P1+P2+P3
+    -1.66666666666666324348e-01, 8.33333333332248946124e-03,  -1.98412698298579493134e-04,  // S1..S6
+    2.75573137070700676789e-06,  -2.50507602534068634195e-08, 1.58969099521155010221e-10,
+    4.16666666666666019037e-02,  -1.38888888888741095749e-03, 2.48015872894767294178e-05,  // C1..C6
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09,  -1.13596475577881948265e-11,
+    6.283185307179586476925286766559};  // 2 pi (the reference's product 2*pi*Phi)
+
+__device__ __forceinline__ void sincos_lean(double x, double* sn, double* cs) {
+  if (!(fabs(x) < 1.0e6)) {
+    sincos(x, sn, cs);
+    return;
+  }
+  const double kInvPio2 = kSC[0], kMagic = kSC[1], P1 = kSC[2], P2 = kSC[3], P3 = kSC[4];
+  const double S1 = kSC[5], S2 = kSC[6], S3 = kSC[7], S4 = kSC[8], S5 = kSC[9], S6 = kSC[10];
+  const double C1 = kSC[11], C2 = kSC[12], C3 = kSC[13], C4 = kSC[14], C5 = kSC[15], C6 = kSC[16];
+  const double t = __fma_rn(x, kInvPio2, kMagic);
+  const double q = __dsub_rn(t, kMagic);  // nearest integer to x * 2/pi
+  const int n = __double2loint(t) & 3;    // quadrant
+  double r = __fma_rn(-q, P1, x);
+  r = __fma_rn(-q, P2, r);
+  r = __fma_rn(-q, P3, r);
+  const double z = __dmul_rn(r, r), v = __dmul_rn(z, r);
+  const double ps = __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, S6, S5), S4), S3), S2);
+  const double s = __fma_rn(v, __fma_rn(z, ps, S1), r);
+  const double pc =
+      __dmul_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, __fma_rn(z, C6, C5), C4), C3), C2), C1));
+  const double hz = __dmul_rn(0.5, z), w = __dsub_rn(1.0, hz);
+  const double c = __dadd_rn(w, __dadd_rn(__dsub_rn(__dsub_rn(1.0, w), hz), __dmul_rn(z, pc)));
+  const double so = (n & 1) ? c : s, co = (n & 1) ? s : c;
+  *sn = (n & 2) ? -so : so;
+  *cs = ((n + 1) & 2) ? -co : co;
+}
+
 __device__ __forceinline__ double2 polar1(double phi) {
   double s, c;
-  sincos(__dmul_rn(kTwoPi, phi), &s, &c);
+  sincos_lean(__dmul_rn(kSC[17], phi), &s, &c);
   return make_double2(c, s);
 }
 
@@ -502,6 +549,21 @@ void launch_k4(const DevK& k, dim3 grid, cudaStream_t st, const int* rows, int n
   }
 }
 
+// K5 with the register capacity the tallest block needs (taller blocks
+// return rank -1 from the kernel and are recomputed on the host).
+void launch_k5(int64_t max_m, unsigned grid, cudaStream_t st, double2* ws, const IdTask* tk, int ntasks, int kmax,
+               double eps, int rowid, double2* vals, int* rank, int* skel, int kcap) {
+  if (max_m <= 256) {
+    cuda_check(cudaFuncSetAttribute(k5_id<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(id_smem<8>())), "k5 smem attribute");
+    k5_id<8><<<grid, kIdWarps * 32, id_smem<8>(), st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
+  } else {
+    cuda_check(cudaFuncSetAttribute(k5_id<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(id_smem<16>())), "k5 smem attribute");
+    k5_id<16><<<grid, kIdWarps * 32, id_smem<16>(), st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
+  }
+}
+
 template <class T>
 T* upload(const T* h, size_t n, const char* what) {
   if (!h || n == 0) return nullptr;
@@ -835,6 +897,7 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   std::vector<IdTask> tk(static_cast<size_t>(ntasks));
   int64_t ws = 0, vals = 0;
   int kcap = 1;
+  int64_t max_m = 0;
   for (int64_t t = 0; t < ntasks; ++t) {
     const int64_t* q = tasks + 5 * t;
     if (q[1] <= 0 || q[3] <= 0 || q[0] < 0 || q[2] < 0 || q[0] + q[1] > n_row_ids || q[2] + q[3] > n_col_ids)
@@ -848,6 +911,7 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
     ws += m * n;
     vals += cap * n;
     kcap = std::max<int>(kcap, static_cast<int>(cap));
+    max_m = std::max(max_m, m);
   }
   out.kcap = kcap;
   out.skel.assign(static_cast<size_t>(ntasks * kcap), 0);
@@ -880,12 +944,9 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
       launch_k3_ws<false>(I.k, nt, I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
     cuda_check(cudaGetLastError(), "k3_sample_ws launch");
     I.end();
-    cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
-               "k5 smem attribute");
     I.begin(5, 0);
-    k5_id<<<nt, kIdWarps * 32, kIdSmem, I.stream>>>(
-        P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0,
-        P.d_vals, P.d_rank, P.d_skel, kcap);
+    launch_k5(max_m, nt, I.stream, P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)),
+              eps, rowid ? 1 : 0, P.d_vals, P.d_rank, P.d_skel, kcap);
     cuda_check(cudaGetLastError(), "k5_id launch");
     I.end();
     if (timing) cuda_check(cudaStreamSynchronize(I.stream), "ID kernels");
@@ -1024,12 +1085,11 @@ extern "C" int midbf_cid_batch(const double* blocks, const int64_t* dims, int64_
     IdPool::grow(P.d_skel, P.skel_cap, nblocks * kcap, false, "cudaMalloc skeletons");
     cuda_check(cudaMemcpy(P.d_ws, blocks, ws * sizeof(double2), cudaMemcpyHostToDevice), "ID blocks H2D");
     IdTask* d_tk = upload(tk.data(), tk.size(), "upload ID tasks");
-    cuda_check(cudaFuncSetAttribute(k5_id, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kIdSmem)),
-               "k5 smem attribute");
     const unsigned nt = static_cast<unsigned>(nblocks);
-    k5_id<<<nt, kIdWarps * 32, kIdSmem>>>(
-        P.d_ws, d_tk, static_cast<int>(nblocks), static_cast<int>(std::max<int64_t>(k_max, 0)), eps, 0, P.d_vals,
-        P.d_rank, P.d_skel, static_cast<int>(kcap));
+    int64_t max_m = 0;
+    for (const IdTask& q : tk) max_m = std::max<int64_t>(max_m, q.m);
+    launch_k5(max_m, nt, nullptr, P.d_ws, d_tk, static_cast<int>(nblocks), static_cast<int>(std::max<int64_t>(k_max, 0)),
+              eps, 0, P.d_vals, P.d_rank, P.d_skel, static_cast<int>(kcap));
     const cudaError_t e = cudaGetLastError();
     std::vector<int> r(static_cast<size_t>(nblocks)), sk(static_cast<size_t>(nblocks * kcap), 0);
     if (e == cudaSuccess) {

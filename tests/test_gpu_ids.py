@@ -24,7 +24,9 @@ def _decaying(rng, m, n, rate):
 @pytest.mark.parametrize("k_max,eps", [(30, 1e-9), (30, 0.0), (0, 1e-6), (8, 1e-12)])
 def test_cid_batch_matches_oracle(gpu, k_max, eps):
     rng = np.random.default_rng(7)
-    shapes = [(150, 64), (150, 120), (40, 30), (7, 200), (256, 512), (1, 5), (64, 1)]
+    # up to 256 rows: k5_id<8>; 257..512 rows (3D blocks, cfg3 320 x 512): k5_id<16>
+    shapes = [(150, 64), (150, 120), (40, 30), (7, 200), (256, 512), (1, 5), (64, 1),
+              (320, 512), (512, 320), (300, 10)]
     blocks = [_decaying(rng, m, n, 0.55) for m, n in shapes]
     got = M.cid_batch(blocks, k_max, eps)
     for B, g in zip(blocks, got):
@@ -32,7 +34,10 @@ def test_cid_batch_matches_oracle(gpu, k_max, eps):
         assert g is not None
         gsk, gV, gk = g
         assert gk == k and np.array_equal(gsk, sk)
-        assert np.abs(gV - V).max() <= 1e-9 * max(1.0, np.abs(V).max())
+        # R11^-1 amplifies rounding by ~1/sigma_k = 0.55^-k (summation
+        # orders differ between the warp reductions and the host loops)
+        tol = max(1e-9, 1e-14 / 0.55 ** k)
+        assert np.abs(gV - V).max() <= tol * max(1.0, np.abs(V).max())
         if k:  # the ID reproduces the block from its skeleton columns
             assert rel(B[:, gsk] @ gV, B) <= 10 * 0.55 ** k + 1e-12
 
@@ -40,7 +45,7 @@ def test_cid_batch_matches_oracle(gpu, k_max, eps):
 def test_cid_batch_hands_back_what_it_cannot_finish(gpu):
     rng = np.random.default_rng(8)
     rank2 = rng.standard_normal((60, 2)) @ rng.standard_normal((2, 50)) + 0j  # tiny diagonals inside k_max
-    big = rng.standard_normal((300, 10)) + 0j                                  # m > 256
+    big = rng.standard_normal((600, 10)) + 0j                                  # m > 512
     zero = np.zeros((20, 30), complex)
     out = M.cid_batch([rank2, big, zero, _decaying(rng, 30, 40, 0.5)], 10, 1e-9)
     assert out[0] is None and out[1] is None  # host fallback cases

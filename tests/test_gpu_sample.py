@@ -141,3 +141,19 @@ def test_factorize_reports_kernel_times(gpu):
     ks = F.kernel_stats()
     assert ks["k3_launches"] >= 3 and ks["k3_entries"] == F.sample_stats()[0]
     assert ks["k3_seconds"] > 0 and ks["k5_launches"] >= 1 and ks["k5_seconds"] > 0
+
+
+def test_sincos_over_argument_ranges(gpu):
+    """The sampler's lean sincos (Cody-Waite + fdlibm kernels, |2 pi Phi| <
+    1e6) and its CUDA-sincos fallback beyond, against glibc: phases from
+    1e-3 to 1e7, both signs, and near multiples of 1/4 (reduction edges)."""
+    rng = np.random.default_rng(31)
+    mags = np.concatenate([10.0 ** rng.uniform(-3, 7, 3000), rng.integers(-4000, 4000, 1000) / 4.0])
+    X = np.ones((1, 1))
+    Om = (mags * rng.choice([-1.0, 1.0], mags.size)).reshape(-1, 1)
+    Om[-1000:, 0] += rng.uniform(-1e-12, 1e-12, 1000)
+    Ko, Km = O.Kernel(O.KIND_NUFFT, X=X, Omega=Om), M.Kernel(M.KIND_NUFFT, X=X, Omega=Om)
+    cols = np.arange(Om.shape[0])
+    (Bk,) = Km.sample([np.array([0])], [cols])
+    ref = Ko.entries(np.zeros_like(cols), cols)
+    assert np.abs(Bk[0] - ref).max() <= 4e-15
