@@ -14,7 +14,7 @@
 // to the host's serial sums).  The phase fix of R's rows is skipped: it
 // cancels in R11^-1 R12 and leaves |R_ii| unchanged.
 //
-// One CTA of kIdWarps warps per block: rows distributed over lanes (row i
+// One CTA of kIdWarps (8 for m <= 256, 4 above) warps per block: rows distributed over lanes (row i
 // -> lane i % 32, register slot i / 32; m <= 32 * kIdRows), squared norms,
 // the column permutation and the Householder vector in shared memory
 // (n <= kIdCols).  Per step warp 0 picks the pivot and builds the reflector,
@@ -35,7 +35,6 @@ namespace midbf::dev {
 // 150 x 120 at cfg1), k5_id<16> m <= 512 (3D blocks, 320 x 512 at cfg3).
 constexpr int kIdRowsMax = 16;
 constexpr int kIdCols = 512;           // n <= 512
-constexpr int kIdWarps = 4;            // warps cooperating on one block
 template <int ROWS>
 constexpr size_t id_smem() {
   return size_t(kIdCols) * (8 + 8 + 4) + size_t(32 * ROWS) * 16 + 64;
@@ -71,7 +70,7 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // ranks[t] = k (or -1: recompute on the host); skel[t * kcap + i] = perm[i];
 // out + ooff: V (k x n, ld k) for a column ID, W = V^T (n x k, ld n) for a row
 // ID (`rowid`: the workspace holds the transposed block).
-template <int kIdRows>
+template <int kIdRows, int kIdWarps>  // register slots per lane, warps cooperating on one block
 __global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
                                                        int ntasks, int kmax, double eps, int rowid,
                                                        double2* __restrict__ out, int* __restrict__ ranks,

@@ -304,7 +304,17 @@ struct Ops<MIDBF_KERNEL_NUFFT> {
 // width <= kMaxW doubles per point (FIO 3D: 6; low-rank / x.xi: r, dim).
 constexpr int kMCap = 512, kNTile = 128, kMaxW = 8;
 constexpr int64_t kTaskEntries = 8192;  // entries per CTA of k3_sample (sample_blocks sub-tasks)
-constexpr size_t kStageSmem = static_cast<size_t>(kMCap + kNTile) * kMaxW * sizeof(double);  // 40 KB
+// Staging width per kind (max of row / column operands): shared memory per
+// CTA 20 KB for FIO 2D, 30 KB for 3D, 40 KB otherwise -- small enough for 8
+// CTAs (all 64 warps) per SM with the FIO kernels.
+template <int KIND>
+__host__ __device__ constexpr int stage_w() {
+  return KIND == MIDBF_KERNEL_FIO2D ? 4 : KIND == MIDBF_KERNEL_FIO3D ? 6 : kMaxW;
+}
+template <int KIND>
+constexpr size_t stage_smem() {
+  return static_cast<size_t>(kMCap + kNTile) * stage_w<KIND>() * sizeof(double);
+}
 
 __host__ __device__ inline bool stageable(int kind, int rank, int dim) {
   switch (kind) {
@@ -328,7 +338,7 @@ __device__ __forceinline__ void fill_staged(const DevK& k, const int* __restrict
   using O = Ops<KIND>;
   const int m = TRANS ? nc : nr, n = TRANS ? nr : nc;
   double* sM = sm;                 // m-side operands, stride kMCap
-  double* sN = sm + kMCap * kMaxW; // n-side operands, stride kNTile
+  double* sN = sm + kMCap * stage_w<KIND>();  // n-side operands, stride kNTile
   for (int r = threadIdx.x; r < m; r += blockDim.x) {
     if (TRANS)
       O::col(k, cid[co + r], sM + r, kMCap);
@@ -490,16 +500,16 @@ void launch_k3(const DevK& k, unsigned grid, cudaStream_t st, const int* tasks, 
   }
   switch (k.kind) {
     case MIDBF_KERNEL_FIO2D:
-      k3_sample_s<MIDBF_KERNEL_FIO2D><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      k3_sample_s<MIDBF_KERNEL_FIO2D><<<grid, 256, stage_smem<MIDBF_KERNEL_FIO2D>(), st>>>(k, tasks, rid, cid, out);
       break;
     case MIDBF_KERNEL_FIO3D:
-      k3_sample_s<MIDBF_KERNEL_FIO3D><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      k3_sample_s<MIDBF_KERNEL_FIO3D><<<grid, 256, stage_smem<MIDBF_KERNEL_FIO3D>(), st>>>(k, tasks, rid, cid, out);
       break;
     case MIDBF_KERNEL_LOWRANK:
-      k3_sample_s<MIDBF_KERNEL_LOWRANK><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      k3_sample_s<MIDBF_KERNEL_LOWRANK><<<grid, 256, stage_smem<MIDBF_KERNEL_LOWRANK>(), st>>>(k, tasks, rid, cid, out);
       break;
     default:
-      k3_sample_s<MIDBF_KERNEL_NUFFT><<<grid, 256, kStageSmem, st>>>(k, tasks, rid, cid, out);
+      k3_sample_s<MIDBF_KERNEL_NUFFT><<<grid, 256, stage_smem<MIDBF_KERNEL_NUFFT>(), st>>>(k, tasks, rid, cid, out);
       break;
   }
 }
@@ -513,16 +523,16 @@ void launch_k3_ws(const DevK& k, unsigned grid, cudaStream_t st, const int4* rc,
   }
   switch (k.kind) {
     case MIDBF_KERNEL_FIO2D:
-      k3_sample_ws_s<MIDBF_KERNEL_FIO2D, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      k3_sample_ws_s<MIDBF_KERNEL_FIO2D, TRANS><<<grid, 256, stage_smem<MIDBF_KERNEL_FIO2D>(), st>>>(k, rc, tk, rid, cid, ws);
       break;
     case MIDBF_KERNEL_FIO3D:
-      k3_sample_ws_s<MIDBF_KERNEL_FIO3D, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      k3_sample_ws_s<MIDBF_KERNEL_FIO3D, TRANS><<<grid, 256, stage_smem<MIDBF_KERNEL_FIO3D>(), st>>>(k, rc, tk, rid, cid, ws);
       break;
     case MIDBF_KERNEL_LOWRANK:
-      k3_sample_ws_s<MIDBF_KERNEL_LOWRANK, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      k3_sample_ws_s<MIDBF_KERNEL_LOWRANK, TRANS><<<grid, 256, stage_smem<MIDBF_KERNEL_LOWRANK>(), st>>>(k, rc, tk, rid, cid, ws);
       break;
     default:
-      k3_sample_ws_s<MIDBF_KERNEL_NUFFT, TRANS><<<grid, 256, kStageSmem, st>>>(k, rc, tk, rid, cid, ws);
+      k3_sample_ws_s<MIDBF_KERNEL_NUFFT, TRANS><<<grid, 256, stage_smem<MIDBF_KERNEL_NUFFT>(), st>>>(k, rc, tk, rid, cid, ws);
       break;
   }
 }
@@ -553,15 +563,19 @@ void launch_k4(const DevK& k, dim3 grid, cudaStream_t st, const int* rows, int n
 // return rank -1 from the kernel and are recomputed on the host).
 void launch_k5(int64_t max_m, unsigned grid, cudaStream_t st, double2* ws, const IdTask* tk, int ntasks, int kmax,
                double eps, int rowid, double2* vals, int* rank, int* skel, int kcap) {
-  if (max_m <= 256) {
-    cuda_check(cudaFuncSetAttribute(k5_id<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(id_smem<8>())), "k5 smem attribute");
-    k5_id<8><<<grid, kIdWarps * 32, id_smem<8>(), st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
-  } else {
-    cuda_check(cudaFuncSetAttribute(k5_id<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(id_smem<16>())), "k5 smem attribute");
-    k5_id<16><<<grid, kIdWarps * 32, id_smem<16>(), st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
-  }
+  // Warps per block, measured (tools/gpu_k5exp.sh, K5 device ms per
+  // factorization): 2D cfg1 8 warps 12.8 vs 4 warps 15.9 ms; 3D cfg3 (k5_id<16>,
+  // 254 registers) 4 warps 73.3 vs 8 warps 76.3 ms.  Capping resident blocks
+  // per SM so the in-flight blocks fit L2 was slower (cfg1 19.6-21.3 ms).
+  auto go = [&](auto kern, size_t smem, int nthreads) {
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "k5 smem attribute");
+    kern<<<grid, nthreads, smem, st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
+  };
+  if (max_m <= 256)
+    go(k5_id<8, 8>, id_smem<8>(), 256);
+  else
+    go(k5_id<16, 4>, id_smem<16>(), 128);
 }
 
 template <class T>
@@ -1034,8 +1048,10 @@ void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel
   int* d_rows = upload(r.data(), r.size(), "upload rows");
   double2* d_f = upload(reinterpret_cast<const double2*>(f), static_cast<size_t>(I.ncols), "upload f");
   const int rb = static_cast<int>((nsel + 255) / 256);
+  // ~16 CTAs per SM; column ranges down to 64 columns, so that a 256-row
+  // eps_b sum (one row block) still fills the GPU
   const int64_t target = 148 * 16;
-  int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>((I.ncols + kTile - 1) / kTile, (target + rb - 1) / rb));
+  int64_t nsplit = std::max<int64_t>(1, std::min<int64_t>((I.ncols + 63) / 64, (target + rb - 1) / rb));
   nsplit = std::min<int64_t>(nsplit, 65535);
   const int64_t cps = (I.ncols + nsplit - 1) / nsplit;
   double2 *d_part = nullptr, *d_g = nullptr;

@@ -17,3 +17,7 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k3_
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r1_launches.log 2>&1; echo "launches rc=$?"
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k1_flow -s 5 -c 1 -f -o gpurun_out/r1_k1_flow python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r1_k1_ncu.log 2>&1; echo "k1 ncu rc=$?"
 fi
+if [ -n "$PROF" ]; then
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k4_direct_s' -c 1 -f -o gpurun_out/r1_k4 python tools/k3_bench.py cfg1 > gpurun_out/k4_full.log 2>&1; echo "ncu k4 rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:'k5_id' -s 1 -c 1 -f -o gpurun_out/r1_k5 python tools/k3_bench.py cfg1 > gpurun_out/k5_full.log 2>&1; echo "ncu k5 rc=$?"
+fi
