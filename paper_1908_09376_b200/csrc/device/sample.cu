@@ -73,11 +73,7 @@ __constant__ double kSC[18] = {
     -2.75573143513906633035e-07, 2.08757232129817482790e-09,  -1.13596475577881948265e-11,
     6.283185307179586476925286766559};  // 2 pi (the reference's product 2*pi*Phi)
 
-__device__ __forceinline__ void sincos_lean(double x, double* sn, double* cs) {
-  if (!(fabs(x) < 1.0e6)) {
-    sincos(x, sn, cs);
-    return;
-  }
+__device__ __forceinline__ void sincos_fast(double x, double* sn, double* cs) {  // |x| < 1e6
   const double kInvPio2 = kSC[0], kMagic = kSC[1], P1 = kSC[2], P2 = kSC[3], P3 = kSC[4];
   const double S1 = kSC[5], S2 = kSC[6], S3 = kSC[7], S4 = kSC[8], S5 = kSC[9], S6 = kSC[10];
   const double C1 = kSC[11], C2 = kSC[12], C3 = kSC[13], C4 = kSC[14], C5 = kSC[15], C6 = kSC[16];
@@ -97,6 +93,30 @@ __device__ __forceinline__ void sincos_lean(double x, double* sn, double* cs) {
   const double so = (n & 1) ? c : s, co = (n & 1) ? s : c;
   *sn = (n & 2) ? -so : so;
   *cs = ((n + 1) & 2) ? -co : co;
+}
+
+__device__ __forceinline__ void sincos_lean(double x, double* sn, double* cs) {
+  if (fabs(x) < 1.0e6)
+    sincos_fast(x, sn, cs);
+  else
+    sincos(x, sn, cs);
+}
+
+// Two independent arguments in one straight-line block, so that the two
+// Horner chains interleave (the single-entry loop stalled on DFMA latency:
+// "wait" 49% of the warp samples in r1_k3).
+__device__ __forceinline__ void polar1x2(double phi0, double phi1, double2* e0, double2* e1) {
+  const double x0 = __dmul_rn(kSC[17], phi0), x1 = __dmul_rn(kSC[17], phi1);
+  double s0, c0, s1, c1;
+  if (fabs(x0) < 1.0e6 && fabs(x1) < 1.0e6) {
+    sincos_fast(x0, &s0, &c0);
+    sincos_fast(x1, &s1, &c1);
+  } else {
+    sincos_lean(x0, &s0, &c0);
+    sincos_lean(x1, &s1, &c1);
+  }
+  *e0 = make_double2(c0, s0);
+  *e1 = make_double2(c1, s1);
 }
 
 __device__ __forceinline__ double2 polar1(double phi) {
@@ -434,12 +454,19 @@ __global__ void __launch_bounds__(256) k4_direct_s(DevK k, const int* __restrict
     }
     __syncthreads();
     if (r < nsel) {
-      for (int q = 0; q < cn; ++q) {
-        const double2 e = polar1(O::phase(k, sR + threadIdx.x, kT, sC + q, kT));
-        const double2 x = fs[q];
+      auto mac = [&](double2 e, double2 x) {  // acc += K * f, std::complex's product (no fma)
         ar = __dadd_rn(ar, __dsub_rn(__dmul_rn(e.x, x.x), __dmul_rn(e.y, x.y)));
         ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(e.x, x.y), __dmul_rn(e.y, x.x)));
+      };
+      int q = 0;
+      for (; q + 1 < cn; q += 2) {  // two entries' sincos interleaved, accumulated in column order
+        double2 e0, e1;
+        polar1x2(O::phase(k, sR + threadIdx.x, kT, sC + q, kT), O::phase(k, sR + threadIdx.x, kT, sC + q + 1, kT),
+                 &e0, &e1);
+        mac(e0, fs[q]);
+        mac(e1, fs[q + 1]);
       }
+      if (q < cn) mac(polar1(O::phase(k, sR + threadIdx.x, kT, sC + q, kT)), fs[q]);
     }
   }
   if (r < nsel) partial[static_cast<int64_t>(blockIdx.y) * nsel + r] = make_double2(ar, ai);
