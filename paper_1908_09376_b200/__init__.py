@@ -249,7 +249,7 @@ class DevicePlan:
             self._h = None
 
     def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3,
-                  compress=True):
+                  compress=True, lite=False):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
@@ -257,9 +257,15 @@ class DevicePlan:
         layout 0 (4 warp pairs x 3 x 16 KB), 1 (8 x 2 x 8 KB), 3 chosen
         by the plan's size (default); 2 is retired and runs 1.  compress: k1_flow
         streams the identity-compressed panels (unit rows / columns of the ID
-        blocks gathered from x instead)."""
+        blocks gathered from x instead).  lite: the dense-only k1_flow
+        (True), the compressed one (False), or chosen by the plan's size
+        (None: dense-only below 200 MB of panels, the plan's initial setting)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
+        if lite is True:
+            f |= 1024
+        elif lite is False and compress:
+            f |= 65536
         _check(lib().midbf_plan_set_flags(self._h, f))
 
     def launches(self, nrhs=1, transpose=False):

@@ -283,14 +283,14 @@ __device__ __forceinline__ void store_x_regs(const StripCtx& c, const double2* v
 // gathers its entries (lane-strided over the flattened panel columns) and
 // polls until none is a sentinel; no warp-collective ops inside, so the
 // producer's lane 0 can run the TMA issue loop concurrently.
-template <int NS>  // stager lanes
+template <int NS, bool CMP>  // stager lanes, identity-compressed records possible
 __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst, int sl) {
   constexpr int kPer = (kXWin + NS - 1) / NS;
   int idx[kPer];
 #pragma unroll
   for (int i = 0; i < kPer; ++i) idx[i] = -1;
   int cb = 0;
-  const bool mapped = c.mapped != 0;
+  const bool mapped = CMP && c.mapped != 0;
   for (int j = 0; j < c.s.nseg; ++j) {
     const int n = c.g[j].n, x0 = c.g[j].x0;
 #pragma unroll
@@ -394,7 +394,9 @@ struct FlowCfg {
 // full and HBM keeps streaming while the consumer is stalled.
 // PROF: per-warp clock64 phase timers (experiment builds only), written to
 // P.prof[(blockIdx.x * 2*FW + warp) * 16 + phase].
-template <int FW, int FS, int SLOT, bool PROF = false>
+// CMP = false: dense strip records only (no identity-compression code on the
+// strips' critical path; small, latency-bound plans, see plan.cu flow_lite).
+template <int FW, int FS, int SLOT, bool PROF = false, bool CMP = true>
 __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_constant__ FlowParams P) {
   using namespace flowdev;
   using Cfg = FlowCfg<FW, FS, SLOT>;
@@ -482,8 +484,8 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
-        FLOW_T(13, stage_x<NS>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
-        if (kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
+        FLOW_T(13, stage_x<NS, CMP>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
+        if (CMP && kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
           // (separate stager warps only; with the in-warp stager of FW > 4
           // the consumers sum in place)
           __syncwarp(mask);
@@ -619,8 +621,8 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       for (int j = 0; j < nseg; ++j) {
         const int n = C.g[j].n;
         // compressed panels: hc rows (this panel's non-unit rows, in order)
-        const int hc = C.g[j].hc;
-        const unsigned urows = C.g[j].urows;
+        const int hc = CMP ? C.g[j].hc : h;
+        const unsigned urows = CMP ? C.g[j].urows : 0u;
         const bool live = row < h && !((urows >> row) & 1u);
         const int prow = __popc(~urows & below);  // row within the streamed panel
         const int cpc = chunk_cols_for(hc, SLOT);
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             if (w0 != win) {
               __syncwarp();
               const int cnt = min(kXWin, n - w0 * kXWin);
-              if (C.mapped == 2)
+              if (CMP && C.mapped == 2)
                 gather_mapped(xin, C.g[j].x0, P.wmap + C.wbase + cb + w0 * kXWin, cnt, xcur, lane);
               else
                 gather_range(xin, io.xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
@@ -693,11 +695,11 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
-      if (kSep && C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
+      if (CMP && kSep && C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
         const double2 t = asum[(k & 1) * 32 + row];
         yr += t.x;
         yi += t.y;
-      } else if (C.mapped == 1 && row < h) {  // identity parts: one staged entry per (panel, add row)
+      } else if (CMP && C.mapped == 1 && row < h) {  // identity parts: one staged entry per (panel, add row)
         for (int j = 0; j < nseg; ++j) {
           const unsigned a = C.g[j].adds;
           if ((a >> row) & 1u) {
@@ -706,7 +708,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             yi += t.y;
           }
         }
-      } else if (C.mapped == 2 && row < h && cpar == 0) {  // wide strips: read (and poll) the entry itself
+      } else if (CMP && C.mapped == 2 && row < h && cpar == 0) {  // wide strips: read (and poll) the entry itself
         for (int j = 0; j < nseg; ++j) {
           const unsigned a = C.g[j].adds;
           if ((a >> row) & 1u) {

@@ -151,6 +151,9 @@ int flow_setup(int num_sms) {
   cuda_check(cudaFuncSetAttribute(k1_flow<FW, FS, SLOT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)),
              "flow smem attribute");
+  cuda_check(cudaFuncSetAttribute(k1_flow<FW, FS, SLOT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "flow smem attribute");
   int per_sm = 0;
   cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_flow<FW, FS, SLOT>, flow_threads<FW>(), smem),
              "occupancy");
@@ -169,7 +172,7 @@ int k2flow_setup(int num_sms) {
 }
 
 template <int FW, int FS, int SLOT>
-void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
+void flow_launch(FlowParams& P, int grid, cudaStream_t stream, bool lite) {
   P.nwarps = grid * FW;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid), 1, 1);
@@ -183,6 +186,8 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream) {
   cfg.numAttrs = 1;
   if (P.prof)
     cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT, true>, P), "k1_flow launch");
+  else if (lite)
+    cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT, false, false>, P), "k1_flow launch");
   else
     cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT>, P), "k1_flow launch");
 }
@@ -990,10 +995,28 @@ int Plan::flow_variant(int d) const {
   const int v = static_cast<int>((flags >> 4) & 3u);
   if (v != 3) return v;
   int64_t bytes = 0;
-  const bool dense = !dir[d].d_fctx || (flags & 512u);
+  const bool dense = flow_dense(d);
   for (const auto& st : dir[d].stages) bytes += dense ? st.payload_bytes : st.flow_bytes;
   return bytes > (int64_t{512} << 20) ? 1 : 0;
 }
+
+// Dense-only k1_flow (no identity-compression code on the strips' critical
+// path) for small plans (< 200 MB of panels), or with flag bit 10 (bit 16:
+// never): the extra per-strip work of
+// the compressed kernel costs more than the bytes it saves when each warp pair
+// owns at most a strip or two per stage (measured).
+bool Plan::flow_lite(int d) const {
+  if (flags & 65536u) return false;  // bit 16: always the compressed kernel
+  if (flags & 1024u) return true;
+  int64_t bytes = 0;
+  for (const auto& st : dir[d].stages) bytes += st.payload_bytes;
+  // measured (tools/gpu_lite.sh, us per apply, default | dense-only |
+  // compressed): cfg0 7.6 MB 17.0 | 16.9 | 19.2, cfg1_unitxi 145 MB
+  // 37.0 (dense-only) vs 40.2, cfg1 358 MB 62.5 (dense-only) vs 55.2
+  return bytes < (int64_t{200} << 20);
+}
+
+bool Plan::flow_dense(int d) const { return !dir[d].d_fctx || (flags & 512u) || flow_lite(d); }
 
 // Up to kFlowColumns right-hand sides run k1_flow once per column: at cfg1 a
 // column costs ~66 us, the narrowest DMMA slice (16 wide) ~155 us.
@@ -1031,7 +1054,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   const int variant = flow_variant(d);
   FlowParams P{};
   // bit 9: dense panels (identity compression off, A/B experiments)
-  P.ctxs = static_cast<const StripCtx*>((D.d_fctx && !(flags & 512u)) ? D.d_fctx : D.d_ctx);
+  const bool lite = flow_lite(d);
+  P.ctxs = static_cast<const StripCtx*>(flow_dense(d) ? D.d_ctx : D.d_fctx);
   P.strips = D.d_strips;
   P.segs = D.d_segs;
   P.arena = D.d_arena;
@@ -1058,10 +1082,10 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   switch (variant) {
     case 1:
     case 2:  // retired variant: runs variant 1
-      flow_launch<8, 2, 8192>(P, flow_grid[1], stream);
+      flow_launch<8, 2, 8192>(P, flow_grid[1], stream, lite);
       break;
     default:
-      flow_launch<4, 3, 16384>(P, flow_grid[0], stream);
+      flow_launch<4, 3, 16384>(P, flow_grid[0], stream, lite);
   }
 }
 

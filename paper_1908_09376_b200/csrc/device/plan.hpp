@@ -141,6 +141,8 @@ class Plan {
   int64_t launches_per_apply(int d, int64_t nrhs) const;
   bool flow_ok(int d, int64_t nrhs) const;
   int flow_variant(int d) const;
+  bool flow_lite(int d) const;   // k1_flow without identity-compression code (dense records)
+  bool flow_dense(int d) const;  // k1_flow streams the dense panels
   bool k2_ok(int d, int64_t nrhs) const;
   bool k2flow_ok(int d, int64_t nrhs) const;
   int k2flow_grid[3] = {0, 0, 0};  // persistent CTAs of k2_flow<1 | 2 | 4> (16 / 32 / 64-wide tiles)

@@ -305,12 +305,13 @@ extern "C" int midbf_plan_stages(midbf_plan_t plan, int transpose, int64_t* out,
 }
 
 // Panel bytes k1_flow streams per stage (identity-compressed unless flag bit
-// 9 is set): out[s], application order.
+// 9 is set or the plan runs the dense-only k1_flow, Plan::flow_lite): out[s],
+// application order.
 extern "C" int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* out, int64_t cap) {
   return guard([&] {
     const Plan& p = *plan->p;
     const auto& D = p.dir[transpose ? 1 : 0];
-    const bool dense = !D.d_fctx || (p.flags & 512u);
+    const bool dense = p.flow_dense(transpose ? 1 : 0);
     int64_t s = 0;
     for (const auto& st : D.stages) {
       if (s >= cap) break;

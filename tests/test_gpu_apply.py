@@ -124,6 +124,7 @@ def test_identity_compression(pair, variant):
     bytes than the stored factor whenever an ID block has any, and the same
     result as the dense panels and the oracle, both directions."""
     name, K, Fo, Fm, plan = pair
+    plan.set_flags()  # the compressed kernel (small plans default to the dense-only one)
     stored = sum(s[1] for s in plan.stages())
     streamed = sum(plan.flow_bytes())
     assert 0 < streamed <= stored
@@ -137,9 +138,13 @@ def test_identity_compression(pair, variant):
         plan.set_flags(variant=variant, compress=False)
         assert sum(plan.flow_bytes()) == stored
         a0, b0, c0 = plan.apply(f), plan.apply(g, transpose=True), plan.apply(F48)
+        plan.set_flags(variant=variant, lite=True)  # dense-only k1_flow
+        assert sum(plan.flow_bytes()) == stored
+        a1, b1 = plan.apply(f), plan.apply(g, transpose=True)
     finally:
         plan.set_flags()
     assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14 and rel(c, c0) <= 1e-14
+    assert np.array_equal(a1, a0) and np.array_equal(b1, b0)  # same dense panels, same order
     assert rel(a, Fo.apply(f)) <= TOL
     assert rel(b, Fo.apply_transpose(g)) <= TOL
     assert rel(c, Fo.apply(F48)) <= TOL
@@ -163,6 +168,7 @@ def test_wide_strip_identity_compression(wide3d):
     (kept columns through a global map, identity adds read from x itself);
     permutation factors stream nothing.  Every layout, both directions."""
     Fo, plan = wide3d
+    plan.set_flags()  # the compressed kernel
     stages, fb = plan.stages(), plan.flow_bytes()
     assert fb[0] == 0 and fb[-1] == 0  # V^1 / U^1 are permutations
     assert fb[1] < stages[1][1] and fb[3] < stages[3][1]  # the wide ID stages

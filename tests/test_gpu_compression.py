@@ -122,6 +122,7 @@ def adversarial(gpu):
 
 def test_streams_less_than_stored(adversarial):
     plan, A, fs = adversarial
+    plan.set_flags()  # the compressed kernel (small plans default to the dense-only one)
     stored = [s[1] for s in plan.stages()]
     fb = plan.flow_bytes()
     assert fb[0] < stored[0] and fb[1] < stored[1] and fb[2] < stored[2]  # wide, V, U
