@@ -170,9 +170,28 @@ __device__ __forceinline__ bool is_sentinel(const double2& v) {
 __device__ __forceinline__ double unsentinel(double v) {
   return __double_as_longlong(v) == -1ll ? __longlong_as_double(0x7ff8000000000000ll) : v;
 }
+// Spin on one entry until it is not the sentinel (loop in PTX, strong loads).
+__device__ __forceinline__ double2 poll_cg(const double2* p) {
+  unsigned long long a, b;
+  asm volatile(
+      "{\n .reg .pred s0, s1;\n"
+      "POLL_CG_AGAIN:\n"
+      " ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];\n"
+      " setp.eq.s64 s0, %0, -1;\n"
+      " setp.eq.or.s64 s1, %1, -1, s0;\n"
+      " @s1 bra POLL_CG_AGAIN;\n}"
+      : "=l"(a), "=l"(b)
+      : "l"(p)
+      : "memory");
+  return make_double2(__longlong_as_double(static_cast<long long>(a)), __longlong_as_double(static_cast<long long>(b)));
+}
 __device__ __forceinline__ double2 ld_cg(const double2* p) {
   double2 v;
-  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  // A strong (relaxed, GPU-scope) load: the polls re-read it until another
+  // CTA's store lands.  With a weak ld.global.cg the compiler may treat a
+  // retry as redundant: ptxas reduced the wide strips' identity-add poll to
+  // a single load and a sentinel leaked into y (nufft3d transpose, variant 0).
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
   return v;
 }
 // Gather cnt entries from x0 (stage 0 through xperm, never polled: user f),
@@ -713,8 +732,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
           const unsigned a = C.g[j].adds;
           if ((a >> row) & 1u) {
             const int xi = C.g[j].x0 + __ldg(P.wmap + C.wbase + C.nkept + C.g[j].aoff + __popc(a & below));
-            double2 t = ld_cg(xin + xi);
-            while (is_sentinel(t)) t = ld_cg(xin + xi);
+            const double2 t = poll_cg(xin + xi);
             yr += t.x;
             yi += t.y;
           }

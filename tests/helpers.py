@@ -27,6 +27,11 @@ def cvec(n, seed, cols=None):
 
 
 def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    for side, v in (("result", a), ("expected", b)):
+        bad = np.flatnonzero(~np.isfinite(v))
+        if bad.size:  # name the side and the entries, not just a NaN norm
+            raise AssertionError(f"{side} has {bad.size} non-finite entries of {v.size}, first {bad[:8].tolist()}")
     nb = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 

@@ -370,3 +370,29 @@ def test_factorization_applies_from_threads(gpu):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+def test_flow_polls_survive_flag_switches(pair):
+    """Regression: the wide strips' identity adds poll the previous stage's
+    output.  With a weak load the retry loop was compiled away and, about
+    every other switch back to variant 0, a not-yet-written (sentinel) entry
+    leaked into y (nufft3d transpose).  Alternate layouts and kernels many
+    times; every result must equal the first bitwise."""
+    name, K, Fo, Fm, plan = pair
+    f, g = cvec(Fo.ncols, 27), cvec(Fo.nrows, 28)
+    want = {}
+    try:
+        for it in range(24):
+            for kw in (dict(variant=0), dict(variant=1), dict(variant=1, lite=True), dict(variant=0, lite=True)):
+                plan.set_flags(**kw)
+                for tr, v in ((False, f), (True, g)):
+                    got = plan.apply(v, transpose=tr)
+                    assert np.isfinite(got).all(), (it, kw, tr)
+                    key = (tr, kw["variant"], kw.get("lite", False))
+                    if key not in want:
+                        want[key] = got
+                        assert rel(got, Fo.apply_transpose(g) if tr else Fo.apply(f)) <= TOL
+                    else:  # run-to-run bitwise (fixed summation order per strip)
+                        assert np.array_equal(got, want[key]), (it, kw, tr)
+    finally:
+        plan.set_flags()
