@@ -258,8 +258,10 @@ class DevicePlan:
         by the plan's size (default); 2 is retired and runs 1.  compress: k1_flow
         streams the identity-compressed panels (unit rows / columns of the ID
         blocks gathered from x instead).  lite: the dense-only k1_flow
-        (True), the compressed one (False), or chosen by the plan's size
-        (None: dense-only below 200 MB of panels, the plan's initial setting)."""
+        (True), the compressed one (False, the default of this call, so
+        set_flags() alone selects the compressed kernel at every size), or
+        chosen by the plan's size (None: dense-only below 200 MB of panels,
+        the plan's initial setting and the bench's default flags 63)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         if lite is True:
