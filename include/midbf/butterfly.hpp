@@ -53,6 +53,22 @@ struct Config {  // :46-51
 
 struct DevicePlanCache;  // opaque: device arenas built from this object
 
+// Holder of a Factorization's device-plan cache.  A copy starts empty (the
+// copy builds its own plan on its first apply), so editing either object
+// after a copy never reaches the other's arenas; moves keep the cache
+// (the block buffers move with it).
+struct DevicePlanSlot {
+  std::shared_ptr<DevicePlanCache> p;
+  DevicePlanSlot() = default;
+  DevicePlanSlot(const DevicePlanSlot&) {}
+  DevicePlanSlot& operator=(const DevicePlanSlot&) {
+    p.reset();
+    return *this;
+  }
+  DevicePlanSlot(DevicePlanSlot&&) noexcept = default;
+  DevicePlanSlot& operator=(DevicePlanSlot&&) noexcept = default;
+};
+
 struct Factorization {  // :53-70
   Index nrows = 0;
   Index ncols = 0;
@@ -70,9 +86,12 @@ struct Factorization {  // :53-70
   double nnz_bound(double c = 4.0) const;
 
   // Device-plan cache (not part of the reference struct).  Built on the
-  // first apply; call invalidate_device_plan() after editing factors.
-  mutable std::shared_ptr<DevicePlanCache> device;
-  void invalidate_device_plan() const { device.reset(); }
+  // first apply and rebuilt when the block layout changes (blocks added,
+  // removed, reallocated or reshaped, perms resized); call
+  // invalidate_device_plan() after editing block VALUES in place.  Thread
+  // safe against concurrent applies (same lock as the cache lookup).
+  mutable DevicePlanSlot device;
+  void invalidate_device_plan() const;
 };
 
 // Reference overload: entries from a host callback (src/butterfly.cpp:708).

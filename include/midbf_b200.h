@@ -221,7 +221,20 @@ int midbf_plan_flow_bytes(midbf_plan_t plan, int transpose, int64_t* out, int64_
 /* Panel bytes (16 per entry) the multi-RHS DMMA kernel multiplies per apply on
  * 32- / 64-wide tiles: unit / zero columns of V-type ID strips skipped. */
 int midbf_plan_k2_bytes(midbf_plan_t plan, int transpose, int64_t* out);
+/* Kernel-path switches (plan.cu): bit0 PDL, bit1 L2 prefetch, bit2 graphs,
+ * bit3 k1_flow, bits4-5 k1_flow variant (3 = by size), bits6-8 / 14-15
+ * timing experiments (results invalid), bit9 dense panels, bit10 dense-only
+ * k1_flow, bit11 no DMMA, bit12 phase timers, bit13 per-stage DMMA, bit16
+ * always the compressed k1_flow.  A new plan starts at 0x3F. */
 int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags);
+int midbf_plan_get_flags(midbf_plan_t plan, unsigned* out);
+/* Kernel launches one apply of nrhs columns issues (1 k1_flow launch per
+ * column up to 2 RHS, 1 k2_flow launch per 64-RHS slice, else one per stage);
+ * the evidence behind bench.py's gpu_launches. */
+int midbf_plan_launches(midbf_plan_t plan, int transpose, int64_t nrhs, int64_t* out);
+/* Phase timers of the last k1_flow launch made with flag bit 12 (profiling
+ * builds/tools only): out holds n int64 counters. */
+int midbf_plan_flow_profile(midbf_plan_t plan, int64_t* out, int64_t n);
 
 /* Seeded inputs of the reference experiment (src/experiment.cpp:75-81). */
 int midbf_random_coefficients(int64_t n, uint64_t seed, double* out);

@@ -218,6 +218,7 @@ class DevicePlan:
         _check(lib().midbf_plan_info(handle, _ip(info)))
         (self.nrows, self.ncols, self.nfactors, self.total_nnz, self.arena_bytes, self.nstrips, self.directions,
          self.max_len) = (int(v) for v in info)
+        self._flags0 = self.get_flags()
 
     @classmethod
     def load(cls, path, directions=1):
@@ -229,8 +230,10 @@ class DevicePlan:
     def from_tables(cls, nrows, ncols, row_perm, col_perm, factors, directions=1):
         """factors: list of (rows, cols, blocks[nb,4], groups[ng,2], [M_b ...]) in product order."""
         shape = np.array([[f[0], f[1], len(f[2]), len(f[3])] for f in factors], dtype=np.int64).reshape(-1, 4)
-        blocks = np.ascontiguousarray(np.concatenate([np.asarray(f[2], np.int64).reshape(-1, 4) for f in factors]))
-        groups = np.ascontiguousarray(np.concatenate([np.asarray(f[3], np.int64).reshape(-1, 2) for f in factors]))
+        blocks = np.ascontiguousarray(np.concatenate([np.asarray(f[2], np.int64).reshape(-1, 4) for f in factors]
+                                                     + [np.zeros((0, 4), np.int64)]))
+        groups = np.ascontiguousarray(np.concatenate([np.asarray(f[3], np.int64).reshape(-1, 2) for f in factors]
+                                                     + [np.zeros((0, 2), np.int64)]))
         payload = np.concatenate([np.asarray(M, np.complex128).ravel(order="F") for f in factors for M in f[4]]
                                  + [np.zeros(1, np.complex128)])
         rp = np.ascontiguousarray(row_perm, dtype=np.int64)
@@ -249,7 +252,7 @@ class DevicePlan:
             self._h = None
 
     def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3,
-                  compress=True, lite=False):
+                  compress=True, lite=None):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
@@ -258,10 +261,10 @@ class DevicePlan:
         by the plan's size (default); 2 is retired and runs 1.  compress: k1_flow
         streams the identity-compressed panels (unit rows / columns of the ID
         blocks gathered from x instead).  lite: the dense-only k1_flow
-        (True), the compressed one (False, the default of this call, so
-        set_flags() alone selects the compressed kernel at every size), or
-        chosen by the plan's size (None: dense-only below 200 MB of panels,
-        the plan's initial setting and the bench's default flags 63)."""
+        (True), the compressed one (False), or chosen by the plan's size
+        (None, the default: dense-only below 200 MB of panels), so
+        set_flags() alone restores a new plan's flags (0x3F, the bench's
+        default flags 63)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         if lite is True:
@@ -269,6 +272,15 @@ class DevicePlan:
         elif lite is False and compress:
             f |= 65536
         _check(lib().midbf_plan_set_flags(self._h, f))
+
+    def get_flags(self):
+        out = C.c_uint()
+        _check(lib().midbf_plan_get_flags(self._h, C.byref(out)))
+        return out.value
+
+    def reset_flags(self):
+        """Restore the flags the plan was created with."""
+        _check(lib().midbf_plan_set_flags(self._h, self._flags0))
 
     def launches(self, nrhs=1, transpose=False):
         """Kernel launches one apply issues."""
@@ -304,15 +316,42 @@ class DevicePlan:
         _check(lib().midbf_apply_async(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))
 
     def apply(self, f, transpose=False, out=None, stream=0):
-        if hasattr(f, "data_ptr"):  # device tensor
+        nout = self.ncols if transpose else self.nrows
+        nin = self.nrows if transpose else self.ncols
+        if hasattr(f, "data_ptr"):  # device tensor: (n,) or (n, nrhs), complex128 on a CUDA device
+            import torch
+
+            if f.dtype != torch.complex128:
+                raise TypeError(f"apply: device operand must be complex128, got {f.dtype}")
+            if not f.is_cuda:
+                raise TypeError("apply: tensors must live on a CUDA device (host data: pass a numpy array)")
+            if f.dim() not in (1, 2):
+                raise ValueError("apply: operand must be a vector or an n x nrhs matrix")
+            if f.shape[0] != nin:
+                raise ValueError("input length does not match the factorization")  # src/butterfly.cpp:645
             nrhs = 1 if f.dim() == 1 else f.shape[1]
-            self.apply_ptr(f.data_ptr(), out.data_ptr(), nrhs, transpose, stream)
+            # the ABI reads and writes column-major n x nrhs
+            fc = f if f.dim() == 1 else f.t().contiguous().t()
+            if fc.dim() == 1:
+                fc = fc.contiguous()
+            shape = (nout,) if f.dim() == 1 else (nout, nrhs)
+            if out is None:
+                out = torch.empty(shape[::-1], dtype=torch.complex128, device=f.device).t() if f.dim() == 2 \
+                    else torch.empty(nout, dtype=torch.complex128, device=f.device)
+            if out.dtype != torch.complex128 or not out.is_cuda or tuple(out.shape) != shape:
+                raise ValueError(f"apply: out must be a complex128 CUDA tensor of shape {shape}")
+            colmajor = out.dim() == 1 and out.is_contiguous() or (
+                out.dim() == 2 and out.stride(0) == 1 and (out.stride(1) == nout or nrhs == 1))
+            dst = out if colmajor else torch.empty(shape[::-1], dtype=torch.complex128, device=f.device).t()
+            if dst.dim() == 1 and dst.stride(0) != 1:
+                dst = torch.empty(nout, dtype=torch.complex128, device=f.device)
+            self.apply_ptr(fc.data_ptr(), dst.data_ptr(), nrhs, transpose, stream)
+            if dst is not out:
+                out.copy_(dst)
             return out
         f = np.asarray(f, dtype=np.complex128)
         vec = f.ndim == 1
         F2 = np.asfortranarray(f.reshape(f.shape[0], -1))
-        nout = self.ncols if transpose else self.nrows
-        nin = self.nrows if transpose else self.ncols
         if F2.shape[0] != nin:
             raise ValueError("input length does not match the factorization")
         g = np.empty((nout, F2.shape[1]), dtype=np.complex128, order="F")

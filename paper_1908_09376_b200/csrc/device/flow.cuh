@@ -185,6 +185,14 @@ __device__ __forceinline__ double2 poll_cg(const double2* p) {
       : "memory");
   return make_double2(__longlong_as_double(static_cast<long long>(a)), __longlong_as_double(static_cast<long long>(b)));
 }
+// The matching strong store: every value another CTA polls is written with a
+// relaxed GPU-scope store, so each (store, poll) pair is a pair of morally
+// strong accesses and the protocol has no data race under the PTX memory
+// model (a weak st.global raced by ld.relaxed would be one; each 8-byte half
+// is single-copy atomic, which is all the sentinel test needs).
+__device__ __forceinline__ void st_signal(double2* p, double2 v) {
+  asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
 __device__ __forceinline__ double2 ld_cg(const double2* p) {
   double2 v;
   // A strong (relaxed, GPU-scope) load: the polls re-read it until another
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
     double2* x0 = P.stagebuf + par_off;
     for (int64_t i = i0; i < P.in_len; i += di) {
       const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
-      x0[i] = make_double2(unsentinel(v.x), unsentinel(v.y));
+      st_signal(x0 + i, make_double2(unsentinel(v.x), unsentinel(v.y)));
     }
   }
   // re-arm the other set for the next apply (nobody reads it during this
@@ -740,7 +748,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       // The stored value is the readiness signal of this row: never let a
       // result alias the "not yet written" sentinel.
-      FLOW_T(7, if (row < h && cpar == 0) yout[yidx] = make_double2(unsentinel(yr), unsentinel(yi)));
+      FLOW_T(7, if (row < h && cpar == 0) st_signal(yout + yidx, make_double2(unsentinel(yr), unsentinel(yi))));
       if (PROF && lane == 0 && C.s.seg0 < kProfStrips) {  // per-strip timeline (ns): ctx ready, x staged, stored
         long long* ts = P.prof + kProfStripBase + 3 * static_cast<int64_t>(C.s.seg0);
         ts[0] = static_cast<long long>(g_ctx);

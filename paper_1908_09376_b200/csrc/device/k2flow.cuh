@@ -104,6 +104,9 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -227,14 +230,22 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
                        "r"(load && !gather ? kval * 16u * kXs : 0u)
                        : "memory");
         __syncwarp();
-        while (!deps) {  // previous-stage producers of this strip's input rows
-          bool ready = true;
-          for (int l = 0; l < st.nseg; ++l) {
-            const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
-            for (int s = d0 + lane; s < d1 && ready; s += 32) ready = ld_acquire(P.done + s) >= target;
+        if (!deps) {
+          while (!deps) {  // previous-stage producers of this strip's input rows
+            bool ready = true;
+            for (int l = 0; l < st.nseg; ++l) {
+              const int d0 = __shfl_sync(0xffffffffu, s_d0, l), d1 = __shfl_sync(0xffffffffu, s_d1, l);
+              for (int s = d0 + lane; s < d1 && ready; s += 32) ready = ld_acquire(P.done + s) >= target;
+            }
+            deps = __all_sync(0xffffffffu, ready);
+            if (!deps) __nanosleep(64);
           }
-          deps = __all_sync(0xffffffffu, ready);
-          if (!deps) __nanosleep(64);
+          // The input rows were written by other CTAs' generic stores and
+          // published by their release adds; every lane's acquire is ordered
+          // before lane 0's copies by the warp barrier, and the proxy fence
+          // orders them before the TMA engine's (async proxy) reads.
+          __syncwarp();
+          fence_proxy_async_global();
         }
         if (load) {
           if (gather) {  // stage 0: lane & 15 = k, RHS (lane >> 4) + 2 i

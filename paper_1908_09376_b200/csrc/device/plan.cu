@@ -718,6 +718,11 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
   const int64_t nf = T.nfactors;
   if (nf > kMaxStages) throw std::invalid_argument("too many factors for one device plan");
   D.stages.clear();
+  if (nf == 0) {  // no factors: the reference's apply_impl is the two permutations (k0_permute)
+    D.in_len = d == 0 ? T.ncols : T.nrows;
+    D.built = true;
+    return;
+  }
   D.ncols_total = 0;
   std::vector<Strip> strips;
   std::vector<Seg> segs;
@@ -879,7 +884,44 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
                  static_cast<long long>(D.nstrips), static_cast<long long>(D.nsegs));
 }
 
+// Table checks the reference's apply relies on (src/butterfly.cpp:642-667):
+// permutation entries index the outer spaces (they drive device gathers and
+// scatters), the outermost factors match the outer dimensions, and a
+// factor-free plan is square (apply_impl then only permutes).
+static void check_tables(const PlanTables& T) {
+  auto perm_ok = [](const int64_t* p, int64_t n, const char* what) {
+    std::vector<char> seen(static_cast<size_t>(std::max<int64_t>(n, 0)), 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (p[i] < 0 || p[i] >= n) throw std::invalid_argument(std::string(what) + " permutation entry out of range");
+      if (seen[static_cast<size_t>(p[i])]++) throw std::invalid_argument(std::string(what) + " permutation repeats an index");
+    }
+  };
+  if (T.nrows < 0 || T.ncols < 0 || T.nfactors < 0) throw std::invalid_argument("negative plan dimension");
+  perm_ok(T.row_perm, T.nrows, "row");
+  perm_ok(T.col_perm, T.ncols, "column");
+  if (T.nfactors == 0) {
+    if (T.nrows != T.ncols) throw std::invalid_argument("a factorization without factors must be square");
+    return;
+  }
+  if (T.factors.front().rows != T.nrows) throw std::invalid_argument("first factor rows do not match nrows");
+  if (T.factors.back().cols != T.ncols) throw std::invalid_argument("last factor columns do not match ncols");
+  for (size_t f = 0; f + 1 < T.factors.size(); ++f)
+    if (T.factors[f].cols != T.factors[f + 1].rows) throw std::invalid_argument("adjacent factor shapes do not chain");
+}
+
+// Factor-free plans: out[out_perm[p]] = in[in_perm[p]] per column.
+__global__ void __launch_bounds__(256) k0_permute(const double2* __restrict__ in, double2* __restrict__ out,
+                                                  const int* __restrict__ in_perm, const int* __restrict__ out_perm,
+                                                  int64_t n, int64_t nrhs) {
+  const int64_t total = n * nrhs;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = i / n, p = i - c * n;
+    out[c * n + out_perm[p]] = in[c * n + in_perm[p]];
+  }
+}
+
 Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
+  check_tables(T);
   device = require_device();
   if (const char* e = std::getenv("MIDBF_STRIP_ROWS")) {  // experiments: strip height 1..32
     const int v = std::atoi(e);
@@ -1025,6 +1067,7 @@ bool Plan::flow_ok(int d, int64_t nrhs) const {
 }
 
 int64_t Plan::launches_per_apply(int d, int64_t nrhs) const {
+  if (dir[d].stages.empty()) return nrows * nrhs > 0 ? 1 : 0;  // k0_permute
   if (flow_ok(d, nrhs)) return nrhs;
   if (k2flow_ok(d, nrhs)) return (nrhs + kK2Rhs - 1) / kK2Rhs;
   if (k2_ok(d, nrhs)) {
@@ -1279,9 +1322,21 @@ void Plan::prepare_flow(int d) {
 void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> lock(mu);
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
+  if (dir[d].stages.empty()) {  // no factors (square, check_tables): the permutations alone
+    const int64_t n = nrows, total = n * nrhs;
+    if (total == 0) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(stream, &cs), "capture status");
+    if (cs == cudaStreamCaptureStatusNone) cuda_check(cudaStreamWaitEvent(stream, ev_last, 0), "order applies");
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms) * 8));
+    k0_permute<<<blocks, 256, 0, stream>>>(in, out, d == 0 ? d_col_perm : d_row_perm, d == 0 ? d_row_perm : d_col_perm,
+                                           n, nrhs);
+    cuda_check(cudaGetLastError(), "k0_permute");
+    if (cs == cudaStreamCaptureStatusNone) cuda_check(cudaEventRecord(ev_last, stream), "event");
+    return;
+  }
   ensure_buffers(nrhs);
   if (flow_ok(d, nrhs)) prepare_flow(d);
-  if (dir[d].stages.empty()) return;
   if (k2flow_ok(d, nrhs)) ensure_k2flow(d);
   // after the previous apply on this plan, whichever stream it ran on
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1371,6 +1426,12 @@ void Plan::apply(const double* f, double* g, int64_t nrhs, bool transpose, cudaS
     }
   }
   if (!din) {
+    // d_io[0] is shared by every host-input apply of this plan: the previous
+    // one (possibly host-in / device-out on another stream, which returns
+    // without a sync) may still be reading it, so the copy waits for it.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(stream, &cs), "capture status");
+    if (cs == cudaStreamCaptureStatusNone) cuda_check(cudaStreamWaitEvent(stream, ev_last, 0), "order staging");
     cuda_check(cudaMemcpyAsync(d_io[0], f, nin * nrhs * sizeof(double2), cudaMemcpyHostToDevice, stream), "H2D");
     in = d_io[0];
   }

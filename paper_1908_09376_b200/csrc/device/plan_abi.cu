@@ -346,6 +346,13 @@ extern "C" int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags) {
   });
 }
 
+extern "C" int midbf_plan_get_flags(midbf_plan_t plan, unsigned* out) {
+  return guard([&] {
+    std::lock_guard<std::recursive_mutex> lock(plan->p->mu);
+    *out = plan->p->flags;
+  });
+}
+
 // Kernel launches of one apply (evidence for bench.py's gpu_launches).
 extern "C" int midbf_plan_launches(midbf_plan_t plan, int transpose, int64_t nrhs, int64_t* out) {
   return guard([&] { *out = plan->p->launches_per_apply(transpose ? 1 : 0, nrhs); });

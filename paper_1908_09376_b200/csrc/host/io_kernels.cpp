@@ -132,12 +132,60 @@ DevicePlanCache::~DevicePlanCache() {
   if (plan) midbf_plan_destroy(plan);
 }
 
-std::shared_ptr<DevicePlanCache> device_plan(const Factorization& F, unsigned directions) {
-  // one mutex for all factorizations: plan builds are rare and brief
+namespace {
+// one mutex for all factorizations: plan builds are rare and brief
+std::mutex& plan_cache_mutex() {
   static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
-  if (F.device && (F.device->directions & directions) == directions) return F.device;
-  const unsigned want = directions | (F.device ? F.device->directions : 0u);
+  return mu;
+}
+// Layout stamp of a factorization: outer sizes, factor / block shapes and
+// offsets, and the block buffers' addresses (a copied or reallocated block
+// has a new buffer).  Cheap (no payload reads), so every apply checks it.
+std::uint64_t layout_stamp(const Factorization& F) {
+  std::uint64_t h = 0x6d69646266ull;
+  auto mix = [&h](std::uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  };
+  mix(static_cast<std::uint64_t>(F.nrows));
+  mix(static_cast<std::uint64_t>(F.ncols));
+  mix(F.row_perm.size());
+  mix(F.col_perm.size());
+  mix(reinterpret_cast<std::uintptr_t>(F.row_perm.data()));
+  mix(reinterpret_cast<std::uintptr_t>(F.col_perm.data()));
+  mix(F.factors.size());
+  for (const Factor& fc : F.factors) {
+    mix(static_cast<std::uint64_t>(fc.rows));
+    mix(static_cast<std::uint64_t>(fc.cols));
+    mix(fc.blocks.size());
+    mix(fc.groups.size());
+    for (const FactorBlock& b : fc.blocks) {
+      mix(static_cast<std::uint64_t>(b.row_off));
+      mix(static_cast<std::uint64_t>(b.col_off));
+      mix(static_cast<std::uint64_t>(b.M.rows()));
+      mix(static_cast<std::uint64_t>(b.M.cols()));
+      mix(reinterpret_cast<std::uintptr_t>(b.M.data()));
+    }
+    for (const auto& g : fc.groups) {
+      mix(static_cast<std::uint64_t>(g.first));
+      mix(static_cast<std::uint64_t>(g.second));
+    }
+  }
+  return h;
+}
+}  // namespace
+
+void Factorization::invalidate_device_plan() const {
+  std::lock_guard<std::mutex> lock(plan_cache_mutex());
+  device.p.reset();  // callers holding the old cache keep it alive until they finish
+}
+
+std::shared_ptr<DevicePlanCache> device_plan(const Factorization& F, unsigned directions) {
+  std::lock_guard<std::mutex> lock(plan_cache_mutex());
+  const std::uint64_t stamp = layout_stamp(F);
+  std::shared_ptr<DevicePlanCache>& cur = F.device.p;
+  if (cur && cur->stamp != stamp) cur.reset();  // layout changed since the plan was built
+  if (cur && (cur->directions & directions) == directions) return cur;
+  const unsigned want = directions | (cur ? cur->directions : 0u);
   std::vector<std::int64_t> shape, blocks, groups;
   for (const Factor& fc : F.factors) {
     shape.insert(shape.end(), {fc.rows, fc.cols, static_cast<std::int64_t>(fc.blocks.size()),
@@ -156,7 +204,8 @@ std::shared_ptr<DevicePlanCache> device_plan(const Factorization& F, unsigned di
                                            static_cast<std::int64_t>(F.factors.size()), shape.data(), blocks.data(),
                                            groups.data(), ptrs.data(), want));
   cache->directions = want;
-  F.device = cache;  // earlier entries live on while callers still hold them
+  cache->stamp = stamp;
+  cur = cache;  // earlier entries live on while callers still hold them
   return cache;
 }
 

@@ -31,6 +31,7 @@ Factorization idbf_factorize_stats(const ker::KernelDesc& K, const tree::Cluster
 struct DevicePlanCache {
   midbf_plan_t plan = nullptr;
   unsigned directions = 0;
+  std::uint64_t stamp = 0;  // layout_stamp of the factorization it was built from
   ~DevicePlanCache();
 };
 // Returns the cache entry (not just the handle) so that a concurrent caller

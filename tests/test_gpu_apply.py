@@ -91,7 +91,7 @@ def test_multi_rhs_fallback_paths(pair, path):
             plan.set_flags(dmma=False)
         got = plan.apply(X)
     finally:
-        plan.set_flags()
+        plan.reset_flags()
     assert plan.launches(67) == 2  # k2_flow: one launch per 64-RHS slice
     assert rel(got, want) <= TOL
     assert rel(default, want) <= TOL
@@ -110,7 +110,7 @@ def test_single_rhs_kernel_variants(pair, variant):
             plan.set_flags(variant=variant)
         a, b = plan.apply(f), plan.apply(g, transpose=True)
     finally:
-        plan.set_flags()
+        plan.reset_flags()
     assert rel(a, Fo.apply(f)) <= TOL
     assert rel(b, Fo.apply_transpose(g)) <= TOL
     if variant != "stages":
@@ -124,7 +124,7 @@ def test_identity_compression(pair, variant):
     bytes than the stored factor whenever an ID block has any, and the same
     result as the dense panels and the oracle, both directions."""
     name, K, Fo, Fm, plan = pair
-    plan.set_flags()  # the compressed kernel (small plans default to the dense-only one)
+    plan.set_flags(lite=False)  # the compressed kernel (small plans default to the dense-only one)
     stored = sum(s[1] for s in plan.stages())
     streamed = sum(plan.flow_bytes())
     assert 0 < streamed <= stored
@@ -133,7 +133,7 @@ def test_identity_compression(pair, variant):
     f, g = cvec(Fo.ncols, 24), cvec(Fo.nrows, 25)
     F48 = cvec(Fo.ncols, 26, cols=48)  # k2_flow on a 64-wide tile: compressed V-type strips
     try:
-        plan.set_flags(variant=variant)
+        plan.set_flags(variant=variant, lite=False)
         a, b, c = plan.apply(f), plan.apply(g, transpose=True), plan.apply(F48)
         plan.set_flags(variant=variant, compress=False)
         assert sum(plan.flow_bytes()) == stored
@@ -142,7 +142,7 @@ def test_identity_compression(pair, variant):
         assert sum(plan.flow_bytes()) == stored
         a1, b1 = plan.apply(f), plan.apply(g, transpose=True)
     finally:
-        plan.set_flags()
+        plan.reset_flags()
     assert rel(a, a0) <= 1e-14 and rel(b, b0) <= 1e-14 and rel(c, c0) <= 1e-14
     assert np.array_equal(a1, a0) and np.array_equal(b1, b0)  # same dense panels, same order
     assert rel(a, Fo.apply(f)) <= TOL
@@ -168,7 +168,7 @@ def test_wide_strip_identity_compression(wide3d):
     (kept columns through a global map, identity adds read from x itself);
     permutation factors stream nothing.  Every layout, both directions."""
     Fo, plan = wide3d
-    plan.set_flags()  # the compressed kernel
+    plan.set_flags(lite=False)  # the compressed kernel
     stages, fb = plan.stages(), plan.flow_bytes()
     assert fb[0] == 0 and fb[-1] == 0  # V^1 / U^1 are permutations
     assert fb[1] < stages[1][1] and fb[3] < stages[3][1]  # the wide ID stages
@@ -177,11 +177,11 @@ def test_wide_strip_identity_compression(wide3d):
     want_f, want_g = Fo.apply(f), Fo.apply_transpose(g)
     try:
         for variant in (0, 1):
-            plan.set_flags(variant=variant)
+            plan.set_flags(variant=variant, lite=False)
             assert rel(plan.apply(f), want_f) <= TOL
             assert rel(plan.apply(g, transpose=True), want_g) <= TOL
     finally:
-        plan.set_flags()
+        plan.reset_flags()
 
 
 def test_multi_rhs_runs_are_bitwise_identical(pair):
@@ -340,6 +340,47 @@ def test_concurrent_applies_on_one_plan(gpu, route):
     assert not errors, errors
 
 
+def test_concurrent_host_in_device_out_applies(gpu):
+    """Host input, device output (the staging copy into the plan's shared
+    input buffer returns without a sync): two threads on their own streams
+    alternate inputs; the H2D of one must not overwrite the staged input
+    while the other's kernels still read it (plan.cu staging)."""
+    import threading
+
+    torch = pytest.importorskip("torch")
+    X = O.grid2d(32)
+    K, Fo = oracle_factorization(O.KIND_FIO2D, X, X, 64, 30, 1e-9)
+    path = saved(Fo)
+    plan = M.DevicePlan.load(path, directions=1)
+    os.unlink(path)
+    ins = [cvec(1024, 140 + i) for i in range(4)]
+    want = [Fo.apply(f) for f in ins]
+    errors = []
+
+    def worker(t):
+        try:
+            s = torch.cuda.Stream()
+            outs = [torch.empty(1024, dtype=torch.complex128, device="cuda") for _ in range(2)]
+            for rep in range(40):
+                i = 2 * t + (rep & 1)
+                plan.apply_ptr(ins[i].ctypes.data, outs[rep & 1].data_ptr(), 1, False, s.cuda_stream)
+                if rep & 1:
+                    s.synchronize()
+                    for j in range(2):
+                        got = outs[j].cpu().numpy()
+                        if rel(got, want[2 * t + j]) > TOL:
+                            errors.append((t, rep, j, rel(got, want[2 * t + j])))
+        except Exception as e:  # noqa: BLE001
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[:4]
+
+
 def test_factorization_applies_from_threads(gpu):
     """bf::apply / apply_transpose on ONE factorization from several threads
     (the cached plan is built once, with a direction added concurrently)."""
@@ -383,7 +424,8 @@ def test_flow_polls_survive_flag_switches(pair):
     want = {}
     try:
         for it in range(24):
-            for kw in (dict(variant=0), dict(variant=1), dict(variant=1, lite=True), dict(variant=0, lite=True)):
+            for kw in (dict(variant=0, lite=False), dict(variant=1, lite=False), dict(variant=1, lite=True),
+                       dict(variant=0, lite=True)):
                 plan.set_flags(**kw)
                 for tr, v in ((False, f), (True, g)):
                     got = plan.apply(v, transpose=tr)
@@ -395,4 +437,65 @@ def test_flow_polls_survive_flag_switches(pair):
                     else:  # run-to-run bitwise (fixed summation order per strip)
                         assert np.array_equal(got, want[key]), (it, kw, tr)
     finally:
-        plan.set_flags()
+        plan.reset_flags()
+
+
+def test_device_tensor_operands_are_checked(pair):
+    """DevicePlan.apply on device tensors: out allocated when absent,
+    row-major (torch default) n x nrhs operands handled as matrices (the ABI
+    is column-major), dtype / length / out shape rejected before the ABI."""
+    torch = pytest.importorskip("torch")
+    name, K, Fo, Fm, plan = pair
+    F3 = cvec(Fo.ncols, 51, cols=3)
+    want = Fo.apply(F3)
+    dev = torch.from_numpy(np.ascontiguousarray(F3)).cuda()  # row-major
+    got = plan.apply(dev)
+    torch.cuda.synchronize()
+    assert rel(got.cpu().numpy(), want) <= TOL
+    out = torch.empty(Fo.nrows, 3, dtype=torch.complex128, device="cuda")  # row-major out
+    plan.apply(dev, out=out)
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), want) <= TOL
+    v = plan.apply(dev[:, 1])  # strided column view
+    torch.cuda.synchronize()
+    assert rel(v.cpu().numpy(), want[:, 1]) <= TOL
+    with pytest.raises(TypeError):
+        plan.apply(dev.to(torch.complex64))
+    with pytest.raises(ValueError):
+        plan.apply(dev[:-1])
+    with pytest.raises(ValueError):
+        plan.apply(dev, out=torch.empty(Fo.nrows - 1, 3, dtype=torch.complex128, device="cuda"))
+
+
+def test_factor_free_plan_is_the_permutations(gpu):
+    """nfactors == 0: the reference's apply_impl only gathers through
+    col_perm and scatters through row_perm (src/butterfly.cpp:650-665)."""
+    rng = np.random.default_rng(5)
+    n = 300
+    rp, cp = rng.permutation(n), rng.permutation(n)
+    plan = M.DevicePlan.from_tables(n, n, rp, cp, [], directions=3)
+    assert plan.launches(1) == 1
+    f = cvec(n, 52, cols=3)
+    want = np.empty_like(f)
+    want[rp] = f[cp]
+    assert np.array_equal(plan.apply(f), want)
+    wt = np.empty_like(f)
+    wt[cp] = f[rp]
+    assert np.array_equal(plan.apply(f, transpose=True), wt)
+
+
+def test_plan_tables_are_validated(gpu):
+    """Permutation entries feed device gathers / scatters and the outer
+    factor shapes the stage buffers: invalid tables are rejected with the
+    reference's invalid_argument class instead of reaching a kernel."""
+    good = (4, 4, [[0, 0, 4, 4]], [[0, 1]], [np.eye(4)])
+    M.DevicePlan.from_tables(4, 4, [0, 1, 2, 3], [3, 2, 1, 0], [good])
+    for rp, cp, facs in (([0, 1, 2, 4], [0, 1, 2, 3], [good]),   # out of range
+                         ([0, 1, 1, 3], [0, 1, 2, 3], [good]),   # repeated
+                         ([0, 1, 2, 3], [0, 1, 2, -1], [good]),  # negative
+                         ([0, 1, 2], [0, 1, 2, 3], [])):         # factor-free, not square
+        with pytest.raises(ValueError):  # std::invalid_argument
+            M.DevicePlan.from_tables(len(rp), len(cp), rp, cp, facs)
+    wide = (4, 5, [[0, 0, 4, 5]], [[0, 1]], [np.ones((4, 5))])
+    with pytest.raises(ValueError):  # last factor has 5 columns, ncols = 4
+        M.DevicePlan.from_tables(4, 4, [0, 1, 2, 3], [0, 1, 2, 3], [wide])

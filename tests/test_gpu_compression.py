@@ -122,7 +122,7 @@ def adversarial(gpu):
 
 def test_streams_less_than_stored(adversarial):
     plan, A, fs = adversarial
-    plan.set_flags()  # the compressed kernel (small plans default to the dense-only one)
+    plan.set_flags(lite=False)  # the compressed kernel (small plans default to the dense-only one)
     stored = [s[1] for s in plan.stages()]
     fb = plan.flow_bytes()
     assert fb[0] < stored[0] and fb[1] < stored[1] and fb[2] < stored[2]  # wide, V, U
@@ -138,11 +138,11 @@ def test_matches_dense_product(adversarial, variant, nrhs):
     f = _cplx(rng, 200, nrhs)
     g = _cplx(rng, 60, nrhs)
     try:
-        plan.set_flags(variant=variant)
+        plan.set_flags(variant=variant, lite=False)
         a, b = plan.apply(f), plan.apply(g, transpose=True)
         plan.set_flags(variant=variant, compress=False)
         a0, b0 = plan.apply(f), plan.apply(g, transpose=True)
     finally:
-        plan.set_flags()
+        plan.reset_flags()
     assert rel(a, A @ f) <= TOL and rel(b, A.T @ g) <= TOL
     assert rel(a0, A @ f) <= TOL and rel(b0, A.T @ g) <= TOL
