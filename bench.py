@@ -62,17 +62,43 @@ def unit_grid(n, dim):
 
 
 def measured_traffic(config, launches):
-    """DRAM bytes per launch of this workload's dominant kernel from the
-    committed ncu capture (profiles/r1_traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
-    try:
-        with open(path) as fh:
-            rec = json.load(fh).get(config)
-    except (OSError, ValueError):
-        return None
-    if not rec or launches != 1:
-        return None
-    return rec["dram_bytes_per_launch"]
+    """DRAM bytes (read + write) per launch of this workload's dominant
+    kernel from the committed ncu capture (profiles/r2_traffic.json, else
+    r1), or None."""
+    for fn in ("r2_traffic.json", "r1_traffic.json"):
+        path = os.path.join(ROOT, "profiles", fn)
+        try:
+            with open(path) as fh:
+                rec = json.load(fh).get(config)
+        except (OSError, ValueError):
+            continue
+        if rec and launches == rec.get("launches_per_apply", 1):
+            return rec["dram_bytes_per_launch"]
+    return None
+
+
+L2_NOTE = "factor payload > 126 MB L2 except cfg0 / cfg1_unitxi (L2-resident); no flush; vectors L2-resident"
+
+
+def static_config(name, world):
+    """The workload as both arms report it (identical dicts)."""
+    if name in ("cfg1", "cfg4", "cfg1_unitxi", "cfg0"):
+        n = 64 if name == "cfg0" else 256
+        k = 20 if name == "cfg0" else 30
+        desc = dict(model="MIDBF 2D FIO", n_per_dim=n, N=n * n, k=k, n0=64, t=5, eps=1e-9,
+                    xi="unit grid (Omega = X)" if name == "cfg1_unitxi" else "integer grid [-n/2,n/2)^2")
+        nrhs = 64 if name == "cfg4" else 1
+    elif name == "cfg2":
+        desc = dict(model="MIDBF 2D low-rank phase r=8", n_per_dim=512, N=512 * 512, k=30, n0=64, t=5, eps=1e-9,
+                    xi="integer grid", phase="rank-8 rsvd of the explicit 2D FIO phase, q=2, V <- V S")
+        nrhs = 1
+    elif name == "cfg3":
+        desc = dict(model="MIDBF 3D FIO", n_per_dim=32, N=32 ** 3, k=64, n0=64, t=5, eps=1e-9,
+                    xi="integer grid [-16,16)^3")
+        nrhs = 1
+    else:
+        raise SystemExit(f"unknown config {name}")
+    return dict(workload=name, nrhs=nrhs, parallelism=f"replicas x{world}", l2=L2_NOTE, **desc)
 
 
 def workload(name):
@@ -105,7 +131,7 @@ def workload(name):
         K = _lowrank_kernel(M, X, Om, A, B)
         return K, X, Om, dict(n0=64, k=30), 1, dict(model="MIDBF 2D low-rank phase r=8", n_per_dim=n, N=n * n,
                                                     k=30, n0=64, t=5, eps=1e-9, xi="integer grid",
-                                                    phase=dict(rank=8, q=2, seconds=t_phase, eps_K=eps_k))
+                                                    inputs=dict(phase_rank=8, q=2, seconds=t_phase, eps_K=eps_k))
     if name == "cfg3":
         n = 32
         X = unit_grid(n, 3)
@@ -186,27 +212,70 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _ref_module():
+    """oracle/_ref (the reference's own code, built in the container where
+    /root/reference exists; the built files travel to the GPU box), or None."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import ref as R
+
+        if os.path.exists(R.LIB_PATH):
+            R.lib()
+            return R
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(F_path, f, nrhs, budget_s=20.0):
-    """Oracle (restated reference apply, OpenMP over groups like
-    src/butterfly.cpp:628) on all host cores: one warm-up, then repeats
-    until the time budget; best and median reported."""
+    """The reference's own bf::apply (oracle/_ref: proj/src compiled
+    unmodified, Exec::Parallel = OpenMP over groups, src/butterfly.cpp:628)
+    on all host cores on the same F, or the oracle restatement when _ref is
+    absent: one warm-up, then repeats until the time budget; best and median
+    reported, plus one serial apply (the oracle, Exec::Serial)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
-    Fo = O.load(F_path)
+    R = _ref_module()
     cores = os.cpu_count()
-    g = Fo.apply(f, parallel=True, threads=cores)
+    Fo = O.load(F_path)
+    if R is not None:
+        Fr = R.Loaded(F_path)
+        run, kind, what = (lambda: Fr.apply(f)), "reference", "the reference's bf::apply (oracle/_ref)"
+    else:
+        run, kind, what = (lambda: Fo.apply(f, parallel=True, threads=cores)), "port", "oracle restatement"
+    g = run()
     times = []
     t_end = time.perf_counter() + budget_s
     while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 200):
         t0 = time.perf_counter()
-        g = Fo.apply(f, parallel=True, threads=cores)
+        g = run()
         times.append(time.perf_counter() - t0)
     t1 = time.perf_counter()
     Fo.apply(f[:, 0] if f.ndim == 2 else f, parallel=False)
     serial = time.perf_counter() - t1
     return g, dict(best=min(times), median=statistics.median(times), reps=len(times), cores=cores,
-                   serial_one=serial, Fo=Fo)
+                   serial_one=serial, kind=kind, what=what)
+
+
+def accuracy(M, K, F, fk, f):
+    """metrics::eps_b (src/metrics.cpp:26-48): rel-L2 of g = F f against the
+    direct sum on 256 rows drawn by la::rand_subset(N, 256, mt19937_64(
+    chain(0, 0x657062))) (src/experiment.cpp:180), direct sums by K4 on the
+    GPU.  For the device-sampled F (K3 entries + K5 IDs, the timed one) and
+    a host-sampled F of the same config (entries through the reference's
+    EntryFn path on the CPU, host IDs).  SURVEY.md §0: with integer xi no
+    k=20/30 factorization is accurate, so both are O(1) and must agree;
+    cfg1_unitxi (Omega = X) is the accuracy-meaningful companion."""
+    seed = M.chain(0, 0x657062)
+    t0 = time.perf_counter()
+    e_dev = K.eps_b(F.apply(f), f, nrows=256, seed=seed)
+    Fh = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="host",
+                          ids="host")
+    e_host = K.eps_b(Fh.apply(f), f, nrows=256, seed=seed)
+    return {"eps_b_device_sampled": e_dev, "eps_b_host_sampled": e_host, "rows": 256,
+            "rows_seed": "chain(0, 0x657062)", "direct_sum": "K4 on the GPU",
+            "host_sampled_total_nnz": Fh.total_nnz, "seconds": time.perf_counter() - t0}
 
 
 def main():
@@ -217,6 +286,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true", help="skip the eps_b key (two direct sums + a host factorize)")
     ap.add_argument("--flags", type=int, default=63,
                     help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel | (v<<4) k1_flow variant (3 = by size) | 512 dense panels | 1024 dense-only k1_flow (default below 200 MB) | 2048 no DMMA | 8192 per-stage DMMA | 65536 never dense-only")
     args = ap.parse_args()
@@ -339,6 +409,8 @@ def main():
     achieved = alg_bytes / (ms_step * 1e-3) / 1e9
     launches = plan.launches(nrhs)
     traffic = measured_traffic(args.config, launches)
+    # DRAM bytes actually moved per apply (ncu, cold cache) over the apply time
+    frac_dram = (traffic * launches / (ms_step * 1e-3) / 1e9 / hbm) if traffic else None
     if nrhs == 1:
         # algorithmic bytes = the factor as stored (16*total_nnz)
         # + vectors.  k1_flow streams fewer: the ID blocks' exact unit rows /
@@ -347,11 +419,14 @@ def main():
         streamed = sum(flow_bytes) + vec_bytes
         sgbs = streamed / (ms_step * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_kind": peak_kind, "traffic": traffic, "algorithmic_bytes_per_apply": alg_bytes,
+                    "peak_kind": peak_kind, "traffic": traffic, "frac_dram": frac_dram,
+                    "algorithmic_bytes_per_apply": alg_bytes,
                     "streamed_bytes_per_apply": streamed, "streamed_gbs": sgbs, "streamed_frac": sgbs / hbm,
-                    "note": "achieved = (16*total_nnz + 16*(N_in+N_out)) / apply time (SURVEY.md 8(d)); k1_flow "
-                            "streams only the identity-compressed panels (streamed_*; traffic = ncu DRAM bytes "
-                            f"of that launch); one apply = {launches} k1_flow launch in one CUDA graph"}
+                    "note": "achieved = (16*total_nnz + 16*(N_in+N_out)) / apply time (SURVEY.md 8(d): the factor "
+                            "as stored); k1_flow streams only the identity-compressed panels (streamed_*), so frac "
+                            "can exceed the bandwidth actually used: frac_dram = ncu DRAM bytes (read+write) of the "
+                            "launch / apply time / peak is the honest HBM efficiency; "
+                            f"one apply = {launches} k1_flow launch in one CUDA graph"}
     else:
         # algorithmic flops = 8 * nrhs * total_nnz; k2_flow skips
         # the exact identity columns of V-type ID strips on 32/64-wide tiles
@@ -361,7 +436,7 @@ def main():
         etf = executed / (ms_step * 1e-3) / 1e12
         roofline = {"bound": "tensor", "achieved": tf, "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                     "frac": tf / FP64_DMMA_TFLOPS, "peak_kind": "measured (tools/fp64_probe.cu, DMMA m8n8k4)",
-                    "traffic": traffic, "algorithmic_flops_per_apply": flops,
+                    "traffic": traffic, "frac_dram": frac_dram, "algorithmic_flops_per_apply": flops,
                     "executed_flops_per_apply": executed, "executed_tflops": etf,
                     "executed_frac": etf / FP64_DMMA_TFLOPS,
                     "hbm_gbs": achieved, "hbm_frac": achieved / hbm,
@@ -382,9 +457,8 @@ def main():
         "vs_baseline": None,
         "dtype": "c128 (complex f64)",
         "data": "synthetic (seeded grids + std::mt19937_64 Gaussian f, reference experiment generators)",
-        "config": dict(workload=args.config, nrhs=nrhs, parallelism=f"replicas x{world}",
-                       l2="factor payload %.1f MB > 126 MB L2 (no flush needed; vectors L2-resident)"
-                          % (16 * F.total_nnz / 1e6), **desc),
+        "config": static_config(args.config, world),
+        "inputs": desc.get("inputs"),
         "roofline": roofline,
         "e2e": {"value": replica_throughput(world, nrhs, e_s * 1e3), "unit": "matvecs/s",
                 "mode": "pipelined midbf_apply_async over 3 pinned host buffer pairs, CUDA events",
@@ -401,6 +475,8 @@ def main():
         "clocks": clk.summary(),
         "host_issue_us_per_step": host_issue_us,
     }
+    if not args.no_accuracy:
+        line["accuracy"] = accuracy(M, K, F, fk, f_host[:, 0])
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         fd_, path = tempfile.mkstemp(suffix=".midbf")
         os.close(fd_)
@@ -410,60 +486,108 @@ def main():
         g_cpu = g_cpu.reshape((F.nrows, nrhs), order="F")
         err = float(np.linalg.norm(g_dev - g_cpu) / np.linalg.norm(g_cpu))
         line["rel_l2_vs_ref"] = err
+        line["rel_l2_vs_ref_note"] = (f"device g vs {cb['what']} on the same F (the product's, handed over as "
+                                      "MIDBF001) and f")
         line["cpu_baseline"] = {"value": nrhs / cb["best"], "unit": "matvecs/s", "cores": cb["cores"],
-                                "kind": "port", "median_value": nrhs / cb["median"],
+                                "kind": cb["kind"], "median_value": nrhs / cb["median"],
                                 "serial_1core_value": 1.0 / cb["serial_one"],
-                                "sample": f"{cb['reps']} applies of the same F and f (best of; one warm-up), "
-                                          "oracle restatement of bf::apply with OpenMP over groups"}
+                                "sample": f"{cb['reps']} applies of the same F and f (best of; one warm-up, "
+                                          f"~20 s budget): {cb['what']}, OpenMP over groups on all host threads"}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
+def reference_points(name):
+    """Point sets / kernel inputs of a config for the CPU arm (numpy only)."""
+    if name in ("cfg1", "cfg4", "cfg1_unitxi", "cfg0"):
+        n = 64 if name == "cfg0" else 256
+        X = unit_grid(n, 2)
+        return X, (X.copy() if name == "cfg1_unitxi" else integer_grid(n, 2)), None, None
+    if name == "cfg2":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import lowrank as LR
+
+        X, Om = unit_grid(512, 2), integer_grid(512, 2)
+        allc, allr = np.arange(len(Om)), np.arange(len(X))
+        # la::rsvd restated in numpy (oracle/lowrank.py) on the explicit phase,
+        # rank 8, q = 2, V <- V S, seed 7: the same recipe as the GPU arm's
+        # A, B (equal to rounding; the timing workload is the same shape)
+        A, B, _, _ = LR.lowrank_phase(lambda i: LR.fio2d_phase_block(X, Om, [i], allc)[0],
+                                      lambda j: LR.fio2d_phase_block(X, Om, allr, [j])[:, 0], len(X), len(Om), 8, 2, 7)
+        return X, Om, A, B
+    if name == "cfg3":
+        return unit_grid(32, 3), integer_grid(32, 3), None, None
+    raise SystemExit(f"unknown config {name}")
+
+
 def reference_arm(args, world, rank):
-    """The reference's own CPU path (oracle restatement: the reference cannot
-    be compiled here) on the same workload: factorize on the CPU, then time
-    bf::apply with all host threads."""
+    """The reference's own CPU path on the same workload: oracle/_ref is
+    /root/reference/proj/src compiled unmodified (against the Eigen stand-in
+    oracle/shim/, oracle/ref.mk).  Factorize with its bf::idbf_factorize
+    (Exec::Parallel, entries from its ker::make_accessor / phase_entry_fn),
+    then time its bf::apply with all host threads, each step one apply of
+    the experiment's f.  Falls back to the oracle restatement (kind "port")
+    only if oracle/_ref is missing.  Under torchrun rank 0 alone runs."""
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     name = args.config
-    if name not in ("cfg0", "cfg1", "cfg1_unitxi", "cfg4"):
-        print(json.dumps({"impl": "reference", "unavailable": f"reference arm wired for 2D FIO configs only ({name})"}))
-        return
-    n = 64 if name == "cfg0" else 256
-    X = unit_grid(n, 2)
-    Om = X.copy() if name == "cfg1_unitxi" else integer_grid(n, 2)
-    k = 20 if name == "cfg0" else 30
-    nrhs = 64 if name == "cfg4" else 1
-    K = O.Kernel(O.KIND_FIO2D, X=X, Omega=Om)
+    cfg = static_config(name, world)
+    nrhs, n0, k = cfg["nrhs"], cfg["n0"], cfg["k"]
+    X, Om, A, B = reference_points(name)
+    kind = {"cfg2": O.KIND_LOWRANK, "cfg3": O.KIND_FIO3D}.get(name, O.KIND_FIO2D)
+    R = _ref_module()
+    seed = O.chain(0, 0x666163)
     t0 = time.perf_counter()
-    Fo = O.factorize(K, X, Om, 64, k=k, eps=1e-9, t=5, seed=O.chain(0, 0x666163), parallel=True)
+    if R is not None:
+        P = R.Problem(kind, X, Om, A=A, B=B)
+        path = P.factorize(n0, k=k, eps=1e-9, t=5, seed=seed, parallel=True)
+        Fr = R.Loaded(path)
+        apply_fn, total_nnz = Fr.apply, Fr.info["total_nnz"]
+        ref_kind, what = "reference", "the reference's bf::idbf_factorize + bf::apply (oracle/_ref, unmodified proj/src)"
+    else:
+        Ko = O.Kernel(kind, X=X, Omega=Om, A=A, B=B)
+        Fo = O.factorize(Ko, X, Om, n0, k=k, eps=1e-9, t=5, seed=seed, parallel=True)
+        cores_ = os.cpu_count()
+        apply_fn, total_nnz = (lambda f: Fo.apply(f, parallel=True, threads=cores_)), Fo.total_nnz
+        ref_kind, what, path = "port", "oracle restatement (oracle/_ref missing)", None
     t_fac = time.perf_counter() - t0
-    f = O.random_coefficients(n * n * nrhs, O.chain(0, 0x66)).reshape((n * n, nrhs), order="F")
+    N = len(Om)
+    f = O.random_coefficients(N * nrhs, O.chain(0, 0x66)).reshape((N, nrhs), order="F")
     if nrhs == 1:
         f = f[:, 0]
     cores = os.cpu_count()
     for _ in range(max(1, args.warmup)):
-        Fo.apply(f, parallel=True, threads=cores)
+        apply_fn(f)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        Fo.apply(f, parallel=True, threads=cores)
+        g = apply_fn(f)
     s = (time.perf_counter() - t0) / args.steps
     v = nrhs / s
+    acc = None
+    if R is not None and not args.no_accuracy:
+        f1 = f if nrhs == 1 else f[:, 0]
+        acc = {"eps_b": P.eps_b(path, f1, 256, O.chain(0, 0x657062)), "rows": 256,
+               "rows_seed": "chain(0, 0x657062)", "direct_sum": "metrics::eps_b on the CPU (src/metrics.cpp:26-53)"}
+    if path:
+        os.unlink(path)
     print(json.dumps({
         "impl": "reference", "metric": "MIDBF matvecs/s at 2D N=256^2 (HBM roofline fraction); rel-L2 err vs ref",
-        "value": v, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "value": v, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps, "warmup": max(1, args.warmup),
         "ms_per_step": s * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128 (complex f64)", "data": "synthetic",
-        "config": {"workload": name, "nrhs": nrhs, "n_per_dim": n, "k": k, "n0": 64},
-        "cpu_baseline": {"value": v, "unit": "matvecs/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} applies of one CPU-built factorization (oracle restatement)"},
+        "dtype": "c128 (complex f64)",
+        "data": "synthetic (seeded grids + std::mt19937_64 Gaussian f, reference experiment generators)",
+        "config": cfg,
+        "cpu_baseline": {"value": v, "unit": "matvecs/s", "cores": cores, "kind": ref_kind,
+                         "sample": f"{args.steps} applies (after {max(1, args.warmup)} warm-up) of one CPU-built "
+                                   f"factorization (total_nnz {total_nnz}): {what}"},
         "e2e": {"value": v, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "factorize_seconds": t_fac,
+        "accuracy": acc,
     }))
 
 

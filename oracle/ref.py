@@ -147,6 +147,33 @@ def apply(path, f, transpose=False):
     return g[:, 0] if vec else g
 
 
+class Loaded:
+    """bf::load_factorization once, bf::apply many times (Exec as stored)."""
+
+    def __init__(self, path):
+        self._h = C.c_void_p()
+        _check(lib().ref_load(str(path).encode(), C.byref(self._h)))
+        self.info = info(path)
+
+    def apply(self, f, transpose=False):
+        f = np.asarray(f, dtype=np.complex128)
+        vec = f.ndim == 1
+        F2 = np.asfortranarray(f.reshape(f.shape[0], -1))
+        nout = self.info["ncols"] if transpose else self.info["nrows"]
+        g = np.empty((nout, F2.shape[1]), dtype=np.complex128, order="F")
+        _check(lib().ref_apply_h(self._h, F2.ctypes.data_as(dptr), i64(F2.shape[0]), i64(F2.shape[1]),
+                                 1 if transpose else 0, g.ctypes.data_as(dptr)))
+        return g[:, 0] if vec else g
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                lib().ref_free(self._h)
+            except Exception:
+                pass
+            self._h = None
+
+
 def info(path):
     o = np.zeros(8, dtype=np.int64)
     _check(lib().ref_info(str(path).encode(), _ip(o)))

@@ -186,6 +186,22 @@ int ref_apply(const char* path, const double* f, std::int64_t n, std::int64_t nr
   });
 }
 
+// A loaded factorization for repeated applies (bench.py's reference arm
+// times bf::apply alone, not the container read).
+int ref_load(const char* path, void** out) {
+  return guard([&] { *out = new bf::Factorization(bf::load_factorization(path)); });
+}
+void ref_free(void* h) { delete static_cast<bf::Factorization*>(h); }
+int ref_apply_h(void* h, const double* f, std::int64_t n, std::int64_t nrhs, int transpose, double* out) {
+  return guard([&] {
+    const bf::Factorization& F = *static_cast<bf::Factorization*>(h);
+    MatXc fs(n, nrhs);
+    std::memcpy(fs.data(), f, sizeof(Cplx) * n * nrhs);
+    const MatXc g = transpose ? bf::apply_transpose(F, fs) : bf::apply(F, fs);
+    std::memcpy(out, g.data(), sizeof(Cplx) * g.rows() * g.cols());
+  });
+}
+
 // nrows ncols L h n0 nfactors total_nnz max_factor_nnz
 int ref_info(const char* path, std::int64_t* o) {
   return guard([&] {

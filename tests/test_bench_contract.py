@@ -40,3 +40,20 @@ def test_reference_arm_other_ranks_are_silent():
              env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert p.returncode == 0, p.stderr
     assert p.stdout.strip() == ""
+
+
+def test_both_arms_report_the_same_config():
+    """The driver compares the two arms' config dicts: both come from
+    bench.static_config, and the reference arm runs the reference's own code
+    (oracle/_ref) when it is built."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    p = _run(["--impl", "reference", "--config", "cfg0", "--steps", "1", "--warmup", "1", "--no-accuracy"])
+    assert p.returncode == 0, p.stderr
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    assert d["config"] == bench.static_config("cfg0", 1)
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert '"config": static_config(args.config, world)' in src  # the GPU arm
+    if os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libmidbf_ref.so")):
+        assert d["cpu_baseline"]["kind"] == "reference"
