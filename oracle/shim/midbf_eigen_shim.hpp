@@ -715,9 +715,28 @@ void gemm_acc(const View<S>& y, const View<S>& a, const View<S>& b, bool subtrac
   // a transposed (row-major) view: dot-product order, then added
   const bool dot_order = a.rows() > 1 && a.innerStride() != 1;
   if (dot_order) {
+    const bool raw = a.outerStride() == 1 && b.innerStride() == 1 && !a.conjugated() && !b.conjugated();
     for (Index j = 0; j < n; ++j)
       for (Index i = 0; i < m; ++i) {
         S s = S(0);
+        if constexpr (shim::is_cplx<S>::value) {
+          if (raw) {  // a(i, :) and b(:, j) contiguous: same order, real arithmetic as above
+            using T = typename S::value_type;
+            const T* ad = reinterpret_cast<const T*>(&a.coeffRef(i, 0));
+            const T* bd = reinterpret_cast<const T*>(&b.coeffRef(0, j));
+            T sr = 0, si = 0;
+            for (Index p = 0; p < k; ++p) {
+              sr += ad[2 * p] * bd[2 * p] - ad[2 * p + 1] * bd[2 * p + 1];
+              si += ad[2 * p] * bd[2 * p + 1] + ad[2 * p + 1] * bd[2 * p];
+            }
+            s = S(sr, si);
+            if (subtract)
+              y.coeffRef(i, j) -= s;
+            else
+              y.coeffRef(i, j) += s;
+            continue;
+          }
+        }
         for (Index p = 0; p < k; ++p) s += a.coeff(i, p) * b.coeff(p, j);
         if (subtract)
           y.coeffRef(i, j) -= s;
@@ -734,10 +753,33 @@ void gemm_acc(const View<S>& y, const View<S>& a, const View<S>& b, bool subtrac
         if (raw) {  // same order, contiguous columns
           S* yc = &y.coeffRef(0, j);
           const S* ac = &a.coeffRef(0, p);
-          if (subtract)
-            for (Index i = 0; i < m; ++i) yc[i] -= ac[i] * bpj;
-          else
-            for (Index i = 0; i < m; ++i) yc[i] += ac[i] * bpj;
+          if constexpr (shim::is_cplx<S>::value) {
+            // (a+bi)(c+di) = (ac - bd) + (ad + bc)i: the value std::complex's
+            // product returns for finite operands (it only re-derives NaN
+            // results), written out so the loop vectorises like Eigen's
+            // packet kernels instead of calling __muldc3's slow path checks
+            using T = typename S::value_type;
+            T* yd = reinterpret_cast<T*>(yc);
+            const T* ad = reinterpret_cast<const T*>(ac);
+            const T c = bpj.real(), d = bpj.imag();
+            if (subtract)
+              for (Index i = 0; i < m; ++i) {
+                const T re = ad[2 * i] * c - ad[2 * i + 1] * d, im = ad[2 * i] * d + ad[2 * i + 1] * c;
+                yd[2 * i] -= re;
+                yd[2 * i + 1] -= im;
+              }
+            else
+              for (Index i = 0; i < m; ++i) {
+                const T re = ad[2 * i] * c - ad[2 * i + 1] * d, im = ad[2 * i] * d + ad[2 * i + 1] * c;
+                yd[2 * i] += re;
+                yd[2 * i + 1] += im;
+              }
+          } else {
+            if (subtract)
+              for (Index i = 0; i < m; ++i) yc[i] -= ac[i] * bpj;
+            else
+              for (Index i = 0; i < m; ++i) yc[i] += ac[i] * bpj;
+          }
           continue;
         }
         for (Index i = 0; i < m; ++i) {
