@@ -287,8 +287,8 @@ def main():
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the eps_b key (two direct sums + a host factorize)")
-    ap.add_argument("--flags", type=int, default=63,
-                    help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel | (v<<4) k1_flow variant (3 = by size) | 512 dense panels | 1024 dense-only k1_flow (default below 200 MB) | 2048 no DMMA | 8192 per-stage DMMA | 65536 never dense-only")
+    ap.add_argument("--flags", type=int, default=131135,
+                    help="plan flags: 1 PDL | 2 L2 prefetch | 4 graph | 8 persistent dataflow kernel | (v<<4) k1_flow variant (3 = by size) | 512 dense panels | 1024 dense-only k1_flow (default below 200 MB) | 2048 no DMMA | 8192 per-stage DMMA | 65536 never dense-only | 131072 chained single-RHS applies (programmatic dependent launch; default)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -225,7 +225,10 @@ int midbf_plan_k2_bytes(midbf_plan_t plan, int transpose, int64_t* out);
  * bit3 k1_flow, bits4-5 k1_flow variant (3 = by size), bits6-8 / 14-15
  * timing experiments (results invalid), bit9 dense panels, bit10 dense-only
  * k1_flow, bit11 no DMMA, bit12 phase timers, bit13 per-stage DMMA, bit16
- * always the compressed k1_flow.  A new plan starts at 0x3F. */
+ * always the compressed k1_flow, bit17 chained single-RHS applies
+ * (consecutive k1_flow grids on one stream launch as programmatic dependents,
+ * non-cooperatively; process-wide, chained grids on different streams are
+ * serialised).  A new plan starts at 0x3F | bit17. */
 int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags);
 int midbf_plan_get_flags(midbf_plan_t plan, unsigned* out);
 /* Kernel launches one apply of nrhs columns issues (1 k1_flow launch per

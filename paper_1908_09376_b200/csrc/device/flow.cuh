@@ -74,6 +74,7 @@ struct FlowParams {
   int nodeps;
   long long* prof;  // phase timers of the PROF instantiation
   const int* wmap;  // wide compressed strips: kept columns, then add columns (StripCtx::wbase)
+  int pdl;          // launched as a programmatic dependent of the previous apply (see k1_flow)
   StageIO st[kMaxStages];
 };
 
@@ -457,8 +458,18 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // Chained applies (P.pdl, programmatic dependent launch): the next apply's
+  // grid may be scheduled as soon as every CTA of this one got here, and its
+  // CTAs take SMs as ours exit.  The panel stream (plan constants) may run
+  // ahead; everything that touches the previous apply's results (epochs,
+  // stage buffers, input, output) waits for its completion and memory flush.
+  const bool tma_lane = producer && (kSep || lane == 0);  // streams plan constants only
+  if (P.pdl) {
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!tma_lane) asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
 
-  const unsigned e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
+  const unsigned e = tma_lane ? 0u : *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
   const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
   if (!producer) {

@@ -179,11 +179,13 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream, bool lite) {
   cfg.blockDim = dim3(flow_threads<FW>(), 1, 1);
   cfg.dynamicSmemBytes = FlowCfg<FW, FS, SLOT>::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = P.pdl ? 0 : 1;  // chained: 1 CTA per SM fits only once the previous grid left
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // chained applies (flow.cuh P.pdl)
+  attr[1].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (P.prof)
     cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT, true>, P), "k1_flow launch");
   else if (lite)
@@ -1122,6 +1124,7 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.in = in;
   P.in_perm = d == 0 ? d_col_perm : d_row_perm;
   P.in_len = D.in_len;
+  P.pdl = (flags & kFlagChain) ? 1 : 0;
   switch (variant) {
     case 1:
     case 2:  // retired variant: runs variant 1
@@ -1319,6 +1322,25 @@ void Plan::prepare_flow(int d) {
   last_grid[d] = grid;
 }
 
+// Process-wide order of chained (non-cooperative, persistent) k1_flow grids,
+// per device: the event of the last one and the stream it ran on (compared
+// only, never used for API calls).
+struct ChainOrder {
+  std::mutex mu;
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  bool used = false;
+};
+static ChainOrder& chain_order(int device) {
+  static ChainOrder orders[64];
+  static std::once_flag once[64];
+  ChainOrder& co = orders[device & 63];
+  std::call_once(once[device & 63], [&co] {
+    cuda_check(cudaEventCreateWithFlags(&co.ev, cudaEventDisableTiming), "chain event");
+  });
+  return co;
+}
+
 void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> lock(mu);
   if (!dir[d].built) throw std::logic_error("plan was built without this apply direction");
@@ -1342,7 +1364,35 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cuda_check(cudaStreamIsCapturing(stream, &cs), "capture status");
   const bool ordered = cs == cudaStreamCaptureStatusNone;
-  if (ordered) cuda_check(cudaStreamWaitEvent(stream, ev_last, 0), "order applies");
+  // chained single-RHS applies (bit 17): plain launches with programmatic
+  // dependent launch, so consecutive applies on one stream overlap launch and
+  // panel prefetch; stream order already orders them, the event wait (which
+  // would serialise the two grids) is only needed across streams
+  const bool chain = ordered && (flags & kFlagChain) && flow_ok(d, nrhs) && nrhs == 1;
+  if (ordered && !(chain && stream == last_stream)) cuda_check(cudaStreamWaitEvent(stream, ev_last, 0), "order applies");
+  if (ordered) last_stream = stream;
+  // Chained grids launch without the cooperative guarantee (it would wait for
+  // the whole GPU and forbid the overlap), so two of them must never share
+  // the SMs: process-wide, a chained k1_flow on another stream than the
+  // previous one waits for it.  On one stream they follow each other.
+  std::unique_lock<std::mutex> chain_lock;
+  ChainOrder* co = nullptr;
+  if (chain) {
+    co = &chain_order(device);
+    chain_lock = std::unique_lock<std::mutex>(co->mu);
+    if (co->last != stream && co->used) cuda_check(cudaStreamWaitEvent(stream, co->ev, 0), "order chained grids");
+  }
+  struct ChainDone {
+    ChainOrder* co;
+    cudaStream_t s;
+    ~ChainDone() {
+      if (co) {
+        cudaEventRecord(co->ev, s);
+        co->last = s;
+        co->used = true;
+      }
+    }
+  } chain_done{co, stream};
   struct Done {
     Plan* p;
     cudaStream_t s;
@@ -1351,7 +1401,7 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
       if (on) cudaEventRecord(p->ev_last, s);
     }
   } done{this, stream, ordered};
-  if (!(flags & 4u)) {
+  if (!(flags & 4u) || chain) {
     launch(d, in, out, nrhs, stream);
     cuda_check(cudaGetLastError(), "apply");
     return;

@@ -14,6 +14,9 @@ namespace midbf::dev {
 struct StripCtx;
 
 constexpr int kMaxStages = 64;
+// Plan flag bit 17: chain consecutive single-RHS k1_flow applies on one stream
+// with programmatic dependent launch (no graph, no same-stream event wait).
+constexpr unsigned kFlagChain = 1u << 17;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 
@@ -133,7 +136,9 @@ class Plan {
   // compression off), bit11 disable K2 (DMMA multi-RHS),
   // bit13 per-stage K2 launches instead of the k2_flow dataflow kernel,
   // bits14-15 k2_flow timing experiments (k2flow.cuh, results invalid).
-  unsigned flags = 0x3F;  // default: k1_flow variant chosen by size (flow_variant), graphs, PDL, prefetch
+  // default: k1_flow variant chosen by size (flow_variant), graphs, PDL,
+  // prefetch, consecutive single-RHS applies chained (kFlagChain)
+  unsigned flags = 0x3F | kFlagChain;
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
   int strip_rows = 32;  // output rows per strip (one warp's lanes)
@@ -183,6 +188,7 @@ class Plan {
 
  private:
   cudaEvent_t ev_last = nullptr;
+  cudaStream_t last_stream = nullptr;  // stream of the previous ordered apply (chain mode skips same-stream waits)
 };
 
 std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions);

@@ -499,3 +499,49 @@ def test_plan_tables_are_validated(gpu):
     wide = (4, 5, [[0, 0, 4, 5]], [[0, 1]], [np.ones((4, 5))])
     with pytest.raises(ValueError):  # last factor has 5 columns, ncols = 4
         M.DevicePlan.from_tables(4, 4, [0, 1, 2, 3], [0, 1, 2, 3], [wide])
+
+
+@pytest.mark.timeout(300)
+def test_chained_grids_of_two_plans_on_two_streams(gpu):
+    """Chained single-RHS applies (flag bit 17, the default) launch k1_flow
+    without the cooperative guarantee; two plans applied concurrently from
+    two threads on two streams must neither deadlock (two persistent grids
+    sharing the SMs) nor mix results: chained grids on different streams are
+    serialised process-wide."""
+    import threading
+
+    torch = pytest.importorskip("torch")
+    jobs = []
+    for n, xi in ((32, None), (64, "int")):
+        X = O.grid2d(n)
+        Om = X if xi is None else integer_grid(n)
+        K, Fo = oracle_factorization(O.KIND_FIO2D, X, Om, 64, 30 if n == 32 else 20, 1e-9)
+        path = saved(Fo)
+        plan = M.DevicePlan.load(path, directions=1)
+        os.unlink(path)
+        assert plan.get_flags() & (1 << 17)
+        f = cvec(Fo.ncols, 60 + n)
+        jobs.append((plan, f, Fo.apply(f)))
+    errors = []
+
+    def worker(i):
+        try:
+            plan, f, want = jobs[i]
+            s = torch.cuda.Stream()
+            fd = torch.from_numpy(f).cuda()
+            outs = [torch.empty(len(want), dtype=torch.complex128, device="cuda") for _ in range(4)]
+            for rep in range(200):
+                plan.apply_ptr(fd.data_ptr(), outs[rep % 4].data_ptr(), 1, False, s.cuda_stream)
+            s.synchronize()
+            for o in outs:
+                if rel(o.cpu().numpy(), want) > TOL:
+                    errors.append((i, rel(o.cpu().numpy(), want)))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
