@@ -252,7 +252,7 @@ class DevicePlan:
             self._h = None
 
     def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3,
-                  compress=True, lite=None, chain=True):
+                  compress=True, lite=None, chain=True, coop=None):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
@@ -266,11 +266,17 @@ class DevicePlan:
         set_flags() alone restores a new plan's flags (0x3F | 1 << 17, the
         bench's default flags 131135).  chain: consecutive single-RHS applies
         on one stream launch as programmatic dependents (k1_flow streams its
-        first panels while the previous apply drains; bit 17, default on)."""
+        first panels while the previous apply drains; bit 17, default on).
+        coop: the CTA-per-strip kernel k1_coop for single-RHS applies (True,
+        bit 18), never (False, bit 19), or by size (None: small plans)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         if chain:
             f |= 1 << 17
+        if coop is True:
+            f |= 1 << 18
+        elif coop is False:
+            f |= 1 << 19
         if lite is True:
             f |= 1024
         elif lite is False and compress:

@@ -50,6 +50,7 @@
 #include "flow.cuh"
 #include "k2.cuh"
 #include "k2flow.cuh"
+#include "coop.cuh"
 
 namespace midbf::dev {
 
@@ -840,6 +841,8 @@ void Plan::build_direction(int d, const PlanTables& T, const double2* d_raw,
           st.xcols += sg.n;
         }
         D.max_seg = std::max(D.max_seg, static_cast<int>(st.nseg));
+        D.max_xcols = std::max(D.max_xcols, static_cast<int>(st.xcols));
+        D.max_strip_bytes = std::max<int64_t>(D.max_strip_bytes, int64_t{16} * st.h * st.xcols);
         strips.push_back(st);
       }
     }
@@ -975,6 +978,16 @@ Plan::Plan(const PlanTables& T, unsigned directions, double2* d_raw_in) {
   flow_grid[1] = flow_setup<8, 2, 8192>(num_sms);
   flow_grid[2] = flow_grid[1];  // variant 2 (6 pairs x 3 x 8 KB) retired: it deadlocked at cfg3
   flow_grid[3] = flow_grid[0];  // unused: variant 3 resolves per direction (flow_variant)
+  {
+    cuda_check(cudaFuncSetAttribute(k1_coop<kCoopWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kCoopSmem)),
+               "coop smem attribute");
+    int per_sm = 0;
+    cuda_check(
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1_coop<kCoopWarps>, kCoopWarps * 32, kCoopSmem),
+        "occupancy");
+    coop_grid = std::min(per_sm * num_sms, kMaxFlowCtas);
+  }
   cuda_check(cudaFuncSetAttribute(k2_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kK2Smem)),
              "k2 smem attribute");
   k2flow_grid[0] = k2flow_setup<1>(num_sms);  // 16-wide tiles
@@ -1060,6 +1073,26 @@ bool Plan::flow_lite(int d) const {
   return bytes < (int64_t{200} << 20);
 }
 
+// k1_coop for small plans (coop.cuh): dense strip records, x windows of at
+// most kCoopX entries.  Default below kCoopBytes of panels (measured, DESIGN.md
+// "small plans"); flag bit 18 forces it, bit 19 forbids it.
+// cfg0 (7.6 MB, L2-resident): k1_flow 14.5 us, k1_coop 9.4 us; at cfg1_unitxi
+// (145 MB) k1_coop streams far below k1_flow (115 vs 33.6 us): it has one
+// strip in flight per SM and no warp specialisation.
+constexpr int64_t kCoopBytes = int64_t{32} << 20;
+bool Plan::coop(int d) const {
+  if (flags & kFlagNoCoop) return false;
+  if (dir[d].max_xcols > kCoopX || dir[d].max_strip_bytes > kCoopSlotBytes || coop_grid <= 0 || !dir[d].d_ctx)
+    return false;
+  if (flags & kFlagCoop) return true;
+  // by size only on the fully default path: an explicit k1_flow layout
+  // (variant bits), dense-only (bit 10) or compressed (bit 16) choice wins
+  if (((flags >> 4) & 3u) != 3u || (flags & (1024u | 65536u))) return false;
+  int64_t bytes = 0;
+  for (const auto& st : dir[d].stages) bytes += st.payload_bytes;
+  return bytes < kCoopBytes;
+}
+
 bool Plan::flow_dense(int d) const { return !dir[d].d_fctx || (flags & 512u) || flow_lite(d); }
 
 // Up to kFlowColumns right-hand sides run k1_flow once per column: at cfg1 a
@@ -1125,6 +1158,24 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.in_perm = d == 0 ? d_col_perm : d_row_perm;
   P.in_len = D.in_len;
   P.pdl = (flags & kFlagChain) ? 1 : 0;
+  if (coop(d)) {
+    P.ctxs = static_cast<const StripCtx*>(D.d_ctx);  // dense records
+    P.nwarps = coop_grid;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(coop_grid), 1, 1);
+    cfg.blockDim = dim3(kCoopWarps * 32, 1, 1);
+    cfg.dynamicSmemBytes = kCoopSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = P.pdl ? 0 : 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cuda_check(cudaLaunchKernelEx(&cfg, k1_coop<kCoopWarps>, P), "k1_coop launch");
+    return;
+  }
   switch (variant) {
     case 1:
     case 2:  // retired variant: runs variant 1
@@ -1313,7 +1364,7 @@ void Plan::launch(int d, const double2* in, double2* out, int64_t nrhs, cudaStre
 // assume one grid size; a variant switch re-initialises them, outside any
 // stream capture and after all earlier work.
 void Plan::prepare_flow(int d) {
-  const int grid = flow_grid[flow_variant(d)];
+  const int grid = coop(d) ? (coop_grid | (1 << 20)) : flow_grid[flow_variant(d)];
   if (last_grid[d] == grid) return;
   Direction& D = dir[d];
   cuda_check(cudaDeviceSynchronize(), "flow reset sync");

@@ -17,6 +17,10 @@ constexpr int kMaxStages = 64;
 // Plan flag bit 17: chain consecutive single-RHS k1_flow applies on one stream
 // with programmatic dependent launch (no graph, no same-stream event wait).
 constexpr unsigned kFlagChain = 1u << 17;
+// bits 18 / 19: force / forbid k1_coop (CTA-per-strip kernel, coop.cuh) for
+// single-RHS applies; by default it runs below kCoopBytes of panels.
+constexpr unsigned kFlagCoop = 1u << 18;
+constexpr unsigned kFlagNoCoop = 1u << 19;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 
@@ -85,6 +89,8 @@ struct Direction {
   unsigned* d_sync = nullptr;     // per-CTA apply epochs (kMaxFlowCtas)
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
   int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
+  int max_xcols = 0;  // widest x window of a strip (k1_coop needs <= kCoopX)
+  int64_t max_strip_bytes = 0;  // largest panel payload of one strip (k1_coop: <= one slot)
   int64_t in_len = 0;  // input length of the first stage (head of the stage buffers)
   // k2_flow (multi-RHS dataflow): per-stage outputs for one 64-RHS slice,
   // per-strip completion counters, per-CTA launch epochs; allocated on first use
@@ -141,6 +147,8 @@ class Plan {
   unsigned flags = 0x3F | kFlagChain;
   std::vector<GraphEntry> graphs;
   int flow_grid[4] = {0, 0, 0, 0};
+  int coop_grid = 0;  // persistent CTAs of k1_coop (small plans, coop.cuh)
+  bool coop(int d) const;
   int strip_rows = 32;  // output rows per strip (one warp's lanes)
   long long* d_prof = nullptr;  // k1_flow phase timers (flag bit 12)
   int64_t launches_per_apply(int d, int64_t nrhs) const;

@@ -97,7 +97,7 @@ def test_multi_rhs_fallback_paths(pair, path):
     assert rel(default, want) <= TOL
 
 
-@pytest.mark.parametrize("variant", [0, 1, "stages"])
+@pytest.mark.parametrize("variant", [0, 1, "stages", "coop", "coop_nochain"])
 def test_single_rhs_kernel_variants(pair, variant):
     """Every k1_flow layout (the size-based default picks 0 or 1) and the
     per-stage fallback (k1_stage) match the oracle, both directions."""
@@ -106,8 +106,12 @@ def test_single_rhs_kernel_variants(pair, variant):
     try:
         if variant == "stages":
             plan.set_flags(flow=False)
+        elif variant == "coop":
+            plan.set_flags(coop=True)
+        elif variant == "coop_nochain":
+            plan.set_flags(coop=True, chain=False)
         else:
-            plan.set_flags(variant=variant)
+            plan.set_flags(variant=variant, coop=False)
         a, b = plan.apply(f), plan.apply(g, transpose=True)
     finally:
         plan.reset_flags()

@@ -44,7 +44,8 @@ def test_back_to_back_applies_are_bitwise_stable(plan_case, transpose):
     total = 0
     try:
         for kw in (dict(variant=0, lite=False), dict(variant=1, lite=False), dict(variant=0, lite=True),
-                   dict(variant=1, lite=True), dict(), dict(chain=False), dict(chain=False, variant=1, lite=False)):
+                   dict(variant=1, lite=True), dict(), dict(chain=False), dict(chain=False, variant=1, lite=False),
+                   dict(coop=True), dict(coop=True, chain=False)):
             plan.set_flags(**kw)
             ref = [torch.empty(nout, dtype=torch.complex128, device="cuda") for _ in range(2)]
             for i in range(2):
@@ -65,4 +66,4 @@ def test_back_to_back_applies_are_bitwise_stable(plan_case, transpose):
             assert not bad, (kw, bad[:8])
     finally:
         plan.reset_flags()
-    assert total >= 7 * REPS
+    assert total >= 9 * REPS
