@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
     const bool live = lane < h;
     const StageIO io = P.st[C.s.stage];
     const double2* xin = io.x + (io.x_par ? par_off : 0);
-    double2* yout = io.y + (io.y_par ? par_off : 0);
+    double2* yout = io.y ? io.y + (io.y_par ? par_off : 0) : P.out;
     // x window (polled; stage 0 reads the permuted input the same way)
     for (int kk = tid; kk < xcols; kk += NT) {
       int j = 0, c = kk;

@@ -75,7 +75,11 @@ struct FlowParams {
   long long* prof;  // phase timers of the PROF instantiation
   const int* wmap;  // wide compressed strips: kept columns, then add columns (StripCtx::wbase)
   int pdl;          // launched as a programmatic dependent of the previous apply (see k1_flow)
-  StageIO st[kMaxStages];
+  // per-stage inputs / outputs, a device table built with the plan (the
+  // launch parameters stay small: they are copied on every launch); the last
+  // stage has y == nullptr and writes `out`
+  const StageIO* st;
+  double2* out;
 };
 
 // A panel as k1_flow streams it.
@@ -638,7 +642,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
       const double2* xin = io.x + (io.x_par ? par_off : 0);
-      double2* yout = io.y + (io.y_par ? par_off : 0);
+      double2* yout = io.y ? io.y + (io.y_par ? par_off : 0) : P.out;
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + (k & 1) * kXWin;
       const unsigned long long g_ctx = PROF ? globaltimer_ns() : 0;

@@ -1016,6 +1016,7 @@ Plan::~Plan() {
     cudaFree(D.d_k2done);
     cudaFree(D.d_k2epoch);
     cudaFree(D.d_stagebuf);
+    cudaFree(D.d_stageio);
     cudaFree(D.d_sync);
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
@@ -1127,6 +1128,29 @@ void Plan::ensure_buffers(int64_t nrhs) {
   }
 }
 
+// The k1_flow / k1_coop stage table (FlowParams::st) on the device, once per
+// direction, outside any stream capture.
+void Plan::ensure_stageio(int d) {
+  Direction& D = dir[d];
+  if (!D.d_stageio) {
+    const int ns = static_cast<int>(D.stages.size());
+    std::vector<StageIO> st(static_cast<size_t>(ns));
+    for (int s = 0; s < ns; ++s) {
+      StageIO& io = st[static_cast<size_t>(s)];
+      io.x = s == 0 ? D.d_stagebuf : D.d_stagebuf + D.stages[s - 1].buf_off;  // stage 0: permuted input
+      io.y = s == ns - 1 ? nullptr : D.d_stagebuf + D.stages[s].buf_off;   // last stage: FlowParams::out
+      io.xperm = nullptr;
+      io.yperm = s == ns - 1 ? (d == 0 ? d_row_perm : d_col_perm) : nullptr;
+      io.x_par = 1;
+      io.y_par = s == ns - 1 ? 0 : 1;
+    }
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(16, st.size() * sizeof(StageIO))), "cudaMalloc stage table");
+    cuda_check(cudaMemcpy(p, st.data(), st.size() * sizeof(StageIO), cudaMemcpyHostToDevice), "upload stage table");
+    D.d_stageio = static_cast<StageIO*>(p);
+  }
+}
+
 void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stream) {
   Direction& D = dir[d];
   const int variant = flow_variant(d);
@@ -1144,16 +1168,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.nstrips = static_cast<int>(D.nstrips);
   P.nodeps = static_cast<int>((flags >> 6) & 7u);  // bits 6-8: timing experiments
   if ((flags & 4096u) && d_prof) P.prof = d_prof;  // bit 12: phase timers (experiments)
-  const int ns = static_cast<int>(D.stages.size());
-  for (int s = 0; s < ns; ++s) {
-    StageIO& io = P.st[s];
-    io.x = s == 0 ? D.d_stagebuf : D.d_stagebuf + D.stages[s - 1].buf_off;  // stage 0: permuted input
-    io.y = s == ns - 1 ? out : D.d_stagebuf + D.stages[s].buf_off;
-    io.xperm = nullptr;
-    io.yperm = s == ns - 1 ? (d == 0 ? d_row_perm : d_col_perm) : nullptr;
-    io.x_par = 1;
-    io.y_par = s == ns - 1 ? 0 : 1;
-  }
+  P.st = D.d_stageio;
+  P.out = out;
   P.in = in;
   P.in_perm = d == 0 ? d_col_perm : d_row_perm;
   P.in_len = D.in_len;
@@ -1409,7 +1425,10 @@ void Plan::apply_device(int d, const double2* in, double2* out, int64_t nrhs, cu
     return;
   }
   ensure_buffers(nrhs);
-  if (flow_ok(d, nrhs)) prepare_flow(d);
+  if (flow_ok(d, nrhs)) {
+    prepare_flow(d);
+    ensure_stageio(d);
+  }
   if (k2flow_ok(d, nrhs)) ensure_k2flow(d);
   // after the previous apply on this plan, whichever stream it ran on
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

@@ -12,6 +12,7 @@
 namespace midbf::dev {
 
 struct StripCtx;
+struct StageIO;
 
 constexpr int kMaxStages = 64;
 // Plan flag bit 17: chain consecutive single-RHS k1_flow applies on one stream
@@ -86,6 +87,7 @@ struct Direction {
   int64_t farena_elems = 0;       // compressed panels, stored behind the dense ones in d_arena
   int64_t ncols_total = 0;        // panel columns over all segments (plan build)
   double2* d_stagebuf = nullptr;  // outputs of every stage but the last, two parity sets
+  StageIO* d_stageio = nullptr;   // k1_flow / k1_coop stage table (built on the first launch)
   unsigned* d_sync = nullptr;     // per-CTA apply epochs (kMaxFlowCtas)
   int64_t nstrips = 0, nsegs = 0, arena_elems = 0, stagebuf_elems = 0;
   int max_seg = 0;  // most panels feeding one strip (k1_flow needs <= kMaxSeg)
@@ -149,6 +151,7 @@ class Plan {
   int flow_grid[4] = {0, 0, 0, 0};
   int coop_grid = 0;  // persistent CTAs of k1_coop (small plans, coop.cuh)
   bool coop(int d) const;
+  void ensure_stageio(int d);
   int strip_rows = 32;  // output rows per strip (one warp's lanes)
   long long* d_prof = nullptr;  // k1_flow phase timers (flag bit 12)
   int64_t launches_per_apply(int d, int64_t nrhs) const;
