@@ -40,6 +40,9 @@ FP64_DFMA_TFLOPS = 36.7
 # ncu SASS thread counters over whole factorizations divided by the entries
 # they sampled; profiles/r1_k3_sample.md), by kernel kind.
 K3_FLOPS_PER_ENTRY = {"fio2d": 66.0, "fio3d": 71.0, "lowrank": 60.0}
+# K4 direct sum, FIO 2D: 2*DFMA + DMUL + DADD per entry = 2*20 + 19 + 15 from
+# ncu SASS counters of an 8192 x 65536 sum (profiles/r2_k4.md)
+K4_FLOPS_PER_ENTRY = {"fio2d": 74.0}
 
 
 def peaks():
@@ -273,9 +276,27 @@ def accuracy(M, K, F, fk, f):
     Fh = M.idbf_factorize(K, fk["n0"], k=fk["k"], eps=1e-9, t=5, seed=M.chain(0, 0x666163), sampler="host",
                           ids="host")
     e_host = K.eps_b(Fh.apply(f), f, nrows=256, seed=seed)
-    return {"eps_b_device_sampled": e_dev, "eps_b_host_sampled": e_host, "rows": 256,
-            "rows_seed": "chain(0, 0x657062)", "direct_sum": "K4 on the GPU",
-            "host_sampled_total_nnz": Fh.total_nnz, "seconds": time.perf_counter() - t0}
+    out = {"eps_b_device_sampled": e_dev, "eps_b_host_sampled": e_host, "rows": 256,
+           "rows_seed": "chain(0, 0x657062)", "direct_sum": "K4 on the GPU",
+           "host_sampled_total_nnz": Fh.total_nnz, "seconds": time.perf_counter() - t0}
+    # K4 throughput on a large direct sum (min(8192, N) rows x N columns)
+    nsel = min(8192, F.nrows)
+    rows = np.arange(nsel, dtype=np.int64)
+    K.direct_sum(f, rows[:256])
+    best = 1e9
+    for _ in range(3):
+        t1 = time.perf_counter()
+        K.direct_sum(f, rows)
+        best = min(best, time.perf_counter() - t1)
+    ent = nsel * F.ncols
+    kind = {M.KIND_FIO2D: "fio2d", M.KIND_FIO3D: "fio3d", M.KIND_LOWRANK: "lowrank"}.get(K.desc.kind)
+    fpe = K4_FLOPS_PER_ENTRY.get(kind)
+    out["k4_direct_sum"] = {"entries": ent, "seconds": best, "entries_per_s": ent / best,
+                            "fp64_tflops": ent / best * fpe / 1e12 if fpe else None,
+                            "fp64_frac": ent / best * fpe / 1e12 / FP64_DFMA_TFLOPS if fpe else None,
+                            "note": "wall time of midbf_direct_sum (uploads + K4 + reduce + D2H); ncu: 78.8% FP64 "
+                                    "pipe at cfg1 (profiles/r2_k4.md)"}
+    return out
 
 
 def main():

@@ -119,6 +119,23 @@ __device__ __forceinline__ void polar1x2(double phi0, double phi1, double2* e0, 
   *e1 = make_double2(c1, s1);
 }
 
+// Four independent arguments (K4: more Horner chains in flight per warp,
+// dependent DFMA latency 17 cycles measured, tools/lat_probe.cu).
+__device__ __forceinline__ void polar1x4(const double (&phi)[4], double2 (&e)[4]) {
+  double x[4], s[4], c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = __dmul_rn(kSC[17], phi[i]);
+  if (fabs(x[0]) < 1.0e6 && fabs(x[1]) < 1.0e6 && fabs(x[2]) < 1.0e6 && fabs(x[3]) < 1.0e6) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sincos_fast(x[i], &s[i], &c[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sincos_lean(x[i], &s[i], &c[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) e[i] = make_double2(c[i], s[i]);
+}
+
 __device__ __forceinline__ double2 polar1(double phi) {
   double s, c;
   sincos_lean(__dmul_rn(kSC[17], phi), &s, &c);
@@ -459,7 +476,16 @@ __global__ void __launch_bounds__(256) k4_direct_s(DevK k, const int* __restrict
         ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(e.x, x.y), __dmul_rn(e.y, x.x)));
       };
       int q = 0;
-      for (; q + 1 < cn; q += 2) {  // two entries' sincos interleaved, accumulated in column order
+      for (; q + 3 < cn; q += 4) {  // four entries' sincos interleaved, accumulated in column order
+        double ph[4];
+        double2 e[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ph[i] = O::phase(k, sR + threadIdx.x, kT, sC + q + i, kT);
+        polar1x4(ph, e);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mac(e[i], fs[q + i]);
+      }
+      for (; q + 1 < cn; q += 2) {  // two entries' sincos interleaved
         double2 e0, e1;
         polar1x2(O::phase(k, sR + threadIdx.x, kT, sC + q, kT), O::phase(k, sR + threadIdx.x, kT, sC + q + 1, kT),
                  &e0, &e1);
