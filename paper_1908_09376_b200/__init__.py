@@ -27,7 +27,9 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmidbf_b200.so")
+# MIDBF_LIB selects another build of the library (the checked build of
+# tests/test_gpu_checked.py); default: the in-tree release build
+LIB_PATH = os.environ.get("MIDBF_LIB") or os.path.join(_HERE, "libmidbf_b200.so")
 
 KIND_FIO2D, KIND_FIO3D, KIND_LOWRANK, KIND_NUFFT, KIND_CONST, KIND_RANK1 = range(6)
 MIDBF_OK, MIDBF_EINVAL, MIDBF_ELOGIC, MIDBF_ERUNTIME, MIDBF_ECUDA = 0, -1, -2, -3, -4

@@ -8,6 +8,29 @@
 
 #include "../status.hpp"
 
+// Checked builds (make checked -> libmidbf_b200_checked.so, -DMIDBF_CHECKED):
+// device-side bounds assertions on every table-driven access of the apply
+// kernels (arena ranges of the panel copies, stage-buffer / output indices,
+// shared-memory slot sizes).  A violation prints its site and traps, which
+// fails the launch with an error instead of reading or writing out of
+// bounds.  This pool closes compute-sanitizer, so the checked build run over
+// the small parity cases (tests/test_gpu_checked.py) stands in for memcheck.
+#ifdef MIDBF_CHECKED
+#include <cstdio>
+#define MIDBF_DCHECK(cond, what)                                                                       \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("MIDBF_CHECKED violation: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,     \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                              \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define MIDBF_DCHECK(cond, what) \
+  do {                           \
+  } while (0)
+#endif
+
 namespace midbf::dev {
 
 inline void cuda_check(cudaError_t e, const char* what) {

@@ -73,8 +73,11 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
     mbar_expect_tx(&full[s], static_cast<unsigned>(bytes));
     bulk_g2s(&ctx[s], src, sizeof(StripCtx), &full[s]);
     unsigned char* dst = slots + size_t(s) * kCoopSlotBytes;
+    MIDBF_DCHECK(bytes - static_cast<int64_t>(sizeof(StripCtx)) <= kCoopSlotBytes, "k1_coop strip exceeds its slot");
     for (int j = 0; j < nseg; ++j) {
       const unsigned b = static_cast<unsigned>(h * __ldg(&src->g[j].n) * 16);
+      MIDBF_DCHECK(__ldg(&src->g[j].off) >= 0 && __ldg(&src->g[j].off) + b / 16 <= P.arena_len,
+                   "k1_coop panel outside the arena");
       bulk_g2s(dst, P.arena + __ldg(&src->g[j].off), b, &full[s]);
       dst += b;
     }
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
       int j = 0, c = kk;
       while (j < nseg - 1 && c >= C.g[j].n) c -= C.g[j].n, ++j;
       const double2* p = xin + C.g[j].x0 + c;
+      MIDBF_DCHECK(kk < kCoopX && p >= P.stagebuf && p < P.stagebuf + 2 * P.par_elems, "k1_coop x gather");
       double2 v = ld_cg(p);
       while (is_sentinel(v)) v = ld_cg(p);
       xs[kk] = v;
@@ -140,6 +144,9 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
       }
       int yidx = C.s.y0 + lane;
       if (io.yperm) yidx = io.yperm[yidx];
+      MIDBF_DCHECK(io.y ? (yout + yidx >= P.stagebuf && yout + yidx < P.stagebuf + 2 * P.par_elems)
+                        : (yidx >= 0 && yidx < P.out_len),
+                   "k1_coop row store outside its buffer");
       st_signal(yout + yidx, make_double2(unsentinel(yr), unsentinel(yi)));
     }
     __syncthreads();  // slot s, xs and red are rewritten next

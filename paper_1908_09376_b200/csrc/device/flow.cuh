@@ -34,6 +34,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "common.cuh"
 #include "plan.hpp"
 
 namespace midbf::dev {
@@ -80,6 +81,8 @@ struct FlowParams {
   // stage has y == nullptr and writes `out`
   const StageIO* st;
   double2* out;
+  int64_t arena_len;  // complex entries of the arena (checked builds)
+  int64_t out_len;    // entries of `out` (checked builds)
 };
 
 // A panel as k1_flow streams it.
@@ -316,7 +319,8 @@ __device__ __forceinline__ void store_x_regs(const StripCtx& c, const double2* v
 // polls until none is a sentinel; no warp-collective ops inside, so the
 // producer's lane 0 can run the TMA issue loop concurrently.
 template <int NS, bool CMP>  // stager lanes, identity-compressed records possible
-__device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst, int sl) {
+__device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst, int sl,
+                                        const double2* xbase_lo = nullptr, const double2* xbase_hi = nullptr) {
   constexpr int kPer = (kXWin + NS - 1) / NS;
   int idx[kPer];
 #pragma unroll
@@ -343,6 +347,9 @@ __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, con
     }
   }
   double2 v[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i)
+    MIDBF_DCHECK(idx[i] < 0 || (xbase_lo <= x + idx[i] && x + idx[i] < xbase_hi), "k1_flow x gather outside the stage buffers");
 #pragma unroll
   for (int i = 0; i < kPer; ++i)
     if (idx[i] >= 0) v[i] = xperm ? __ldg(x + __ldg(xperm + idx[i])) : ld_cg(x + idx[i]);
@@ -526,7 +533,8 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
-        FLOW_T(13, stage_x<NS, CMP>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl));
+        FLOW_T(13, stage_x<NS, CMP>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl, P.stagebuf,
+                                    P.stagebuf + 2 * P.par_elems));
         if (CMP && kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
           // (separate stager warps only; with the in-warp stager of FW > 4
           // the consumers sum in place)
@@ -581,6 +589,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
           } else {
             fence_proxy_async();
             mbar_expect_tx(&cfull[sc], sizeof(StripCtx));
+            MIDBF_DCHECK(gw + static_cast<int64_t>(kf) * P.nwarps < P.nstrips, "k1_flow strip record index");
             bulk_g2s(&ctx[sc], P.ctxs + gw + static_cast<int64_t>(kf) * P.nwarps, sizeof(StripCtx), &cfull[sc]);
           }
           ++kf;
@@ -604,6 +613,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             FLOW_T(1, mbar_wait(&empty[slot], ((q / FS) & 1) ^ 1));
             fence_proxy_async();
             const unsigned bytes = static_cast<unsigned>(h * ncol * 16);
+            MIDBF_DCHECK(bytes <= SLOT, "k1_flow panel chunk exceeds its slot");
+            MIDBF_DCHECK(C.g[j].off >= 0 && C.g[j].off + static_cast<int64_t>(col + ncol) * h <= P.arena_len,
+                         "k1_flow panel outside the arena");
             mbar_expect_tx(&full[slot], bytes);
             bulk_g2s(slots + size_t(slot) * SLOT, src + static_cast<int64_t>(col) * h, bytes, &full[slot]);
             prefetch(false);
@@ -763,6 +775,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       // The stored value is the readiness signal of this row: never let a
       // result alias the "not yet written" sentinel.
+      MIDBF_DCHECK(!(row < h && cpar == 0) || (io.y ? (yout + yidx >= P.stagebuf && yout + yidx < P.stagebuf + 2 * P.par_elems)
+                                                    : (yidx >= 0 && yidx < P.out_len)),
+                   "k1_flow row store outside its buffer");
       FLOW_T(7, if (row < h && cpar == 0) st_signal(yout + yidx, make_double2(unsentinel(yr), unsentinel(yi))));
       if (PROF && lane == 0 && C.s.seg0 < kProfStrips) {  // per-strip timeline (ns): ctx ready, x staged, stored
         long long* ts = P.prof + kProfStripBase + 3 * static_cast<int64_t>(C.s.seg0);

@@ -91,6 +91,7 @@ struct K2FParams {
   // timing experiments only (flag bits 14-15), results invalid: 1 skip the
   // dependency waits, 2 stream only (no math), 3 math only (no loads)
   int mode;
+  int64_t arena_len;  // complex entries of the arena (checked builds)
   K2FStage st[kMaxStages];
 };
 
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
           __syncwarp();
           if (load) {
             if (!prun) {
+              MIDBF_DCHECK(!(ok && lane < kK2Kc) || (psrc >= 0 && psrc + h <= P.arena_len), "k2_flow panel column");
               if (ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
             } else {
               unsigned r = runs;
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
                 r &= r - 1;
                 const int r1 = r ? __ffs(r) - 1 : kval;
                 const int64_t src = __shfl_sync(0xffffffffu, psrc, r0);
+                MIDBF_DCHECK(lane != 0 || (src >= 0 && src + int64_t(r1 - r0) * h <= P.arena_len), "k2_flow panel run");
                 if (lane == 0) flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
               }
             }

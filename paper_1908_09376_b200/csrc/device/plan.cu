@@ -1173,6 +1173,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.in = in;
   P.in_perm = d == 0 ? d_col_perm : d_row_perm;
   P.in_len = D.in_len;
+  P.arena_len = D.arena_elems + D.farena_elems;
+  P.out_len = d == 0 ? nrows : ncols;
   P.pdl = (flags & kFlagChain) ? 1 : 0;
   if (coop(d)) {
     P.ctxs = static_cast<const StripCtx*>(D.d_ctx);  // dense records
@@ -1297,6 +1299,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   const bool comp = D.d_k2strips && !(flags & 512u);
   P.xmap = D.d_k2xmap;
   P.addx = D.d_k2addx;
+  P.arena_len = D.arena_elems + D.farena_elems;
   P.arena = D.d_arena;
   P.done = D.d_k2done;
   P.epoch = D.d_k2epoch;

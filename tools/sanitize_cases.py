@@ -28,9 +28,11 @@ def run(name, kind, X, Om, n0, k):
     worst = 0.0
     f, g = cvec(Fo.ncols, 1), cvec(Fo.nrows, 2)
     for kw in (dict(variant=0, lite=False), dict(variant=1, lite=False), dict(variant=0, lite=True),
-               dict(flow=False), dict()):
+               dict(flow=False), dict(), dict(chain=False), dict(coop=True), dict(coop=True, chain=False)):
         plan.set_flags(**kw)
-        worst = max(worst, rel(plan.apply(f), Fo.apply(f)), rel(plan.apply(g, transpose=True), Fo.apply_transpose(g)))
+        for _ in range(3):  # consecutive applies alternate the stage-buffer parity sets
+            worst = max(worst, rel(plan.apply(f), Fo.apply(f)),
+                        rel(plan.apply(g, transpose=True), Fo.apply_transpose(g)))
     for nrhs in (8, 70):
         Xm = cvec(Fo.ncols, 3, cols=nrhs)
         worst = max(worst, rel(plan.apply(Xm), Fo.apply(Xm)))
