@@ -285,17 +285,16 @@ def accuracy(M, K, F, fk, f):
     K.direct_sum(f, rows[:256])
     best = 1e9
     for _ in range(3):
-        t1 = time.perf_counter()
         K.direct_sum(f, rows)
-        best = min(best, time.perf_counter() - t1)
+        best = min(best, K.last_direct_sum_seconds())
     ent = nsel * F.ncols
     kind = {M.KIND_FIO2D: "fio2d", M.KIND_FIO3D: "fio3d", M.KIND_LOWRANK: "lowrank"}.get(K.desc.kind)
     fpe = K4_FLOPS_PER_ENTRY.get(kind)
     out["k4_direct_sum"] = {"entries": ent, "seconds": best, "entries_per_s": ent / best,
                             "fp64_tflops": ent / best * fpe / 1e12 if fpe else None,
                             "fp64_frac": ent / best * fpe / 1e12 / FP64_DFMA_TFLOPS if fpe else None,
-                            "note": "wall time of midbf_direct_sum (uploads + K4 + reduce + D2H); ncu: 78.8% FP64 "
-                                    "pipe at cfg1 (profiles/r2_k4.md)"}
+                            "note": "device time (CUDA events) of K4 + its fixed-order reduction, best of 3; "
+                                    "ncu: 78.8% FP64 pipe at cfg1 (profiles/r2_k4.md)"}
     return out
 
 

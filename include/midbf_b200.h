@@ -130,6 +130,9 @@ int midbf_sample(const midbf_kernel_desc* kernel, int64_t ntasks, const int64_t*
  * dense_matvec (tests/test_butterfly.cpp:29-37).  Host pointers. */
 int midbf_direct_sum(const midbf_kernel_desc* kernel, const double* f, const int64_t* rows, int64_t nsel,
                      double* g);
+/* Device seconds (CUDA events around K4 and its fixed-order reduction) of the
+ * calling thread's last midbf_direct_sum. */
+int midbf_last_direct_sum_seconds(double* out);
 
 /* ----------------------------------------- batched interpolative decompositions
  * Column IDs of explicit blocks on the GPU (K5): la::cid_from_rows

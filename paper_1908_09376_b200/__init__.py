@@ -183,6 +183,13 @@ class Kernel:
         _check(lib().midbf_direct_sum(C.byref(self.desc), _p(f.view(np.float64)), rp, i64(n), _p(g.view(np.float64))))
         return g
 
+    @staticmethod
+    def last_direct_sum_seconds():
+        """Device seconds of this thread's last direct_sum (K4 + reduction)."""
+        out = C.c_double()
+        _check(lib().midbf_last_direct_sum_seconds(C.byref(out)))
+        return out.value
+
     def eps_b(self, g_b, f, nrows=256, seed=0):
         """metrics::eps_b_of (src/metrics.cpp:26-48), direct sum on the GPU."""
         N = len(g_b)

@@ -1088,6 +1088,13 @@ void EntrySampler::phase_block(int64_t nr, const int64_t* rows, int64_t nc, cons
   cuda_check(e, "phase block");
 }
 
+// Device time of the calling thread's last direct sum (K4 + its fixed-order
+// reduction, CUDA events), for throughput reporting.
+double& last_direct_sum_seconds() {
+  thread_local double s = 0.0;
+  return s;
+}
+
 void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel, double* g) {
   Impl& I = *impl_;
   if (nsel == 0) return;
@@ -1110,10 +1117,21 @@ void EntrySampler::direct_sum(const double* f, const int64_t* rows, int64_t nsel
   double2 *d_part = nullptr, *d_g = nullptr;
   cuda_check(cudaMalloc(&d_part, nsplit * nsel * sizeof(double2)), "cudaMalloc partial");
   cuda_check(cudaMalloc(&d_g, nsel * sizeof(double2)), "cudaMalloc g");
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cuda_check(cudaEventRecord(e0, 0), "event");
   launch_k4(I.k, dim3(rb, static_cast<unsigned>(nsplit)), 0, d_rows, static_cast<int>(nsel), d_f, I.ncols, cps, d_part);
   cuda_check(cudaGetLastError(), "k4_direct launch");
   k4_reduce<<<rb, 256>>>(d_part, static_cast<int>(nsel), static_cast<int>(nsplit), d_g);
   cuda_check(cudaGetLastError(), "k4_reduce launch");
+  cuda_check(cudaEventRecord(e1, 0), "event");
+  cuda_check(cudaEventSynchronize(e1), "event");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  last_direct_sum_seconds() = 1e-3 * ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   cuda_check(cudaMemcpy(g, d_g, nsel * sizeof(double2), cudaMemcpyDeviceToHost), "direct sum D2H");
   cudaFree(d_part);
   cudaFree(d_g);
@@ -1191,6 +1209,10 @@ extern "C" int midbf_direct_sum(const midbf_kernel_desc* kernel, const double* f
     midbf::dev::EntrySampler s(*kernel);
     s.direct_sum(f, rows, nsel, g);
   });
+}
+
+extern "C" int midbf_last_direct_sum_seconds(double* out) {
+  return guard([&] { *out = midbf::dev::last_direct_sum_seconds(); });
 }
 
 extern "C" int midbf_device_count(int* out) {

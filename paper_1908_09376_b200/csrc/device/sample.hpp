@@ -57,4 +57,6 @@ class EntrySampler {
   std::unique_ptr<Impl> impl_;
 };
 
+double& last_direct_sum_seconds();  // device time of the thread's last direct sum (K4)
+
 }  // namespace midbf::dev
