@@ -200,16 +200,69 @@ SweepOut sweep(const Filler& fill, const IdFn& ids, const tree::ClusterTree& tx,
   static const bool timing = std::getenv("MIDBF_FACT_TIMING") != nullptr;
   auto tnow = [] { return std::chrono::steady_clock::now(); };
   const auto t_a = tnow();
-  // column samples, one per system (:434-441)
+  // column samples, one per system (:434-441).  Systems with the same column
+  // part sample from the same pool, and the mock-Chebyshev candidate search
+  // (nodes, nearest points) depends on the pool alone, so it runs once per
+  // distinct pool; each system then makes its own picks with its own stream
+  // (the random top-up), exactly as the reference's per-system call.
   std::vector<IndexVec> csamp(static_cast<size_t>(ns));
   const bool par = cfg.exec == Exec::Parallel;
+  {
+    std::vector<IndexVec> pool(static_cast<size_t>(ns));
 #pragma omp parallel for schedule(dynamic) if (par && ns > 1)
-  for (Index s = 0; s < ns; ++s) {
-    IndexVec pool;
-    pool.reserve(static_cast<size_t>(sys[s].col.size));
-    for (const Cell& c : sys[s].col.cells) pool.insert(pool.end(), c.ids.begin(), c.ids.end());
-    std::mt19937_64 rng(mix(mix(salt ^ mix(0x73636f6cull)) ^ mix(static_cast<std::uint64_t>(s))));
-    csamp[s] = pick(pool, Om, want, rng);
+    for (Index s = 0; s < ns; ++s) {
+      pool[s].reserve(static_cast<size_t>(sys[s].col.size));
+      for (const Cell& c : sys[s].col.cells) pool[s].insert(pool[s].end(), c.ids.begin(), c.ids.end());
+    }
+    std::vector<Index> rep(static_cast<size_t>(ns));  // first system with the same pool
+    std::vector<Index> uniq;
+    for (Index s = 0; s < ns; ++s) {
+      rep[s] = s;
+      for (Index u : uniq)
+        if (pool[u] == pool[s]) {
+          rep[s] = u;
+          break;
+        }
+      if (rep[s] == s) uniq.push_back(s);
+    }
+    struct Cand {
+      MatXd C;
+      la::ChebNodes N;
+      std::vector<Index> cand;
+    };
+    std::vector<Cand> cd(static_cast<size_t>(ns));
+    std::vector<std::pair<Index, Index>> node_tasks;  // (pool, node) over every distinct pool
+    for (Index u : uniq) {
+      const IndexVec& pl = pool[u];
+      const Index n = static_cast<Index>(pl.size());
+      if (n <= want) continue;
+      Cand& c = cd[u];
+      c.C = MatXd(n, Om.cols());
+      for (Index i = 0; i < n; ++i)
+        for (Index a = 0; a < Om.cols(); ++a) c.C(i, a) = Om(pl[static_cast<size_t>(i)], a);
+      c.N = la::cheb_nodes(c.C, want);
+      c.cand.resize(static_cast<size_t>(c.N.nodes * la::kChebCand));
+      for (Index t = 0; t < c.N.nodes; ++t) node_tasks.emplace_back(u, t);
+    }
+#pragma omp parallel for schedule(dynamic) if (par && node_tasks.size() > 1)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(node_tasks.size()); ++q) {
+      const auto [u, t] = node_tasks[static_cast<size_t>(q)];
+      Cand& c = cd[u];
+      la::cheb_candidates_node(c.C, c.N, t, c.cand.data() + t * la::kChebCand);
+    }
+#pragma omp parallel for schedule(dynamic) if (par && ns > 1)
+    for (Index s = 0; s < ns; ++s) {
+      const IndexVec& pl = pool[s];
+      if (static_cast<Index>(pl.size()) <= want) {  // the pool unchanged and unsorted (:362)
+        csamp[s] = pl;
+        continue;
+      }
+      std::mt19937_64 rng(mix(mix(salt ^ mix(0x73636f6cull)) ^ mix(static_cast<std::uint64_t>(s))));
+      const Cand& c = cd[rep[s]];
+      const IndexVec sel = la::cheb_pick(c.C, want, c.N, c.cand.data(), rng);
+      csamp[s].resize(sel.size());
+      for (size_t i = 0; i < sel.size(); ++i) csamp[s][i] = pl[static_cast<size_t>(sel[i])];
+    }
   }
 
   const auto t_b = tnow();
@@ -496,9 +549,15 @@ Filler device_filler(dev::EntrySampler& smp, FactorizeStats* stats) {
       tasks[5 * q + 4] = 0;
       rid.insert(rid.end(), j.rows, j.rows + j.nr);
       cid.insert(cid.end(), j.cols, j.cols + j.nc);
-      j.out->resize(j.nr, j.nc);
-      outs[q] = reinterpret_cast<double*>(j.out->data());
       total += j.nr * j.nc;
+    }
+    // the destination blocks are allocated (and first touched) in parallel:
+    // cfg1's S blocks are 59 MB of fresh pages, ~20 ms single-threaded
+#pragma omp parallel for schedule(dynamic, 4) if (jobs.size() > 8)
+    for (std::int64_t q = 0; q < static_cast<std::int64_t>(jobs.size()); ++q) {
+      FillJob& j = jobs[static_cast<size_t>(q)];
+      j.out->resize(j.nr, j.nc);
+      outs[static_cast<size_t>(q)] = reinterpret_cast<double*>(j.out->data());
     }
     const auto t0 = std::chrono::steady_clock::now();
     smp.sample_blocks(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(),

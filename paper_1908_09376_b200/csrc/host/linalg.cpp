@@ -16,6 +16,7 @@
 #include <stdexcept>
 
 #include "midbf/linalg.hpp"
+#include "midbf_internal.hpp"
 
 namespace midbf::la {
 namespace {
@@ -179,14 +180,18 @@ RowID rid_from_cols(const MatXc& C, const RankSpec& spec) {
   return r;
 }
 
-IndexVec mock_chebyshev_points(const MatXd& P, Index s, std::mt19937_64& rng) {
+// mock_chebyshev_points (src/linalg.cpp:329-388) in three parts, so that the
+// candidate search (the O(n * c^d) part) can also run on the GPU
+// (EntrySampler::cheb_candidates) with the same arithmetic:
+//   cheb_nodes       c, the bounding box and the tensor nodes (last axis fastest);
+//   cheb_candidates  each node's kChebCand nearest points by (distance, index);
+//   cheb_pick        the picks in node order -- the first untaken candidate is
+//                    the reference's "nearest unused point, first on ties"; a
+//                    full scan when every candidate is taken -- then the random
+//                    top-up and the sort.
+ChebNodes cheb_nodes(const MatXd& P, Index s) {
   const Index n = P.rows(), d = P.cols();
-  IndexVec picked;
-  if (s >= n) {
-    picked.resize(static_cast<size_t>(n));
-    std::iota(picked.begin(), picked.end(), Index{0});
-    return picked;
-  }
+  ChebNodes N;
   Index c = 1;  // largest c with c^d <= s
   while (std::pow(static_cast<double>(c + 1), static_cast<double>(d)) <= static_cast<double>(s)) ++c;
   std::vector<double> mid(static_cast<size_t>(d)), half(static_cast<size_t>(d));
@@ -202,60 +207,74 @@ IndexVec mock_chebyshev_points(const MatXd& P, Index s, std::mt19937_64& rng) {
   const double kPi = 3.14159265358979323846;
   Index nodes = 1;
   for (Index a = 0; a < d; ++a) nodes *= c;
-  std::vector<char> taken(static_cast<size_t>(n), 0);
-  // Node coordinates (last axis varies fastest), as the reference builds them.
-  std::vector<double> nodec(static_cast<size_t>(nodes * d));
+  N.c = c;
+  N.d = d;
+  N.nodes = nodes;
+  N.nodec.resize(static_cast<size_t>(nodes * d));
   for (Index t = 0; t < nodes; ++t) {
     Index rem = t;
     for (Index a = d - 1; a >= 0; --a) {
       const Index j = rem % c;
       rem /= c;
-      nodec[static_cast<size_t>(t * d + a)] = mid[a] + half[a] * std::cos((2.0 * j + 1.0) * kPi / (2.0 * c));
+      N.nodec[static_cast<size_t>(t * d + a)] = mid[a] + half[a] * std::cos((2.0 * j + 1.0) * kPi / (2.0 * c));
     }
   }
-  auto dist_to = [&](Index i, Index t) {
-    double dist = 0.0;
-    for (Index a = 0; a < d; ++a) {
-      const double e = P(i, a) - nodec[static_cast<size_t>(t * d + a)];
-      dist += e * e;
-    }
-    return dist;
-  };
-  // Each node's kCand nearest points by (distance, index), independent of the
-  // picks, in parallel; then the picks in node order take the first untaken
-  // candidate -- the reference's "nearest unused point, first on ties" --
-  // and fall back to a full scan when every candidate is already taken.
-  constexpr Index kCand = 8;
-  std::vector<Index> cand(static_cast<size_t>(nodes * kCand), -1);
-  std::vector<double> cdist(static_cast<size_t>(nodes * kCand), std::numeric_limits<double>::infinity());
-#pragma omp parallel for schedule(dynamic) if (n * nodes >= (Index{1} << 20))
-  for (Index t = 0; t < nodes; ++t) {
-    Index* ci = cand.data() + t * kCand;
-    double* cd = cdist.data() + t * kCand;
-    for (Index i = 0; i < n; ++i) {
-      const double dist = dist_to(i, t);
-      if (!(dist < cd[kCand - 1])) continue;  // ties keep the earlier index
-      Index q = kCand - 1;
-      while (q > 0 && dist < cd[q - 1]) {
-        cd[q] = cd[q - 1];
-        ci[q] = ci[q - 1];
-        --q;
-      }
-      cd[q] = dist;
-      ci[q] = i;
-    }
+  return N;
+}
+
+namespace {
+double cheb_dist(const MatXd& P, const ChebNodes& N, Index i, Index t) {
+  double dist = 0.0;
+  for (Index a = 0; a < N.d; ++a) {
+    const double e = P(i, a) - N.nodec[static_cast<size_t>(t * N.d + a)];
+    dist += e * e;
   }
+  return dist;
+}
+}  // namespace
+
+void cheb_candidates_node(const MatXd& P, const ChebNodes& N, Index t, Index* ci) {
+  const Index n = P.rows();
+  double cd[kChebCand];
+  for (Index q = 0; q < kChebCand; ++q) {
+    cd[q] = std::numeric_limits<double>::infinity();
+    ci[q] = -1;
+  }
+  for (Index i = 0; i < n; ++i) {
+    const double dist = cheb_dist(P, N, i, t);
+    if (!(dist < cd[kChebCand - 1])) continue;  // ties keep the earlier index
+    Index q = kChebCand - 1;
+    while (q > 0 && dist < cd[q - 1]) {
+      cd[q] = cd[q - 1];
+      ci[q] = ci[q - 1];
+      --q;
+    }
+    cd[q] = dist;
+    ci[q] = i;
+  }
+}
+
+void cheb_candidates(const MatXd& P, const ChebNodes& N, Index* cand) {
+#pragma omp parallel for schedule(dynamic) if (P.rows() * N.nodes >= (Index{1} << 20))
+  for (Index t = 0; t < N.nodes; ++t) cheb_candidates_node(P, N, t, cand + t * kChebCand);
+}
+
+IndexVec cheb_pick(const MatXd& P, Index s, const ChebNodes& N, const Index* cand, std::mt19937_64& rng) {
+  const Index n = P.rows(), nodes = N.nodes;
+  std::vector<char> taken(static_cast<size_t>(n), 0);
+  IndexVec picked;
+  picked.reserve(static_cast<size_t>(s));
   for (Index t = 0; t < nodes; ++t) {
     Index best = -1;
-    for (Index q = 0; q < kCand && best < 0; ++q) {
-      const Index i = cand[static_cast<size_t>(t * kCand + q)];
+    for (Index q = 0; q < kChebCand && best < 0; ++q) {
+      const Index i = cand[static_cast<size_t>(t * kChebCand + q)];
       if (i >= 0 && !taken[i]) best = i;
     }
     if (best < 0) {  // all candidates taken: full scan over the untaken points
       double bd = std::numeric_limits<double>::infinity();
       for (Index i = 0; i < n; ++i) {
         if (taken[i]) continue;
-        const double dist = dist_to(i, t);
+        const double dist = cheb_dist(P, N, i, t);
         if (dist < bd) {
           bd = dist;
           best = i;
@@ -277,6 +296,20 @@ IndexVec mock_chebyshev_points(const MatXd& P, Index s, std::mt19937_64& rng) {
   }
   std::sort(picked.begin(), picked.end());
   return picked;
+}
+
+IndexVec mock_chebyshev_points(const MatXd& P, Index s, std::mt19937_64& rng) {
+  const Index n = P.rows();
+  IndexVec picked;
+  if (s >= n) {
+    picked.resize(static_cast<size_t>(n));
+    std::iota(picked.begin(), picked.end(), Index{0});
+    return picked;
+  }
+  const ChebNodes N = cheb_nodes(P, s);
+  std::vector<Index> cand(static_cast<size_t>(N.nodes * kChebCand));
+  cheb_candidates(P, N, cand.data());
+  return cheb_pick(P, s, N, cand.data(), rng);
 }
 
 IndexVec rand_subset(Index n, Index k, std::mt19937_64& rng) {

@@ -3,9 +3,27 @@
 
 #include <cstdint>
 #include <memory>
+#include <random>
+#include <vector>
 
 #include "midbf/butterfly.hpp"
 #include "midbf_b200.h"
+
+namespace midbf::la {
+
+// mock_chebyshev_points in parts (linalg.cpp): the candidate search also runs
+// on the GPU with the same arithmetic (dev::EntrySampler::cheb_candidates).
+constexpr Index kChebCand = 8;  // nearest points kept per node, by (distance, index)
+struct ChebNodes {
+  Index c = 0, d = 0, nodes = 0;
+  std::vector<double> nodec;  // nodes x d, row-major
+};
+ChebNodes cheb_nodes(const MatXd& P, Index s);
+void cheb_candidates(const MatXd& P, const ChebNodes& N, Index* cand);  // nodes x kChebCand, -1: none
+void cheb_candidates_node(const MatXd& P, const ChebNodes& N, Index t, Index* cand);  // node t's kChebCand
+IndexVec cheb_pick(const MatXd& P, Index s, const ChebNodes& N, const Index* cand, std::mt19937_64& rng);
+
+}  // namespace midbf::la
 
 namespace midbf::bf {
 
