@@ -14,19 +14,21 @@
 // column-major, panels appended in strip order and strips in application
 // order, so one apply streams the arena once, front to back.
 //
-// k1_flow (single RHS, default): ONE persistent launch for all stages.
-//   * 1 CTA per SM, 4 warps; each warp is its own producer and consumer:
-//     lane 0 claims strips from a global counter (strips are numbered stage by
-//     stage, so claims run in dependency order) and streams their panels into
-//     the warp's ring of 3 x 16 KB shared-memory slots with cp.async.bulk
-//     (TMA bulk copy, mbarrier complete_tx), up to 48 KB in flight per warp;
-//   * before touching its input x a strip waits only for the few strips of the
-//     previous stage that produce that x range (per-strip release/acquire
-//     flags carrying the apply epoch) — there is no stage-wide barrier, so HBM
-//     streaming continues across stage boundaries;
-//   * x is staged in a per-warp shared window (stage 0 gathers f through
-//     col_perm), each lane owns one output row; the last stage scatters
-//     through row_perm.
+// k1_flow (single RHS, default; flow.cuh): ONE persistent launch for all
+//   stages.  1 CTA per SM, 4 (or 8 for plans > 512 MB) consumer / producer
+//   / x-stager warp triples; strips are dealt round-robin to the consumer
+//   warps stage by stage (static deal, no counters); each producer streams
+//   its consumer's panels into a ring of shared-memory slots with
+//   cp.async.bulk (TMA bulk copy, mbarrier complete_tx); a strip's x window
+//   is gathered by the stager, which polls the previous stage's output until
+//   no entry carries the sentinel (the data is its own ready signal: relaxed
+//   GPU-scope stores and loads, no flags) — there is no stage-wide barrier,
+//   so HBM streaming continues across stage boundaries; each lane owns one
+//   output row; the last stage scatters through row_perm.  Consecutive
+//   applies on one stream are chained by programmatic dependent launch
+//   (flag bit 17).
+// k1_coop (single RHS, plans below kCoopBytes; coop.cuh): a CTA per strip,
+//   its 8 warps splitting the columns, panels of the next strips prefetched.
 // k1_stage (multi-RHS fallback and A/B reference): one launch per stage,
 //   warp per strip, streaming 128-bit loads; chained with programmatic
 //   dependent launch inside a CUDA graph.
