@@ -707,23 +707,34 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
           if (live && P.nodeps != 4) {
             // one consumer warp per SM sub-partition: 4 independent
             // accumulators keep the DFMA chains short (latency 8 cycles)
-            int cc = cpar;
-            for (; cc + 7 * cstep < ncol; cc += 8 * cstep) {
-              double2 m[8], xr[8];
+            // pointer walk with the column step a compile-time constant
+            // (x offsets immediate, panel offsets loop-invariant): one add
+            // per panel load instead of the index arithmetic
+            auto body = [&](auto cs_) {
+              constexpr int CS = decltype(cs_)::value;
+              const int ms = CS * hc;  // panel elements between this lane's columns
+              const double2* mp = M + cpar * hc + prow;
+              const double2* xp = xv + cpar;
+              int c = cpar;
+              for (; c + 7 * CS < ncol; c += 8 * CS, mp += 8 * ms, xp += 8 * CS) {
+                double2 m[8], xr[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                m[i] = M[(cc + i * cstep) * hc + prow];
-                xr[i] = xv[cc + i * cstep];
+                for (int i = 0; i < 8; ++i) {
+                  m[i] = mp[i * ms];
+                  xr[i] = xp[i * CS];
+                }
+                cmac(ar0, ai0, m[0], xr[0]);
+                cmac(ar1, ai1, m[1], xr[1]);
+                cmac(ar2, ai2, m[2], xr[2]);
+                cmac(ar3, ai3, m[3], xr[3]);
+                cmac(ar0, ai0, m[4], xr[4]);
+                cmac(ar1, ai1, m[5], xr[5]);
+                cmac(ar2, ai2, m[6], xr[6]);
+                cmac(ar3, ai3, m[7], xr[7]);
               }
-              cmac(ar0, ai0, m[0], xr[0]);
-              cmac(ar1, ai1, m[1], xr[1]);
-              cmac(ar2, ai2, m[2], xr[2]);
-              cmac(ar3, ai3, m[3], xr[3]);
-              cmac(ar0, ai0, m[4], xr[4]);
-              cmac(ar1, ai1, m[5], xr[5]);
-              cmac(ar2, ai2, m[6], xr[6]);
-              cmac(ar3, ai3, m[7], xr[7]);
-            }
+              return c;
+            };
+            int cc = halves ? body(std::integral_constant<int, 2>{}) : body(std::integral_constant<int, 1>{});
             if (cc + 3 * cstep < ncol) {  // remainder spread over the 4 chains
               cmac(ar0, ai0, M[cc * hc + prow], xv[cc]);
               cmac(ar1, ai1, M[(cc + cstep) * hc + prow], xv[cc + cstep]);
