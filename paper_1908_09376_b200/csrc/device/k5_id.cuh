@@ -71,7 +71,7 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // out + ooff: V (k x n, ld k) for a column ID, W = V^T (n x k, ld n) for a row
 // ID (`rowid`: the workspace holds the transposed block).
 template <int kIdRows, int kIdWarps>  // register slots per lane, warps cooperating on one block
-__global__ void __launch_bounds__(kIdWarps * 32) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
+__global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
                                                        int ntasks, int kmax, double eps, int rowid,
                                                        double2* __restrict__ out, int* __restrict__ ranks,
                                                        int* __restrict__ skel, int kcap) {

@@ -1070,7 +1070,7 @@ bool Plan::flow_lite(int d) const {
   if (flags & 1024u) return true;
   int64_t bytes = 0;
   for (const auto& st : dir[d].stages) bytes += st.payload_bytes;
-  // measured (tools/gpu_lite.sh, us per apply, default | dense-only |
+  // measured (round 1, tools/flow_ab.py; us per apply, default | dense-only |
   // compressed): cfg0 7.6 MB 17.0 | 16.9 | 19.2, cfg1_unitxi 145 MB
   // 37.0 (dense-only) vs 40.2, cfg1 358 MB 62.5 (dense-only) vs 55.2
   return bytes < (int64_t{200} << 20);

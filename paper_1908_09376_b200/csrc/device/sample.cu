@@ -616,7 +616,7 @@ void launch_k4(const DevK& k, dim3 grid, cudaStream_t st, const int* rows, int n
 // return rank -1 from the kernel and are recomputed on the host).
 void launch_k5(int64_t max_m, unsigned grid, cudaStream_t st, double2* ws, const IdTask* tk, int ntasks, int kmax,
                double eps, int rowid, double2* vals, int* rank, int* skel, int kcap) {
-  // Warps per block, measured (tools/gpu_k5exp.sh, K5 device ms per
+  // Warps per block, measured (round 1, K5 device ms per
   // factorization): 2D cfg1 8 warps 12.8 vs 4 warps 15.9 ms; 3D cfg3 (k5_id<16>,
   // 254 registers) 4 warps 73.3 vs 8 warps 76.3 ms.  Capping resident blocks
   // per SM so the in-flight blocks fit L2 was slower (cfg1 19.6-21.3 ms).
@@ -625,8 +625,15 @@ void launch_k5(int64_t max_m, unsigned grid, cudaStream_t st, double2* ws, const
                "k5 smem attribute");
     kern<<<grid, nthreads, smem, st>>>(ws, tk, ntasks, kmax, eps, rowid, vals, rank, skel, kcap);
   };
-  if (max_m <= 256)
+  // register slots sized to the tallest block (fewer registers, more
+  // resident blocks): 2D k = 30 blocks are 150 x {64, 120} (t k = 150
+  // samples), 3D k = 64 blocks 320 x {64, 512}
+  if (max_m <= 160)
+    go(k5_id<5, 8>, id_smem<5>(), 256);
+  else if (max_m <= 256)
     go(k5_id<8, 8>, id_smem<8>(), 256);
+  else if (max_m <= 320)
+    go(k5_id<10, 4>, id_smem<10>(), 128);
   else
     go(k5_id<16, 4>, id_smem<16>(), 128);
 }
