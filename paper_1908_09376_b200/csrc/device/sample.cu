@@ -395,15 +395,47 @@ __device__ __forceinline__ void fill_staged(const DevK& k, const int* __restrict
     __syncthreads();
     double2* out = B + static_cast<int64_t>(c0) * m;
     int r = threadIdx.x % m, c = threadIdx.x / m;
-    for (int e = threadIdx.x; c < nt; e += blockDim.x) {
-      const double phi = TRANS ? O::phase(k, sN + c, kNTile, sM + r, kMCap) : O::phase(k, sM + r, kMCap, sN + c, kNTile);
-      out[e] = polar1(phi);
+    auto step = [&]() {
       r += sr;
       c += sc;
       if (r >= m) {
         r -= m;
         ++c;
       }
+    };
+    int e = threadIdx.x;
+    // four of this thread's entries per iteration: four independent sincos
+    // Horner chains (dependent DFMA latency 17 cycles, tools/lat_probe.cu)
+    for (;;) {
+      int rr[4], cc[4];
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        rr[i] = r;
+        cc[i] = c;
+        ok = ok && c < nt;
+        step();
+      }
+      if (!ok) {  // fewer than four left: back to the first of them, one at a time
+        r = rr[0];
+        c = cc[0];
+        break;
+      }
+      double ph[4];
+      double2 v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        ph[i] = TRANS ? O::phase(k, sN + cc[i], kNTile, sM + rr[i], kMCap)
+                      : O::phase(k, sM + rr[i], kMCap, sN + cc[i], kNTile);
+      polar1x4(ph, v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[e + i * static_cast<int>(blockDim.x)] = v[i];
+      e += 4 * static_cast<int>(blockDim.x);
+    }
+    for (; c < nt; e += blockDim.x) {
+      const double phi = TRANS ? O::phase(k, sN + c, kNTile, sM + r, kMCap) : O::phase(k, sM + r, kMCap, sN + c, kNTile);
+      out[e] = polar1(phi);
+      step();
     }
   }
 }
