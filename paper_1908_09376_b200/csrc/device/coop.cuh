@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
   const int64_t par_off = (e & 1u) ? P.par_elems : 0;
   {  // stage -1: the input permutation into the head of this apply's set
     double2* x0 = P.stagebuf + par_off;
+    wait_in_flag(P.in_flag, P.in_seq);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + tid; i < P.in_len; i += static_cast<int64_t>(G) * NT) {
       const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
       st_signal(x0 + i, make_double2(unsentinel(v.x), unsentinel(v.y)));

@@ -65,6 +65,12 @@ struct FlowParams {
   double2* stagebuf;  // both parity sets of intermediate stage buffers
   int64_t par_elems;  // complex entries per parity set
   const double2* in;  // user input (read once by the permutation prologue)
+  // Pipelined host-operand applies (Plan::apply_async): the input is copied
+  // on another stream, followed by a one-byte flag write; the prologue waits
+  // for flag == in_seq instead of the stream waiting on an event, so the
+  // chained launch is not broken by a cross-stream dependency.  Null: none.
+  const unsigned char* in_flag;
+  unsigned in_seq;
   const int* in_perm;
   int64_t in_len;
   int nstrips;
@@ -200,6 +206,19 @@ __device__ __forceinline__ double2 poll_cg(const double2* p) {
 // is single-copy atomic, which is all the sentinel test needs).
 __device__ __forceinline__ void st_signal(double2* p, double2 v) {
   asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+// Wait for the input-ready flag of a pipelined host-operand apply (see
+// FlowParams::in_flag); bounded: a flag that never arrives traps instead of
+// hanging the GPU.
+__device__ __forceinline__ void wait_in_flag(const unsigned char* f, unsigned seq) {
+  if (!f) return;
+  for (long long it = 0;; ++it) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u8 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if ((v & 0xffu) == (seq & 0xffu)) return;
+    if (it > (1ll << 26)) __trap();
+    __nanosleep(128);
+  }
 }
 __device__ __forceinline__ double2 ld_cg(const double2* p) {
   double2 v;
@@ -492,6 +511,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
     const int64_t i0 = (static_cast<int64_t>(blockIdx.x) * nw + wl) * 32 + lane;
     const int64_t di = static_cast<int64_t>(gridDim.x) * nw * 32;
     double2* x0 = P.stagebuf + par_off;
+    wait_in_flag(P.in_flag, P.in_seq);
     for (int64_t i = i0; i < P.in_len; i += di) {
       const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
       st_signal(x0 + i, make_double2(unsentinel(v.x), unsentinel(v.y)));

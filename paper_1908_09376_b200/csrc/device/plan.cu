@@ -1023,6 +1023,7 @@ Plan::~Plan() {
   }
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   if (ev_last) cudaEventDestroy(ev_last);
+  cudaFree(d_inflag);
   if (s_h2d) {
     cudaStreamSynchronize(s_d2h);
     for (auto& a : aslots) {
@@ -1173,6 +1174,8 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.st = D.d_stageio;
   P.out = out;
   P.in = in;
+  P.in_flag = next_in_flag;
+  P.in_seq = next_in_seq;
   P.in_perm = d == 0 ? d_col_perm : d_row_perm;
   P.in_len = D.in_len;
   P.arena_len = D.arena_elems + D.farena_elems;
@@ -1605,8 +1608,28 @@ void Plan::apply_async(const double* f, double* g, int64_t nrhs, bool transpose,
     S.elems = need;
   }
   cuda_check(cudaMemcpyAsync(S.d_in, f, nin * nrhs * sizeof(double2), cudaMemcpyHostToDevice, s_h2d), "H2D");
-  cuda_check(cudaEventRecord(S.in_ready, s_h2d), "event");
-  cuda_check(cudaStreamWaitEvent(s_comp, S.in_ready, 0), "wait H2D");
+  // A chained single-RHS apply waits for its input inside the kernel (a flag
+  // byte written after the copy on the copy stream) rather than through a
+  // cross-stream event, which would break the programmatic chain on s_comp.
+  const bool in_kernel_wait = (flags & kFlagChain) && flow_ok(d, nrhs) && nrhs == 1 && !dir[d].stages.empty();
+  if (in_kernel_wait) {
+    if (!d_inflag) {
+      cuda_check(cudaMalloc(&d_inflag, 64), "cudaMalloc input flags");
+      cuda_check(cudaMemset(d_inflag, 0, 64), "input flags");
+    }
+    const int si = static_cast<int>(&S - aslots);
+    S.flag_seq = static_cast<unsigned char>(S.flag_seq + 1 == 0 ? 1 : S.flag_seq + 1);
+    cuda_check(cudaMemsetAsync(d_inflag + si, S.flag_seq, 1, s_h2d), "input flag");
+    next_in_flag = d_inflag + si;
+    next_in_seq = S.flag_seq;
+  } else {
+    cuda_check(cudaEventRecord(S.in_ready, s_h2d), "event");
+    cuda_check(cudaStreamWaitEvent(s_comp, S.in_ready, 0), "wait H2D");
+  }
+  struct ClearFlag {
+    Plan* p;
+    ~ClearFlag() { p->next_in_flag = nullptr; }
+  } clear_flag{this};
   apply_device(d, S.d_in, S.d_out, nrhs, s_comp);
   cuda_check(cudaEventRecord(S.applied, s_comp), "event");
   cuda_check(cudaStreamWaitEvent(s_d2h, S.applied, 0), "wait apply");

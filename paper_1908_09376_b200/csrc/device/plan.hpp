@@ -107,6 +107,7 @@ struct AsyncSlot {  // device staging of one in-flight host-operand apply
   int64_t elems = 0;
   bool used = false;
   cudaEvent_t in_ready = nullptr, applied = nullptr, done = nullptr;
+  unsigned char flag_seq = 0;  // value of this slot's input-ready flag byte for its latest use
 };
 
 struct GraphEntry {
@@ -199,7 +200,12 @@ class Plan {
 
  private:
   cudaEvent_t ev_last = nullptr;
-  cudaStream_t last_stream = nullptr;  // stream of the previous ordered apply (chain mode skips same-stream waits)
+  cudaStream_t last_stream = nullptr;
+  // input-ready flags of the pipelined host-operand path (one byte per async
+  // slot) and the flag the next single-RHS flow launch waits on (apply_async)
+  unsigned char* d_inflag = nullptr;
+  const unsigned char* next_in_flag = nullptr;
+  unsigned next_in_seq = 0;  // stream of the previous ordered apply (chain mode skips same-stream waits)
 };
 
 std::unique_ptr<Plan> load_plan(const std::string& path, unsigned directions);
