@@ -111,7 +111,10 @@ int midbf_apply(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int
  * `stream` waits for this call's result (synchronize it before reading g or
  * reusing f; f is read asynchronously and is not ordered after earlier
  * work on `stream`).  Consecutive calls overlap their copies with the
- * previous apply.  Pinned host memory is needed for real overlap. */
+ * previous apply.  Pinned host memory is needed for real overlap.  A
+ * chained single-RHS apply waits for its staged f inside the kernel (a
+ * one-byte flag the copy stream sets after the H2D copy), so its launch
+ * stays chained to the previous apply. */
 int midbf_apply_async(midbf_plan_t plan, const double* f, double* g, int64_t nrhs, int transpose, void* stream);
 
 /* ------------------------------------------------------- entry sampling
