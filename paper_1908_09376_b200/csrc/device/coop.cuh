@@ -84,15 +84,37 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
   };
   if (tid == 0)
     for (int i = 0; i < kCoopSlots && i < nmine; ++i) fetch(i);  // plan constants: before the wait
+  // P.direct0: stage 0 gathers the user input through the permutation itself
+  // (no stage -1 hop on the chain); the first strip's permutation indices are
+  // plan constants, loaded before the wait.
+  constexpr int kPre = kCoopX / NT;
+  int pre[kPre];
+#pragma unroll
+  for (int t = 0; t < kPre; ++t) pre[t] = -1;
+  if (P.direct0 && nmine > 0) {
+    const StripCtx* c0 = P.ctxs + blockIdx.x;
+    if (__ldg(&c0->s.stage) == 0) {
+      const int nseg = __ldg(&c0->s.nseg), xcols = __ldg(&c0->s.xcols);
+#pragma unroll
+      for (int t = 0; t < kPre; ++t) {
+        const int kk = tid + t * NT;
+        if (kk < xcols) {
+          int j = 0, c = kk;
+          while (j < nseg - 1 && c >= __ldg(&c0->g[j].n)) c -= __ldg(&c0->g[j].n), ++j;
+          pre[t] = __ldg(P.in_perm + __ldg(&c0->g[j].x0) + c);
+        }
+      }
+    }
+  }
   if (P.pdl) {
     if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
   }
   const unsigned e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int64_t par_off = (e & 1u) ? P.par_elems : 0;
-  {  // stage -1: the input permutation into the head of this apply's set
+  wait_in_flag(P.in_flag, P.in_seq);
+  if (!P.direct0) {  // stage -1: the input permutation into the head of this apply's set
     double2* x0 = P.stagebuf + par_off;
-    wait_in_flag(P.in_flag, P.in_seq);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * NT + tid; i < P.in_len; i += static_cast<int64_t>(G) * NT) {
       const double2 v = __ldg(P.in + __ldg(P.in_perm + i));
       st_signal(x0 + i, make_double2(unsentinel(v.x), unsentinel(v.y)));
@@ -108,8 +130,23 @@ __global__ void __launch_bounds__(W * 32) k1_coop(const __grid_constant__ FlowPa
     const StageIO io = P.st[C.s.stage];
     const double2* xin = io.x + (io.x_par ? par_off : 0);
     double2* yout = io.y ? io.y + (io.y_par ? par_off : 0) : P.out;
-    // x window (polled; stage 0 reads the permuted input the same way)
-    for (int kk = tid; kk < xcols; kk += NT) {
+    // x window (polled; stage 0 reads the permuted input the same way, or
+    // the user input through the permutation with P.direct0)
+    if (P.direct0 && C.s.stage == 0) {
+#pragma unroll
+      for (int t = 0; t < kPre; ++t) {  // xcols <= kCoopX = kPre * NT
+        const int kk = tid + t * NT;
+        if (kk >= xcols) break;
+        int pi = i == 0 ? pre[t] : -1;
+        if (pi < 0) {
+          int j = 0, c = kk;
+          while (j < nseg - 1 && c >= C.g[j].n) c -= C.g[j].n, ++j;
+          pi = __ldg(P.in_perm + C.g[j].x0 + c);
+        }
+        MIDBF_DCHECK(kk < kCoopX && pi >= 0 && pi < P.in_len, "k1_coop input gather");
+        xs[kk] = __ldg(P.in + pi);
+      }
+    } else for (int kk = tid; kk < xcols; kk += NT) {
       int j = 0, c = kk;
       while (j < nseg - 1 && c >= C.g[j].n) c -= C.g[j].n, ++j;
       const double2* p = xin + C.g[j].x0 + c;

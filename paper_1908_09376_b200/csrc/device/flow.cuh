@@ -89,6 +89,7 @@ struct FlowParams {
   double2* out;
   int64_t arena_len;  // complex entries of the arena (checked builds)
   int64_t out_len;    // entries of `out` (checked builds)
+  int direct0;        // stage 0 gathers the user input through in_perm itself (no stage -1 prologue)
 };
 
 // A panel as k1_flow streams it.
@@ -262,8 +263,8 @@ __device__ __forceinline__ void gather_range(const double2* x, const int* xperm,
   }
 }
 // Wide compressed strips: gather cnt kept columns x[x0 + map[kk]], polling.
-__device__ __forceinline__ void gather_mapped(const double2* x, int x0, const int* map, int cnt, double2* dst,
-                                              int lane) {
+__device__ __forceinline__ void gather_mapped(const double2* x, const int* xperm, int x0, const int* map, int cnt,
+                                              double2* dst, int lane) {
   for (int base = 0; base < cnt; base += 32 * 4) {
     double2 v[4];
     int idx[4];
@@ -274,9 +275,9 @@ __device__ __forceinline__ void gather_mapped(const double2* x, int x0, const in
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (idx[i] >= 0) v[i] = ld_cg(x + idx[i]);
-    bool ok;
-    do {
+      if (idx[i] >= 0) v[i] = xperm ? __ldg(x + __ldg(xperm + idx[i])) : ld_cg(x + idx[i]);
+    bool ok = xperm != nullptr;  // the user input is never polled
+    if (!ok) do {
       ok = true;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -337,7 +338,7 @@ __device__ __forceinline__ void store_x_regs(const StripCtx& c, const double2* v
 // gathers its entries (lane-strided over the flattened panel columns) and
 // polls until none is a sentinel; no warp-collective ops inside, so the
 // producer's lane 0 can run the TMA issue loop concurrently.
-template <int NS, bool CMP>  // stager lanes, identity-compressed records possible
+template <int NS, bool CMP, bool PF = false>  // stager lanes, identity-compressed records possible, prefetch only
 __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, const int* xperm, double2* dst, int sl,
                                         const double2* xbase_lo = nullptr, const double2* xbase_hi = nullptr) {
   constexpr int kPer = (kXWin + NS - 1) / NS;
@@ -364,6 +365,15 @@ __device__ __forceinline__ void stage_x(const StripCtx& c, const double2* x, con
         idx[i] = c.g[t >> 8].x0 + static_cast<int>(t & 0xffu);
       }
     }
+  }
+  if (PF) {  // touch the permutation entries (plan constants) so the gather after the dependency wait hits L1
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      if (idx[i] >= 0 && xperm) {
+        unsigned t;
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(t) : "l"(xperm + idx[i]));
+      }
+    return;
   }
   double2 v[kPer];
 #pragma unroll
@@ -494,15 +504,21 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   // ahead; everything that touches the previous apply's results (epochs,
   // stage buffers, input, output) waits for its completion and memory flush.
   const bool tma_lane = producer && (kSep || lane == 0);  // streams plan constants only
+  // With direct stage-0 gathers the separate x-stager warps run ahead of the
+  // dependency wait as far as their first window's permutation indices (plan
+  // constants), so that only the input loads follow the wait.
+  const bool early = kSep && stager_warp && P.pdl && P.direct0;
   if (P.pdl) {
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (!tma_lane) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!tma_lane && !early) asm volatile("griddepcontrol.wait;" ::: "memory");
   }
 
-  const unsigned e = tma_lane ? 0u : *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
+  unsigned e = (tma_lane || early) ? 0u : *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
-  const int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
-  if (!producer) {
+  int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
+  if (!producer && P.direct0) {
+    wait_in_flag(P.in_flag, P.in_seq);  // stage 0 reads the input itself
+  } else if (!producer) {
     // stage -1: the input permutation, gathered once into the head of this
     // apply's set (sentinel-armed; stage 0 polls it like any other stage) by
     // the consumer / stager warps while the producers start streaming panels
@@ -546,15 +562,29 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   auto stager = [&](auto ns, int sl, unsigned mask, bool arriver) {
     constexpr int NS = decltype(ns)::value;
     const int nmine = gw < P.nstrips ? (P.nstrips - 1 - gw) / P.nwarps + 1 : 0;
+    bool waited = !early;
+    auto dep_wait = [&]() {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      e = *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
+      par_off = (e & 1u) ? P.par_elems : 0;
+      waited = true;
+    };
     for (int k = 0; k < nmine; ++k) {
       const int sc = k % kQN, b = k & 1;
       FLOW_T(3, mbar_wait(&cfull[sc], (k / kQN) & 1));
       const StripCtx& C = ctx[sc];
+      if (!waited) {
+        if (C.s.stage == 0 && C.s.xcols <= kXWin)
+          stage_x<NS, CMP, true>(C, P.in, P.in_perm, xb + b * kXWin, sl);
+        dep_wait();
+      }
       if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
-        FLOW_T(13, stage_x<NS, CMP>(C, io.x + (io.x_par ? par_off : 0), io.xperm, xb + b * kXWin, sl, P.stagebuf,
-                                    P.stagebuf + 2 * P.par_elems));
+        const bool d0 = P.direct0 && C.s.stage == 0;
+        FLOW_T(13, stage_x<NS, CMP>(C, d0 ? P.in : io.x + (io.x_par ? par_off : 0), d0 ? P.in_perm : io.xperm,
+                                    xb + b * kXWin, sl, d0 ? P.in : P.stagebuf,
+                                    d0 ? P.in + P.in_len : P.stagebuf + 2 * P.par_elems));
         if (CMP && kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
           // (separate stager warps only; with the in-warp stager of FW > 4
           // the consumers sum in place)
@@ -582,6 +612,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         mbar_arrive(&xfull[b]);  // each lane's own entries (release)
       }
     }
+    if (!waited) dep_wait();
     rearm(sl, NS);
   };
 
@@ -673,7 +704,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
-      const double2* xin = io.x + (io.x_par ? par_off : 0);
+      const bool d0 = P.direct0 && C.s.stage == 0;
+      const double2* xin = d0 ? P.in : io.x + (io.x_par ? par_off : 0);
+      const int* xperm = d0 ? P.in_perm : io.xperm;
       double2* yout = io.y ? io.y + (io.y_par ? par_off : 0) : P.out;
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + (k & 1) * kXWin;
@@ -712,9 +745,9 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
               __syncwarp();
               const int cnt = min(kXWin, n - w0 * kXWin);
               if (CMP && C.mapped == 2)
-                gather_mapped(xin, C.g[j].x0, P.wmap + C.wbase + cb + w0 * kXWin, cnt, xcur, lane);
+                gather_mapped(xin, xperm, C.g[j].x0, P.wmap + C.wbase + cb + w0 * kXWin, cnt, xcur, lane);
               else
-                gather_range(xin, io.xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
+                gather_range(xin, xperm, C.g[j].x0 + w0 * kXWin, cnt, xcur, lane);
               __syncwarp();
               win = w0;
             }
@@ -798,7 +831,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
           const unsigned a = C.g[j].adds;
           if ((a >> row) & 1u) {
             const int xi = C.g[j].x0 + __ldg(P.wmap + C.wbase + C.nkept + C.g[j].aoff + __popc(a & below));
-            const double2 t = poll_cg(xin + xi);
+            const double2 t = xperm ? __ldg(xin + __ldg(xperm + xi)) : poll_cg(xin + xi);
             yr += t.x;
             yi += t.y;
           }

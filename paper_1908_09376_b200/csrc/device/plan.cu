@@ -1181,9 +1181,16 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.arena_len = D.arena_elems + D.farena_elems;
   P.out_len = d == 0 ? nrows : ncols;
   P.pdl = (flags & kFlagChain) ? 1 : 0;
+  // Stage 0 gathers the user input through the permutation itself (no
+  // stage -1 prologue), its permutation indices loaded before the chained
+  // wait; 4-pair layout only (separate stager warps): measured cfg1 51.7 ->
+  // 50.1 us, cfg1_unitxi 36.4 -> 35.1; with the 8-pair layout's in-warp
+  // stager cfg2 got slower (242 -> 245 us).  Flag bit 24 keeps the prologue.
+  P.direct0 = (variant == 0 && !(flags & kFlagPrologue)) ? 1 : 0;
   if (coop(d)) {
     P.ctxs = static_cast<const StripCtx*>(D.d_ctx);  // dense records
     P.nwarps = coop_grid;
+    P.direct0 = (flags & kFlagPrologue) ? 0 : 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(coop_grid), 1, 1);
     cfg.blockDim = dim3(kCoopWarps * 32, 1, 1);

@@ -22,6 +22,9 @@ constexpr unsigned kFlagChain = 1u << 17;
 // single-RHS applies; by default it runs below kCoopBytes of panels.
 constexpr unsigned kFlagCoop = 1u << 18;
 constexpr unsigned kFlagNoCoop = 1u << 19;
+// k1_flow: gather the input permutation in a stage -1 prologue instead of in
+// stage 0's x windows (A/B experiments)
+constexpr unsigned kFlagPrologue = 1u << 24;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 

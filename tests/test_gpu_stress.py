@@ -45,7 +45,8 @@ def test_back_to_back_applies_are_bitwise_stable(plan_case, transpose):
     try:
         for kw in (dict(variant=0, lite=False), dict(variant=1, lite=False), dict(variant=0, lite=True),
                    dict(variant=1, lite=True), dict(), dict(chain=False), dict(chain=False, variant=1, lite=False),
-                   dict(coop=True), dict(coop=True, chain=False)):
+                   dict(coop=True), dict(coop=True, chain=False), dict(variant=0, prologue=True),
+                   dict(variant=0, lite=True, chain=False)):
             plan.set_flags(**kw)
             ref = [torch.empty(nout, dtype=torch.complex128, device="cuda") for _ in range(2)]
             for i in range(2):
@@ -66,4 +67,4 @@ def test_back_to_back_applies_are_bitwise_stable(plan_case, transpose):
             assert not bad, (kw, bad[:8])
     finally:
         plan.reset_flags()
-    assert total >= 9 * REPS
+    assert total >= 11 * REPS
