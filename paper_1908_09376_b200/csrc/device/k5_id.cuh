@@ -35,10 +35,16 @@ namespace midbf::dev {
 // 150 x 120 at cfg1), k5_id<16> m <= 512 (3D blocks, 320 x 512 at cfg3).
 constexpr int kIdRowsMax = 16;
 constexpr int kIdCols = 512;           // n <= 512
+// Dynamic shared memory: squared norms (current, reference), |R_ii|, the
+// column permutation, the Householder vector and R11 (r11 x r11, the
+// epilogue's triangular solves; r11 = k_max when 1 <= k_max <= 64, else 0
+// and the epilogue reads R from the workspace).
+constexpr int kIdR11Max = 64;
 template <int ROWS>
-constexpr size_t id_smem() {
-  return size_t(kIdCols) * (8 + 8 + 4) + size_t(32 * ROWS) * 16 + 64;
+constexpr size_t id_smem(int r11 = 0) {
+  return size_t(kIdCols) * (8 + 8 + 8 + 4) + size_t(32 * ROWS) * 16 + size_t(r11) * r11 * 16 + 64;
 }
+__host__ __device__ inline int id_r11(int kmax) { return kmax >= 1 && kmax <= kIdR11Max ? kmax : 0; }
 
 struct IdTask {
   int64_t off;   // block B (m x n, column-major) in the workspace
@@ -71,7 +77,7 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // out + ooff: V (k x n, ld k) for a column ID, W = V^T (n x k, ld n) for a row
 // ID (`rowid`: the workspace holds the transposed block).
 template <int kIdRows, int kIdWarps>  // register slots per lane, warps cooperating on one block
-__global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
+__global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(double2* __restrict__ ws, const IdTask* __restrict__ tasks,
                                                        int ntasks, int kmax, double eps, int rowid,
                                                        double2* __restrict__ out, int* __restrict__ ranks,
                                                        int* __restrict__ skel, int kcap) {
@@ -80,8 +86,11 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
   extern __shared__ __align__(16) unsigned char k5smem[];
   double* cur = reinterpret_cast<double*>(k5smem);
   double* ref = cur + kIdCols;
-  double2* vsh = reinterpret_cast<double2*>(ref + kIdCols);  // Householder vector (rows)
-  int* perm = reinterpret_cast<int*>(vsh + kIdMaxRows);
+  double* dg = ref + kIdCols;                               // |R_ii|
+  double2* vsh = reinterpret_cast<double2*>(dg + kIdCols);  // Householder vector (rows)
+  double2* R11 = vsh + kIdMaxRows;                          // r11 x r11 (epilogue)
+  const int r11 = id_r11(kmax);
+  int* perm = reinterpret_cast<int*>(R11 + r11 * r11);
   __shared__ int sh_p, sh_stop, sh_rank, sh_fb;
   __shared__ double sh_beta;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -152,16 +161,17 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
       }
     }
     __syncthreads();
-    double2* col = B + static_cast<int64_t>(k) * m;
     if (w == 0) {  // Householder vector from column k (rows k..m-1)
+      double2* col = B + static_cast<int64_t>(k) * m;
       double2 x[kIdRows];
-      double xs = 0.0;
 #pragma unroll
       for (int r = 0; r < kIdRows; ++r) {
         const int i = lane + 32 * r;
         x[r] = (i >= k && i < m) ? col[i] : make_double2(0, 0);
-        xs += nrm2(x[r]);
       }
+      double xs = 0.0;
+#pragma unroll
+      for (int r = 0; r < kIdRows; ++r) xs += nrm2(x[r]);
       xs = wsum(xs);
       const double xn = sqrt(xs);
       if (xn == 0.0) {
@@ -187,13 +197,15 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
           }
         }
         vs = wsum(vs);
-        if (lane == (k & 31)) col[k] = make_double2(-ph.x * xn, -ph.y * xn);
+        const double2 rkk = make_double2(-ph.x * xn, -ph.y * xn);
+        if (lane == (k & 31)) col[k] = rkk;
 #pragma unroll
         for (int r = 0; r < kIdRows; ++r) {
           const int i = lane + 32 * r;
           if (i < m) vsh[i] = i == k ? make_double2(1.0, 0.0) : (i > k ? x[r] : make_double2(0, 0));
         }
         if (lane == 0) {
+          dg[k] = sqrt(nrm2(rkk));
           sh_beta = 2.0 / (1.0 + vs);
           sh_stop = 0;
         }
@@ -208,44 +220,69 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
       const int i = lane + 32 * r;
       v[r] = i < m ? vsh[i] : make_double2(0, 0);
     }
-    // trailing columns (warp w: k+1+w, k+1+w+kIdWarps, ...): c -= beta v (v^H c)
-    for (int j = k + 1 + w; j < n; j += kIdWarps) {
-      double2* c = B + static_cast<int64_t>(j) * m;
-      double2 cv[kIdRows];
-      double wr = 0.0, wi = 0.0;
+    // trailing columns (warp w: k+1+w, k+1+w+kIdWarps, ...): c -= beta v (v^H c),
+    // two columns per pass (kIdRows <= 8) so their loads and reduction
+    // chains overlap
+    constexpr int kPair = kIdRows <= 8 ? 2 : 1;
+    for (int j0 = k + 1 + w; j0 < n; j0 += kPair * kIdWarps) {
+      double2 cv[kPair][kIdRows];
+      double wr[kPair], wi[kPair];
 #pragma unroll
-      for (int r = 0; r < kIdRows; ++r) {
-        const int i = lane + 32 * r;
-        cv[r] = (i >= k && i < m) ? c[i] : make_double2(0, 0);
-        const double2 q = cmulc(cv[r], v[r]);
-        wr += q.x;
-        wi += q.y;
-      }
-      wr = wsum(wr);
-      wi = wsum(wi);
-      const double2 cw = make_double2(wr, -wi);  // conj(w)
-      double rest = 0.0, ck = 0.0;
+      for (int u = 0; u < kPair; ++u) {
+        const int j = j0 + u * kIdWarps;
+        const double2* c = B + static_cast<int64_t>(j) * m;
+        wr[u] = 0.0;
+        wi[u] = 0.0;
 #pragma unroll
-      for (int r = 0; r < kIdRows; ++r) {
-        const int i = lane + 32 * r;
-        if (i >= k && i < m) {
-          const double2 d = cmul(make_double2(beta * v[r].x, beta * v[r].y), cw);
-          cv[r].x -= d.x;
-          cv[r].y -= d.y;
-          c[i] = cv[r];
-          if (i == k) ck = nrm2(cv[r]);
-          else rest += nrm2(cv[r]);
+        for (int r = 0; r < kIdRows; ++r) {
+          const int i = lane + 32 * r;
+          cv[u][r] = (j < n && i >= k && i < m) ? c[i] : make_double2(0, 0);
         }
       }
-      ck = __shfl_sync(0xffffffffu, ck, k & 31);
-      double cj = cur[j] - ck;
-      double rj = ref[j];
-      if (cj < 0.0 || cj <= 1e-12 * rj) {  // recompute guard
-        const double s = wsum(rest);
-        cj = m - k > 1 ? s : 0.0;
-        rj = cj;
+#pragma unroll
+      for (int u = 0; u < kPair; ++u)
+#pragma unroll
+        for (int r = 0; r < kIdRows; ++r) {
+          const double2 q = cmulc(cv[u][r], v[r]);
+          wr[u] += q.x;
+          wi[u] += q.y;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < kPair; ++u) {
+          wr[u] += __shfl_xor_sync(0xffffffffu, wr[u], o);
+          wi[u] += __shfl_xor_sync(0xffffffffu, wi[u], o);
+        }
+#pragma unroll
+      for (int u = 0; u < kPair; ++u) {
+        const int j = j0 + u * kIdWarps;
+        if (j >= n) break;
+        double2* c = B + static_cast<int64_t>(j) * m;
+        const double2 cw = make_double2(wr[u], -wi[u]);  // conj(w)
+        double rest = 0.0, ck = 0.0;
+#pragma unroll
+        for (int r = 0; r < kIdRows; ++r) {
+          const int i = lane + 32 * r;
+          if (i >= k && i < m) {
+            const double2 d = cmul(make_double2(beta * v[r].x, beta * v[r].y), cw);
+            cv[u][r].x -= d.x;
+            cv[u][r].y -= d.y;
+            c[i] = cv[u][r];
+            if (i == k) ck = nrm2(cv[u][r]);
+            else rest += nrm2(cv[u][r]);
+          }
+        }
+        ck = __shfl_sync(0xffffffffu, ck, k & 31);
+        double cj = cur[j] - ck;
+        double rj = ref[j];
+        if (cj < 0.0 || cj <= 1e-12 * rj) {  // recompute guard
+          const double s = wsum(rest);
+          cj = m - k > 1 ? s : 0.0;
+          rj = cj;
+        }
+        if (lane == 0) cur[j] = cj, ref[j] = rj;
       }
-      if (lane == 0) cur[j] = cj, ref[j] = rj;
     }
     __syncthreads();
   }
@@ -256,17 +293,16 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
   if (tid == 0) {
     int rank = 0;
     bool fallback = false;
-    const double d0 = steps > 0 ? sqrt(nrm2(B[0])) : 0.0;
+    const double d0 = steps > 0 ? dg[0] : 0.0;
     if (steps > 0 && d0 != 0.0) {
       if (steps == cap && cap < full)
-        for (int i = 0; i < steps; ++i)
-          fallback = fallback || sqrt(nrm2(B[static_cast<int64_t>(i) * m + i])) <= 1e-14 * d0;
+        for (int i = 0; i < steps; ++i) fallback = fallback || dg[i] <= 1e-14 * d0;
       int mm = steps;
-      while (mm > 0 && sqrt(nrm2(B[static_cast<int64_t>(mm - 1) * m + mm - 1])) <= 1e-14 * d0) --mm;
+      while (mm > 0 && dg[mm - 1] <= 1e-14 * d0) --mm;
       rank = mm;
       if (eps > 0.0)
         for (int i = 0; i < mm; ++i)
-          if (sqrt(nrm2(B[static_cast<int64_t>(i) * m + i])) <= eps * d0) {
+          if (dg[i] <= eps * d0) {
             rank = i + 1;
             break;
           }
@@ -283,6 +319,34 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 3 : 1) k5_id(dou
 
   // V(:, perm[j]) = e_j (j < rank), else R11^-1 R(0:rank, j); thread per column
   double2* V = out + tk.ooff;
+  if (r11 >= rank) {  // R11 staged in shared memory, the solution in registers / local memory
+    for (int q = tid; q < rank * rank; q += kIdWarps * 32) {
+      const int i = q % rank, l = q / rank;
+      R11[q] = i <= l ? B[static_cast<int64_t>(l) * m + i] : make_double2(0, 0);
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += kIdWarps * 32) {
+      const int pj = perm[j];
+      auto at = [&](int i) -> double2& {
+        return rowid ? V[static_cast<int64_t>(i) * n + pj] : V[static_cast<int64_t>(pj) * rank + i];
+      };
+      if (j < rank) {
+        for (int i = 0; i < rank; ++i) at(i) = make_double2(i == j ? 1.0 : 0.0, 0.0);
+        continue;
+      }
+      const double2* bj = B + static_cast<int64_t>(j) * m;
+      for (int i = rank - 1; i >= 0; --i) {
+        double2 s = bj[i];
+        for (int l = i + 1; l < rank; ++l) {
+          const double2 q = cmul(R11[l * rank + i], at(l));
+          s.x -= q.x;
+          s.y -= q.y;
+        }
+        at(i) = cdiv(s, R11[i * rank + i]);
+      }
+    }
+    return;
+  }
   for (int j = tid; j < n; j += kIdWarps * 32) {
     const int pj = perm[j];
     auto at = [&](int i) -> double2& {
