@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   unsigned e = (tma_lane || early) ? 0u : *reinterpret_cast<volatile unsigned*>(P.epoch + blockIdx.x) + 1u;
   const int gw = blockIdx.x * FW + c;
   int64_t par_off = (e & 1u) ? P.par_elems : 0;  // this apply's set of stage buffers
-  if (!producer && P.direct0) {
+  if (!producer && kSep && P.direct0) {
     wait_in_flag(P.in_flag, P.in_seq);  // stage 0 reads the input itself
   } else if (!producer) {
     // stage -1: the input permutation, gathered once into the head of this
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
         const StageIO io = P.st[C.s.stage];
-        const bool d0 = P.direct0 && C.s.stage == 0;
+        const bool d0 = kSep && P.direct0 && C.s.stage == 0;
         FLOW_T(13, stage_x<NS, CMP>(C, d0 ? P.in : io.x + (io.x_par ? par_off : 0), d0 ? P.in_perm : io.xperm,
                                     xb + b * kXWin, sl, d0 ? P.in : P.stagebuf,
                                     d0 ? P.in + P.in_len : P.stagebuf + 2 * P.par_elems));
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
-      const bool d0 = P.direct0 && C.s.stage == 0;
+      const bool d0 = kSep && P.direct0 && C.s.stage == 0;  // (4-pair layout only: plan.cu)
       const double2* xin = d0 ? P.in : io.x + (io.x_par ? par_off : 0);
       const int* xperm = d0 ? P.in_perm : io.xperm;
       double2* yout = io.y ? io.y + (io.y_par ? par_off : 0) : P.out;

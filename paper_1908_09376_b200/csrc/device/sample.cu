@@ -770,11 +770,14 @@ struct EntrySampler::Impl {
   }
   static constexpr int64_t kChunk = ChunkPool::kChunk;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // ID batches: downloads overlapping the next part's kernels
   void ensure_stream() {
     if (!stream) cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    if (!cstream) cuda_check(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking), "stream");
   }
   ~Impl() {
     if (stream) cudaStreamDestroy(stream);
+    if (cstream) cudaStreamDestroy(cstream);
   }
 };
 
@@ -1042,19 +1045,53 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
     cudaFree(d_tk);
   };
   try {
-    const unsigned nt = static_cast<unsigned>(ntasks);
-    I.begin(3, ws);
-    if (rowid)
-      launch_k3_ws<true>(I.k, nt, I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
-    else
-      launch_k3_ws<false>(I.k, nt, I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
-    cuda_check(cudaGetLastError(), "k3_sample_ws launch");
-    I.end();
-    I.begin(5, 0);
-    launch_k5(max_m, nt, I.stream, P.d_ws, d_tk, static_cast<int>(ntasks), static_cast<int>(std::max<int64_t>(k_max, 0)),
-              eps, rowid ? 1 : 0, P.d_vals, P.d_rank, P.d_skel, kcap);
-    cuda_check(cudaGetLastError(), "k5_id launch");
-    I.end();
+    // Pipelined in parts: part p's V/W values download on a second stream
+    // while part p+1 is sampled (K3) and decomposed (K5) -- the values are
+    // contiguous per part (task order).  2D batches only (m <= 160, cfg1:
+    // 56 MB per 1024-task batch, the ID batches 7.0 -> 5.0 ms); the 3D
+    // blocks' K5 (320 x 512, few resident per SM) lost more to the partial
+    // waves of four launches (cfg3 K5 68 -> 108 ms) than the overlap saves.
+    const int parts = (ntasks >= 512 && max_m <= 160) ? 4 : 1;
+    std::vector<cudaEvent_t> evs;
+    auto drop_events = [&] {
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+      evs.clear();
+    };
+    try {
+      for (int part = 0; part < parts; ++part) {
+        const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
+        if (t1 <= t0) continue;
+        const unsigned nt = static_cast<unsigned>(t1 - t0);
+        const int64_t w0 = tk[static_cast<size_t>(t0)].off, w1 = t1 < ntasks ? tk[static_cast<size_t>(t1)].off : ws;
+        I.begin(3, w1 - w0);
+        if (rowid)
+          launch_k3_ws<true>(I.k, nt, I.stream, d_rc + t0, d_tk + t0, d_rid, d_cid, P.d_ws);
+        else
+          launch_k3_ws<false>(I.k, nt, I.stream, d_rc + t0, d_tk + t0, d_rid, d_cid, P.d_ws);
+        cuda_check(cudaGetLastError(), "k3_sample_ws launch");
+        I.end();
+        I.begin(5, 0);
+        launch_k5(max_m, nt, I.stream, P.d_ws, d_tk + t0, static_cast<int>(nt),
+                  static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0, P.d_vals, P.d_rank + t0,
+                  P.d_skel + t0 * kcap, kcap);
+        cuda_check(cudaGetLastError(), "k5_id launch");
+        I.end();
+        cudaEvent_t ev = nullptr;
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        evs.push_back(ev);
+        cuda_check(cudaEventRecord(ev, I.stream), "event record");
+        cuda_check(cudaStreamWaitEvent(I.cstream, ev, 0), "event wait");
+        const int64_t v0 = tk[static_cast<size_t>(t0)].ooff, v1 = t1 < ntasks ? tk[static_cast<size_t>(t1)].ooff : vals;
+        if (v1 > v0)
+          cuda_check(cudaMemcpyAsync(P.h_vals + v0, P.d_vals + v0, (v1 - v0) * sizeof(double2),
+                                     cudaMemcpyDeviceToHost, I.cstream),
+                     "ID values D2H");
+      }
+    } catch (...) {
+      cudaStreamSynchronize(I.cstream);
+      drop_events();
+      throw;
+    }
     if (timing) cuda_check(cudaStreamSynchronize(I.stream), "ID kernels");
     const auto t_k = now();
     if (timing)
@@ -1062,20 +1099,22 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
                    static_cast<long long>(ntasks), 1e3 * std::chrono::duration<double>(t_prep - t_start).count(),
                    1e3 * std::chrono::duration<double>(t_up - t_prep).count(),
                    1e3 * std::chrono::duration<double>(t_k - t_up).count());
-    cuda_check(cudaMemcpyAsync(P.h_vals, P.d_vals, vals * sizeof(double2), cudaMemcpyDeviceToHost, I.stream),
-               "ID values D2H");
     cuda_check(cudaMemcpyAsync(out.rank.data(), P.d_rank, ntasks * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
                "ID ranks D2H");
     cuda_check(
         cudaMemcpyAsync(out.skel.data(), P.d_skel, ntasks * kcap * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
         "ID skeletons D2H");
     cuda_check(cudaStreamSynchronize(I.stream), "ID batch");
+    const cudaError_t ce = cudaStreamSynchronize(I.cstream);
+    drop_events();
+    cuda_check(ce, "ID values D2H");
     I.collect();
     if (timing)
       std::fprintf(stderr, "[id] D2H %.2f ms (%lld MB)\n", 1e3 * std::chrono::duration<double>(now() - t_k).count(),
                    static_cast<long long>(vals * 16 >> 20));
   } catch (...) {
     cudaStreamSynchronize(I.stream);
+    cudaStreamSynchronize(I.cstream);
     I.collect();
     cleanup();
     throw;

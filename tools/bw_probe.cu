@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <algorithm>
 
 #define CK(x)                                                                    \
   do {                                                                           \
@@ -113,7 +114,7 @@ int main(int argc, char** argv) {
   struct Cfg {
     int warps, chunk, depth, ctas_per_sm;
   } cfgs[] = {{4, 16384, 3, 1}, {8, 8192, 3, 1}};
-  for (size_t sz : {size_t(358) << 20, bytes}) {
+  for (size_t sz : {std::min(size_t(358) << 20, bytes), bytes}) {
     for (int mode : {0, 3, 4}) {
       for (int coop : {0, 1}) {
         for (const Cfg& c : cfgs) {

@@ -33,15 +33,18 @@ def main():
     torch.cuda.synchronize()
     fw = {15: 4, 31: 8, 47: 6}[flags & 63]
     grid = 148
-    nw = (3 if fw <= 4 else 2) * fw  # warps per CTA: consumers, producers (+ x stagers when fw <= 4)
+    dual = bool(flags & (1 << 25))  # two consumers per pair (4-pair layout): warps 3fw..4fw
+    nw = (3 if fw <= 4 else 2) * fw + (fw if dual else 0)  # consumers, producers (+ x stagers when fw <= 4)
     n = grid * nw * 16
     out = np.zeros(n, dtype=np.int64)
     M.lib().midbf_plan_flow_profile(plan._h, out.ctypes.data_as(C.POINTER(C.c_int64)), C.c_int64(n))
     t = out.reshape(grid, nw, 16)
     cons, prod = t[:, :fw, :].reshape(-1, 16), t[:, fw:2 * fw, :].reshape(-1, 16)
     roles = [("consumer", cons), ("producer", prod)]
-    if nw == 3 * fw:
-        roles.append(("x stager", t[:, 2 * fw:, :].reshape(-1, 16)))
+    if fw <= 4:
+        roles.append(("x stager", t[:, 2 * fw:3 * fw, :].reshape(-1, 16)))
+    if dual:
+        roles.append(("consumer 1", t[:, 3 * fw:, :].reshape(-1, 16)))
     clk = 1.965e3  # cycles per us
     ent, pro, end = t[:, :, 14], t[:, :, 15], t[:, :, 11]
     base = ent[ent > 0].min()
