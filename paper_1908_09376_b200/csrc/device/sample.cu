@@ -981,7 +981,7 @@ void EntrySampler::sample_blocks(int64_t ntasks, const int64_t* tasks, const int
 
 void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
                               const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps,
-                              IdBatch& out) {
+                              IdBatch& out, const std::function<void(int64_t, int64_t)>& on_part) {
   Impl& I = *impl_;
   static const bool timing = std::getenv("MIDBF_ID_TIMING") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
@@ -1053,10 +1053,14 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
     // waves of four launches (cfg3 K5 68 -> 108 ms) than the overlap saves.
     const int parts = (ntasks >= 512 && max_m <= 160) ? 4 : 1;
     std::vector<cudaEvent_t> evs;
+    std::vector<cudaEvent_t> done(static_cast<size_t>(parts), nullptr);  // part's results on the host
     auto drop_events = [&] {
       for (cudaEvent_t e : evs) cudaEventDestroy(e);
       evs.clear();
+      for (cudaEvent_t& e : done)
+        if (e) cudaEventDestroy(e), e = nullptr;
     };
+    out.vals = reinterpret_cast<const double*>(P.h_vals);
     try {
       for (int part = 0; part < parts; ++part) {
         const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
@@ -1086,8 +1090,24 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
           cuda_check(cudaMemcpyAsync(P.h_vals + v0, P.d_vals + v0, (v1 - v0) * sizeof(double2),
                                      cudaMemcpyDeviceToHost, I.cstream),
                      "ID values D2H");
+        cuda_check(cudaMemcpyAsync(out.rank.data() + t0, P.d_rank + t0, (t1 - t0) * sizeof(int),
+                                   cudaMemcpyDeviceToHost, I.cstream),
+                   "ID ranks D2H");
+        cuda_check(cudaMemcpyAsync(out.skel.data() + t0 * kcap, P.d_skel + t0 * kcap, (t1 - t0) * kcap * sizeof(int),
+                                   cudaMemcpyDeviceToHost, I.cstream),
+                   "ID skeletons D2H");
+        cuda_check(cudaEventCreateWithFlags(&done[static_cast<size_t>(part)], cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(done[static_cast<size_t>(part)], I.cstream), "event record");
+      }
+      // hand finished parts to the caller (host copy-out) while later parts compute
+      for (int part = 0; part < parts; ++part) {
+        const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
+        if (t1 <= t0) continue;
+        cuda_check(cudaEventSynchronize(done[static_cast<size_t>(part)]), "ID part");
+        if (on_part) on_part(t0, t1);
       }
     } catch (...) {
+      cudaStreamSynchronize(I.stream);
       cudaStreamSynchronize(I.cstream);
       drop_events();
       throw;
@@ -1099,11 +1119,6 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
                    static_cast<long long>(ntasks), 1e3 * std::chrono::duration<double>(t_prep - t_start).count(),
                    1e3 * std::chrono::duration<double>(t_up - t_prep).count(),
                    1e3 * std::chrono::duration<double>(t_k - t_up).count());
-    cuda_check(cudaMemcpyAsync(out.rank.data(), P.d_rank, ntasks * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
-               "ID ranks D2H");
-    cuda_check(
-        cudaMemcpyAsync(out.skel.data(), P.d_skel, ntasks * kcap * sizeof(int), cudaMemcpyDeviceToHost, I.stream),
-        "ID skeletons D2H");
     cuda_check(cudaStreamSynchronize(I.stream), "ID batch");
     const cudaError_t ce = cudaStreamSynchronize(I.cstream);
     drop_events();
@@ -1121,7 +1136,6 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   }
   cleanup();
   I.launched_entries += ws;
-  out.vals = reinterpret_cast<const double*>(P.h_vals);
 }
 
 void EntrySampler::phase_block(int64_t nr, const int64_t* rows, int64_t nc, const int64_t* cols, double* out) {

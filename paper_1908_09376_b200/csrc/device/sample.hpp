@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -38,8 +39,12 @@ class EntrySampler {
     int kcap = 0;
     const double* vals = nullptr;  // pinned, process-wide: valid until the next sample_ids call
   };
+  // on_part(t0, t1), when given, runs on the calling thread as soon as tasks
+  // [t0, t1) are complete on the host side of `out` (values, ranks,
+  // skeletons), while the device still works on later tasks.
   void sample_ids(int64_t ntasks, const int64_t* tasks, const int64_t* row_ids, int64_t n_row_ids,
-                  const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps, IdBatch& out);
+                  const int64_t* col_ids, int64_t n_col_ids, bool rowid, int64_t k_max, double eps, IdBatch& out,
+                  const std::function<void(int64_t, int64_t)>& on_part = {});
   // Phi(rows, cols) (real, column-major nr x nc; rows / cols null: 0..n-1)
   // for the kernels with a phase (FIO 2D/3D, low-rank, x.xi).
   void phase_block(int64_t nr, const int64_t* rows, int64_t nc, const int64_t* cols, double* out);

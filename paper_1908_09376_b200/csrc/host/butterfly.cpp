@@ -591,9 +591,23 @@ IdFn device_ids(dev::EntrySampler& smp, const Filler& fill, const Config& cfg, F
     }
     const auto t0 = std::chrono::steady_clock::now();
     dev::EntrySampler::IdBatch b;
+    // copy-out of each finished part (host memcpy into the result blocks)
+    // while the device computes the next parts
+    auto copy_out = [&](std::int64_t q0, std::int64_t q1) {
+#pragma omp parallel for schedule(dynamic, 16)
+      for (std::int64_t q = q0; q < q1; ++q) {
+        const int k = b.rank[q];
+        if (k < 0) continue;
+        const Index r = rowid ? jobs[q].nr : k, c = rowid ? k : jobs[q].nc;
+        res[q].M = MatXc(r, c);
+        if (r * c > 0)
+          std::memcpy(static_cast<void*>(res[q].M.data()), b.vals + b.ooff[q], static_cast<size_t>(16 * r * c));
+        res[q].pos.assign(b.skel.begin() + q * b.kcap, b.skel.begin() + q * b.kcap + k);
+      }
+    };
     smp.sample_ids(static_cast<std::int64_t>(jobs.size()), tasks.data(), rid.data(),
                    static_cast<std::int64_t>(rid.size()), cid.data(), static_cast<std::int64_t>(cid.size()), rowid,
-                   cfg.rank.k_max, cfg.rank.eps, b);
+                   cfg.rank.k_max, cfg.rank.eps, b, copy_out);
     std::vector<IdJob> redo;
     std::vector<size_t> at;
     for (size_t q = 0; q < jobs.size(); ++q)
@@ -601,16 +615,6 @@ IdFn device_ids(dev::EntrySampler& smp, const Filler& fill, const Config& cfg, F
         redo.push_back(jobs[q]);
         at.push_back(q);
       }
-#pragma omp parallel for schedule(dynamic, 16)
-    for (std::int64_t q = 0; q < static_cast<std::int64_t>(jobs.size()); ++q) {
-      const int k = b.rank[q];
-      if (k < 0) continue;
-      const Index r = rowid ? jobs[q].nr : k, c = rowid ? k : jobs[q].nc;
-      res[q].M = MatXc(r, c);
-      if (r * c > 0)
-        std::memcpy(static_cast<void*>(res[q].M.data()), b.vals + b.ooff[q], static_cast<size_t>(16 * r * c));
-      res[q].pos.assign(b.skel.begin() + q * b.kcap, b.skel.begin() + q * b.kcap + k);
-    }
     static const bool timing = std::getenv("MIDBF_ID_TIMING") != nullptr;
     if (timing)
       std::fprintf(stderr, "[id] batch total %.2f ms (incl. copy-out)\n",
