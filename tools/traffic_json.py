@@ -43,6 +43,12 @@ def main():
                               f"--clock-control none -k regex:'k1_flow|k2_flow' -s 4 -c 2 python bench.py --config {cfg} "
                               f"--steps 2 --warmup 4 (cold-cache, serialised launches)"}
     path = os.path.join(ROOT, "profiles", f"{tag}_traffic.json")
+    try:  # configs not captured this time keep their previous record
+        prev = json.load(open(path))
+    except (OSError, ValueError):
+        prev = {}
+    prev.update(out)
+    out = prev
     json.dump(out, open(path, "w"), indent=1, sort_keys=True)
     for k, v in sorted(out.items()):
         print(k, v["kernel"], v["dram_bytes_per_launch"] / 1e6, "MB", v["duration_ns_median"] / 1e3, "us")
