@@ -18,9 +18,10 @@
 //     multiplies the panel columns with the staged x entries (fp64 FMA), and
 //     after the last panel writes its row (the row value is the ready signal).
 // Dependencies: a strip reads x[x0, x0+n) of each panel from the previous
-// stage's output buffer, which is armed with a sentinel bit pattern before the
-// apply; an x stager polls exactly the entries a strip needs until none is a
-// sentinel (the data is its own ready signal: no flags, no fences) and stages
+// stage's output buffer (stage 0 of the 4-pair layout: from the user's f
+// through in_perm, FlowParams::direct0), which is armed with a sentinel bit
+// pattern before the apply; an x stager polls exactly the entries a strip
+// needs until none is a sentinel (the data is its own ready signal: no flags, no fences) and stages
 // them in shared memory up to two strips ahead of the consumer (x_full /
 // x_empty mbarriers).  The stager is a dedicated warp per pair when the
 // register file allows (<= 4 pairs), else the producer warp's lanes 1..31.

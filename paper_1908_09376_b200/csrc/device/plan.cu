@@ -20,7 +20,8 @@
 //   warps stage by stage (static deal, no counters); each producer streams
 //   its consumer's panels into a ring of shared-memory slots with
 //   cp.async.bulk (TMA bulk copy, mbarrier complete_tx); a strip's x window
-//   is gathered by the stager, which polls the previous stage's output until
+//   is gathered by the stager (stage 0 of the 4-pair layout: straight from f
+//   through col_perm), which polls the previous stage's output until
 //   no entry carries the sentinel (the data is its own ready signal: relaxed
 //   GPU-scope stores and loads, no flags) — there is no stage-wide barrier,
 //   so HBM streaming continues across stage boundaries; each lane owns one
