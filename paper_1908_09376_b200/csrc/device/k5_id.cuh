@@ -17,9 +17,10 @@
 // One CTA of kIdWarps (8 for m <= 256, 4 above) warps per block: rows distributed over lanes (row i
 // -> lane i % 32, register slot i / 32; m <= 32 * kIdRows), squared norms,
 // the column permutation and the Householder vector in shared memory
-// (n <= kIdCols).  Per step warp 0 picks the pivot and builds the reflector,
-// then all warps update interleaved trailing columns (two CTA barriers per
-// step).  Blocks outside those limits,
+// (n <= kIdCols).  Per step warp 0 picks the pivot and builds the reflector
+// (positions are permuted, the columns stay where K3 sampled them: no column
+// swaps through L2), then all warps update interleaved trailing columns, two
+// per pass (two CTA barriers per step).  Blocks outside those limits,
 // and blocks whose first min(m,n,k_max) diagonals hit id_rank's 1e-14 tail
 // trim below the full factorization (the host's fallback case), return
 // rank -1: the caller recomputes them on the host.
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
   double2* R11 = vsh + kIdMaxRows;                          // r11 x r11 (epilogue)
   const int r11 = id_r11(kmax);
   int* perm = reinterpret_cast<int*>(R11 + r11 * r11);
-  __shared__ int sh_p, sh_stop, sh_rank, sh_fb;
+  __shared__ int sh_stop, sh_rank, sh_fb;
   __shared__ double sh_beta;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t = blockIdx.x;
@@ -134,35 +135,23 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         const int op = __shfl_xor_sync(0xffffffffu, bp, o);
         if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
       }
-      if (lane == 0) {
-        sh_p = bp;
-        if (bp != k) {
-          const int tp = perm[k];
-          perm[k] = perm[bp];
-          perm[bp] = tp;
-          double tv = cur[k];
-          cur[k] = cur[bp];
-          cur[bp] = tv;
-          tv = ref[k];
-          ref[k] = ref[bp];
-          ref[bp] = tv;
-        }
+      // Positions are permuted, columns stay where K3 put them: position k
+      // is column perm[k] of the workspace (no column swap through L2, and
+      // the pivot and the reflector are one warp-0 phase)
+      if (lane == 0 && bp != k) {
+        const int tp = perm[k];
+        perm[k] = perm[bp];
+        perm[bp] = tp;
+        double tv = cur[k];
+        cur[k] = cur[bp];
+        cur[bp] = tv;
+        tv = ref[k];
+        ref[k] = ref[bp];
+        ref[bp] = tv;
       }
-    }
-    __syncthreads();
-    const int p = sh_p;
-    if (p != k) {
-      double2* a = B + static_cast<int64_t>(k) * m;
-      double2* b = B + static_cast<int64_t>(p) * m;
-      for (int i = tid; i < m; i += kIdWarps * 32) {
-        const double2 tmp = a[i];
-        a[i] = b[i];
-        b[i] = tmp;
-      }
-    }
-    __syncthreads();
-    if (w == 0) {  // Householder vector from column k (rows k..m-1)
-      double2* col = B + static_cast<int64_t>(k) * m;
+      __syncwarp();
+      // Householder vector from position k's column (rows k..m-1)
+      double2* col = B + static_cast<int64_t>(perm[k]) * m;
       double2 x[kIdRows];
 #pragma unroll
       for (int r = 0; r < kIdRows; ++r) {
@@ -230,7 +219,7 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
 #pragma unroll
       for (int u = 0; u < kPair; ++u) {
         const int j = j0 + u * kIdWarps;
-        const double2* c = B + static_cast<int64_t>(j) * m;
+        const double2* c = B + static_cast<int64_t>(j < n ? perm[j] : 0) * m;
         wr[u] = 0.0;
         wi[u] = 0.0;
 #pragma unroll
@@ -258,7 +247,7 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
       for (int u = 0; u < kPair; ++u) {
         const int j = j0 + u * kIdWarps;
         if (j >= n) break;
-        double2* c = B + static_cast<int64_t>(j) * m;
+        double2* c = B + static_cast<int64_t>(perm[j]) * m;
         const double2 cw = make_double2(wr[u], -wi[u]);  // conj(w)
         double rest = 0.0, ck = 0.0;
 #pragma unroll
@@ -322,7 +311,7 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
   if (r11 >= rank) {  // R11 staged in shared memory, the solution in registers / local memory
     for (int q = tid; q < rank * rank; q += kIdWarps * 32) {
       const int i = q % rank, l = q / rank;
-      R11[q] = i <= l ? B[static_cast<int64_t>(l) * m + i] : make_double2(0, 0);
+      R11[q] = i <= l ? B[static_cast<int64_t>(perm[l]) * m + i] : make_double2(0, 0);
     }
     __syncthreads();
     for (int j = tid; j < n; j += kIdWarps * 32) {
@@ -334,7 +323,7 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         for (int i = 0; i < rank; ++i) at(i) = make_double2(i == j ? 1.0 : 0.0, 0.0);
         continue;
       }
-      const double2* bj = B + static_cast<int64_t>(j) * m;
+      const double2* bj = B + static_cast<int64_t>(pj) * m;
       for (int i = rank - 1; i >= 0; --i) {
         double2 s = bj[i];
         for (int l = i + 1; l < rank; ++l) {
@@ -357,13 +346,13 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
       continue;
     }
     for (int i = rank - 1; i >= 0; --i) {
-      double2 s = B[static_cast<int64_t>(j) * m + i];
+      double2 s = B[static_cast<int64_t>(pj) * m + i];
       for (int l = i + 1; l < rank; ++l) {
-        const double2 q = cmul(B[static_cast<int64_t>(l) * m + i], at(l));
+        const double2 q = cmul(B[static_cast<int64_t>(perm[l]) * m + i], at(l));
         s.x -= q.x;
         s.y -= q.y;
       }
-      at(i) = cdiv(s, B[static_cast<int64_t>(i) * m + i]);
+      at(i) = cdiv(s, B[static_cast<int64_t>(perm[i]) * m + i]);
     }
   }
 }

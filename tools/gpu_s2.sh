@@ -1,6 +1,4 @@
 set -o pipefail; mkdir -p gpurun_out
 make -q -C paper_1908_09376_b200 || make -C paper_1908_09376_b200 -j16 >/dev/null || exit 9
-B=131135
-timeout 300 python tools/flow_ab.py cfg1_unitxi $B $((B+65536)) $((B+65536-48+16)) --rounds 7 > gpurun_out/s17_ab.txt 2>&1
-timeout 300 python tools/flow_ab.py cfg1_unitxi $B $((B+65536)) --transpose --rounds 5 >> gpurun_out/s17_ab.txt 2>&1
-timeout 300 python tools/flow_ab.py cfg0 $B $((B+524288)) $((B+524288+65536)) --rounds 7 >> gpurun_out/s17_ab.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_ids.py tests/test_gpu_fullsize.py tests/test_gpu_lowrank.py tests/test_gpu_sample.py -q -x -p no:cacheprovider > gpurun_out/s18_tests.txt 2>&1; tail -2 gpurun_out/s18_tests.txt
+timeout 600 python tools/fact_timing.py cfg1 cfg1_unitxi cfg3 > gpurun_out/s18_fact.txt 2>&1
