@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <mutex>
 #include <stdexcept>
 #include <vector>
@@ -689,9 +690,11 @@ struct IdPool {
   double2* d_ws = nullptr;
   double2* d_vals = nullptr;
   double2* h_vals = nullptr;
+  int* h_rank = nullptr;  // pinned: per-part D2H without a host-blocking staged copy
+  int* h_skel = nullptr;
   int* d_rank = nullptr;
   int* d_skel = nullptr;
-  int64_t ws_cap = 0, vals_cap = 0, hvals_cap = 0, rank_cap = 0, skel_cap = 0;
+  int64_t ws_cap = 0, vals_cap = 0, hvals_cap = 0, rank_cap = 0, skel_cap = 0, hrank_cap = 0, hskel_cap = 0;
   template <typename T>
   static void grow(T*& p, int64_t& cap, int64_t need, bool pinned, const char* what) {
     if (need <= cap) return;
@@ -1033,6 +1036,8 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   IdPool::grow(P.h_vals, P.hvals_cap, vals, true, "cudaMallocHost ID values");
   IdPool::grow(P.d_rank, P.rank_cap, ntasks, false, "cudaMalloc ranks");
   IdPool::grow(P.d_skel, P.skel_cap, ntasks * kcap, false, "cudaMalloc skeletons");
+  IdPool::grow(P.h_rank, P.hrank_cap, ntasks, true, "cudaMallocHost ranks");
+  IdPool::grow(P.h_skel, P.hskel_cap, ntasks * kcap, true, "cudaMallocHost skeletons");
   int* d_rid = upload(rid.data(), rid.size(), "upload row ids");
   int* d_cid = upload(cid.data(), cid.size(), "upload col ids");
   int4* d_rc = upload(rc.data(), rc.size(), "upload ID tasks");
@@ -1061,6 +1066,14 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
         if (e) cudaEventDestroy(e), e = nullptr;
     };
     out.vals = reinterpret_cast<const double*>(P.h_vals);
+    // MIDBF_ID_TIMING: device timeline of the parts (kernels done / values on host)
+    std::vector<cudaEvent_t> tev;
+    auto tmark = [&](cudaStream_t st) {
+      if (!timing) return;
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreate(&e) == cudaSuccess && cudaEventRecord(e, st) == cudaSuccess) tev.push_back(e);
+    };
+    tmark(I.stream);
     try {
       for (int part = 0; part < parts; ++part) {
         const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
@@ -1080,6 +1093,7 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
                   P.d_skel + t0 * kcap, kcap);
         cuda_check(cudaGetLastError(), "k5_id launch");
         I.end();
+        tmark(I.stream);
         cudaEvent_t ev = nullptr;
         cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
         evs.push_back(ev);
@@ -1090,21 +1104,33 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
           cuda_check(cudaMemcpyAsync(P.h_vals + v0, P.d_vals + v0, (v1 - v0) * sizeof(double2),
                                      cudaMemcpyDeviceToHost, I.cstream),
                      "ID values D2H");
-        cuda_check(cudaMemcpyAsync(out.rank.data() + t0, P.d_rank + t0, (t1 - t0) * sizeof(int),
-                                   cudaMemcpyDeviceToHost, I.cstream),
+        // (pinned staging: a D2H into pageable memory would block the host
+        // until the part is done, serialising the issue of the later parts)
+        cuda_check(cudaMemcpyAsync(P.h_rank + t0, P.d_rank + t0, (t1 - t0) * sizeof(int), cudaMemcpyDeviceToHost,
+                                   I.cstream),
                    "ID ranks D2H");
-        cuda_check(cudaMemcpyAsync(out.skel.data() + t0 * kcap, P.d_skel + t0 * kcap, (t1 - t0) * kcap * sizeof(int),
+        cuda_check(cudaMemcpyAsync(P.h_skel + t0 * kcap, P.d_skel + t0 * kcap, (t1 - t0) * kcap * sizeof(int),
                                    cudaMemcpyDeviceToHost, I.cstream),
                    "ID skeletons D2H");
         cuda_check(cudaEventCreateWithFlags(&done[static_cast<size_t>(part)], cudaEventDisableTiming), "event");
         cuda_check(cudaEventRecord(done[static_cast<size_t>(part)], I.cstream), "event record");
+        tmark(I.cstream);
       }
+      if (timing)
+        std::fprintf(stderr, "[id]   issued at %.2f ms\n", 1e3 * std::chrono::duration<double>(now() - t_up).count());
       // hand finished parts to the caller (host copy-out) while later parts compute
       for (int part = 0; part < parts; ++part) {
         const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
         if (t1 <= t0) continue;
         cuda_check(cudaEventSynchronize(done[static_cast<size_t>(part)]), "ID part");
+        std::memcpy(out.rank.data() + t0, P.h_rank + t0, static_cast<size_t>(t1 - t0) * sizeof(int));
+        std::memcpy(out.skel.data() + t0 * kcap, P.h_skel + t0 * kcap, static_cast<size_t>((t1 - t0) * kcap) * sizeof(int));
+        const auto t_ready = now();
         if (on_part) on_part(t0, t1);
+        if (timing)
+          std::fprintf(stderr, "[id]   part %d: results on host at %.2f ms, copied out at %.2f ms\n", part,
+                       1e3 * std::chrono::duration<double>(t_ready - t_up).count(),
+                       1e3 * std::chrono::duration<double>(now() - t_up).count());
       }
     } catch (...) {
       cudaStreamSynchronize(I.stream);
@@ -1121,6 +1147,18 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
                    1e3 * std::chrono::duration<double>(t_k - t_up).count());
     cuda_check(cudaStreamSynchronize(I.stream), "ID batch");
     const cudaError_t ce = cudaStreamSynchronize(I.cstream);
+    if (timing && ce == cudaSuccess) {
+      std::string line = "[id]   device timeline (ms, kernels done | values on host):";
+      for (size_t q = 1; q < tev.size(); ++q) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[q]);
+        char b[32];
+        std::snprintf(b, sizeof b, " %.2f", ms);
+        line += b;
+      }
+      std::fprintf(stderr, "%s\n", line.c_str());
+    }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
     drop_events();
     cuda_check(ce, "ID values D2H");
     I.collect();
