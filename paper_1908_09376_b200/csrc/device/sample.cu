@@ -1051,12 +1051,14 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   };
   try {
     // Pipelined in parts: part p's V/W values download on a second stream
-    // while part p+1 is sampled (K3) and decomposed (K5) -- the values are
-    // contiguous per part (task order).  2D batches only (m <= 160, cfg1:
-    // 56 MB per 1024-task batch, the ID batches 7.0 -> 5.0 ms); the 3D
-    // blocks' K5 (320 x 512, few resident per SM) lost more to the partial
-    // waves of four launches (cfg3 K5 68 -> 108 ms) than the overlap saves.
-    const int parts = (ntasks >= 512 && max_m <= 160) ? 4 : 1;
+    // (and are copied out on the host, on_part) while part p+1 is sampled
+    // (K3) and decomposed (K5) -- the values are contiguous per part (task
+    // order).  At least 256 tasks per part (about one K5 wave): smaller parts
+    // leave the tall 3D blocks' K5 in partial waves (cfg3 4 parts of 128:
+    // K5 68 -> 109 ms).  Measured (tools/fact_timing.py): cfg1 1024-task
+    // batches 7 -> 3.6 ms, factorize 55 -> 44-46 ms with 4 parts (2: 48,
+    // 8: 49-62); cfg3 512-task batches, 2 parts: 145 -> 134 ms.
+    const int parts = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, ntasks / 256)));
     std::vector<cudaEvent_t> evs;
     std::vector<cudaEvent_t> done(static_cast<size_t>(parts), nullptr);  // part's results on the host
     auto drop_events = [&] {
