@@ -1,6 +1,10 @@
 // C ABI over the host factorization object (include/midbf_b200.h, "host
 // factorization object" section) plus the shared error plumbing.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -91,14 +95,41 @@ int midbf_factorize(midbf_fact_t* out, const midbf_kernel_desc* kernel, int64_t 
     if (!out || !kernel) throw std::invalid_argument("null argument");
     if (!kernel->X || !kernel->Omega || (kernel->dim != 2 && kernel->dim != 3))
       throw std::invalid_argument("factorize needs 2D/3D point sets X and Omega in the kernel description");
+    static const bool timing = std::getenv("MIDBF_FACT_TIMING") != nullptr;
+    const auto t_in = std::chrono::steady_clock::now();
     const midbf::MatXd X = points(kernel->X, kernel->nrows, kernel->dim);
     const midbf::MatXd O = points(kernel->Omega, kernel->ncols, kernel->dim);
     // both trees at a common depth (src/experiment.cpp:140-144)
-    auto tx = midbf::tree::build_tree(X, n0);
-    auto to = midbf::tree::build_tree(O, n0);
+    midbf::tree::ClusterTree tx, to;
+    std::exception_ptr terr;
+#pragma omp parallel sections num_threads(2)
+    {
+#pragma omp section
+      {
+        try {
+          tx = midbf::tree::build_tree(X, n0);
+        } catch (...) {
+#pragma omp critical
+          terr = std::current_exception();
+        }
+      }
+#pragma omp section
+      {
+        try {
+          to = midbf::tree::build_tree(O, n0);
+        } catch (...) {
+#pragma omp critical
+          terr = std::current_exception();
+        }
+      }
+    }
+    if (terr) std::rethrow_exception(terr);
     const int L = std::max(tx.depth, to.depth);
     if (tx.depth != L) tx = midbf::tree::build_tree(X, n0, L);
     if (to.depth != L) to = midbf::tree::build_tree(O, n0, L);
+    if (timing)
+      std::fprintf(stderr, "[factorize] points + trees %.2f ms\n",
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count());
     midbf::bf::Config cfg;
     cfg.rank = {k_max, eps};
     cfg.t = t;
@@ -114,6 +145,10 @@ int midbf_factorize(midbf_fact_t* out, const midbf_kernel_desc* kernel, int64_t 
     } else {
       throw std::invalid_argument("sampler must be 0, 1 or 2");
     }
+    if (timing)
+      std::fprintf(stderr, "[factorize] total %.2f ms (library %.2f ms)\n",
+                   1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now() - t_in).count(),
+                   1e3 * h->stats.seconds);
     *out = h.release();
   });
 }

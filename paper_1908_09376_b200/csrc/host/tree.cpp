@@ -62,8 +62,12 @@ ClusterTree build_tree(const MatXd& X, Index n0, int min_depth) {
   T.dim = dim;
   T.n0 = n0;
   T.perm.resize(static_cast<size_t>(n));
-  std::iota(T.perm.begin(), T.perm.end(), Index{0});
-  std::stable_sort(T.perm.begin(), T.perm.end(), [&](Index a, Index b) { return key[a] < key[b]; });
+  {  // stable order by key = order by (key, index); sorting the pairs avoids the indirect compares
+    std::vector<std::pair<std::uint64_t, Index>> kv(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) kv[static_cast<size_t>(i)] = {key[static_cast<size_t>(i)], i};
+    std::sort(kv.begin(), kv.end());
+    for (Index p = 0; p < n; ++p) T.perm[static_cast<size_t>(p)] = kv[static_cast<size_t>(p)].second;
+  }
   T.pos_of.resize(static_cast<size_t>(n));
   for (Index p = 0; p < n; ++p) T.pos_of[static_cast<size_t>(T.perm[p])] = p;
 
