@@ -261,7 +261,7 @@ class DevicePlan:
             self._h = None
 
     def set_flags(self, pdl=True, prefetch=True, graph=True, flow=True, dmma=True, dmma_flow=True, variant=3,
-                  compress=True, lite=None, chain=True, coop=None, prologue=False):
+                  compress=True, lite=None, chain=True, coop=None, prologue=False, k2_mul4=False):
         """Kernel-path switches: persistent dataflow kernel (flow) for single
         RHS, else per-stage kernels chained with PDL (+ L2 prefetch); graphs;
         multi-RHS on the FP64 tensor cores (dmma), as one dataflow launch per
@@ -279,7 +279,9 @@ class DevicePlan:
         coop: the CTA-per-strip kernel k1_coop for single-RHS applies (True,
         bit 18), never (False, bit 19), or by size (None: small plans).
         prologue: k1_flow's 4-pair layout gathers the permuted input in a
-        stage -1 prologue instead of in stage 0's x windows (bit 24)."""
+        stage -1 prologue instead of in stage 0's x windows (bit 24).
+        k2_mul4: k2_flow's 64-wide tiles multiply complex entries with four
+        real DMMAs instead of Gauss's three (bit 26)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         if chain:
@@ -290,6 +292,8 @@ class DevicePlan:
             f |= 1 << 19
         if prologue:
             f |= 1 << 24
+        if k2_mul4:
+            f |= 1 << 26
         if lite is True:
             f |= 1024
         elif lite is False and compress:

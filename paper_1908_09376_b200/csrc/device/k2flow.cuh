@@ -114,7 +114,10 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 
 }  // namespace k2fdev
 
-template <int NCB>
+// G3: complex products with three real DMMAs (Gauss: P1 = a.re c.re,
+// P2 = a.im c.im, P3 = (a.re + a.im)(c.re + c.im); re = P1 - P2,
+// im = P3 - P1 - P2) instead of four; the kernel is DMMA-bound.
+template <int NCB, bool G3 = true>
 __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant__ K2FParams P) {
   using Cfg = K2FCfg<NCB>;
   constexpr int kW = Cfg::W, kXs = Cfg::XS, kXBuf = Cfg::XBUF, kSlots = Cfg::SLOTS;
@@ -288,11 +291,12 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
     const int row = 8 * rb + g;
     int gc = 0, nit = 0;
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
-      double acc[NCB][2][2];
+      constexpr int NA = G3 ? 3 : 2;  // accumulators per D fragment: re, im (or P1, P2, P3)
+      double acc[NCB][NA][2];
 #pragma unroll
       for (int cb = 0; cb < NCB; ++cb)
 #pragma unroll
-        for (int r = 0; r < 2; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
+        for (int r = 0; r < NA; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
       int4 m = make_int4(0, 0, 0, 0);
       int nq = 1;
       for (int q = 0; q < nq; ++q, ++gc) {
@@ -317,16 +321,26 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
 #pragma unroll
             for (int cb = 0; cb < NCB; ++cb) bv[cb] = make_double2(0, 0);
           }
-          const double naim = -a.y;
+          if (G3) {
+            const double sa = a.x + a.y;
 #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb) {
-            dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
-            dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
-          }
+            for (int cb = 0; cb < NCB; ++cb) {
+              dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
+              dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].y);
+              dmma(acc[cb][NA - 1][0], acc[cb][NA - 1][1], sa, bv[cb].x + bv[cb].y);
+            }
+          } else {
+            const double naim = -a.y;
 #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb) {
-            dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
-            dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
+            for (int cb = 0; cb < NCB; ++cb) {
+              dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
+              dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
+            }
+#pragma unroll
+            for (int cb = 0; cb < NCB; ++cb) {
+              dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
+              dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
+            }
           }
         };
         if (P.mode == 2) {
@@ -339,6 +353,16 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+      if (G3) {  // (P1, P2, P3) -> (re, im) in acc[.][0], acc[.][1]
+#pragma unroll
+        for (int cb = 0; cb < NCB; ++cb)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double p1 = acc[cb][0][i], p2 = acc[cb][1][i];
+            acc[cb][0][i] = p1 - p2;
+            acc[cb][1][i] = acc[cb][NA - 1][i] - p1 - p2;
+          }
       }
       // D fragment: row 8*rb + g, RHS (W/2)*ch + cb*8 + 2t + {0,1}
       const int stage = m.z & 255;

@@ -168,11 +168,18 @@ int flow_setup(int num_sms) {
 template <int NCB>
 int k2flow_setup(int num_sms) {
   const size_t smem = K2FCfg<NCB>::kSmem;
-  cuda_check(cudaFuncSetAttribute(k2_flow<NCB>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+  constexpr bool kG3 = NCB == 4;  // (64-wide tiles: Gauss's three DMMAs by default, see launch_k2flow)
+  cuda_check(cudaFuncSetAttribute(k2_flow<NCB, kG3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
              "k2_flow smem attribute");
-  int per_sm = 0;
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_flow<NCB>, kK2FThreads, smem), "occupancy");
-  return std::min(per_sm * num_sms, kMaxFlowCtas);  // 0: unavailable
+  cuda_check(cudaFuncSetAttribute(k2_flow<NCB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)),
+             "k2_flow smem attribute");
+  int per_sm = 0, per_sm4 = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_flow<NCB, kG3>, kK2FThreads, smem), "occupancy");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm4, k2_flow<NCB, false>, kK2FThreads, smem),
+             "occupancy");
+  return std::min(std::min(per_sm, per_sm4) * num_sms, kMaxFlowCtas);  // 0: unavailable
 }
 
 template <int FW, int FS, int SLOT>
@@ -1358,18 +1365,23 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         off += len;
       }
     }
+    // Gauss's three real DMMAs per complex product on 64-wide tiles (cfg4,
+    // 64 RHS: 377 -> 366 us); the 16-wide tiles measured slower with it (162
+    // -> 166 us at 16 RHS: the extra accumulators spill), so 16 / 32 keep
+    // four.  Flag bit 26 forces four everywhere (A/B).
+    const bool mul4 = (flags & kFlagK2Mul4) != 0;
     switch (wi) {
       case 0:
         cfg.dynamicSmemBytes = K2FCfg<1>::kSmem;
-        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<1>, P), "k2_flow launch");
+        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<1, false>, P), "k2_flow launch");
         break;
       case 1:
         cfg.dynamicSmemBytes = K2FCfg<2>::kSmem;
-        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<2>, P), "k2_flow launch");
+        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<2, false>, P), "k2_flow launch");
         break;
       default:
         cfg.dynamicSmemBytes = K2FCfg<4>::kSmem;
-        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<4>, P), "k2_flow launch");
+        cuda_check(cudaLaunchKernelEx(&cfg, mul4 ? k2_flow<4, false> : k2_flow<4, true>, P), "k2_flow launch");
     }
   }
 }

@@ -25,6 +25,8 @@ constexpr unsigned kFlagNoCoop = 1u << 19;
 // k1_flow: gather the input permutation in a stage -1 prologue instead of in
 // stage 0's x windows (A/B experiments)
 constexpr unsigned kFlagPrologue = 1u << 24;
+// k2_flow: four real DMMAs per complex product instead of Gauss's three (A/B)
+constexpr unsigned kFlagK2Mul4 = 1u << 26;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 

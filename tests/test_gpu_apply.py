@@ -75,10 +75,12 @@ def test_dmma_multi_rhs_matches_oracle(pair, nrhs):
     assert rel(plan.apply(Y, transpose=True), Fo.apply_transpose(Y)) <= TOL
 
 
-@pytest.mark.parametrize("path", ["k2_stage", "k1_stage"])
+@pytest.mark.parametrize("path", ["k2_stage", "k1_stage", "k2_mul4"])
 def test_multi_rhs_fallback_paths(pair, path):
-    """Per-stage DMMA launches (flag bit 13) and the per-stage FMA kernels
-    (bit 11) give the same result as the dataflow default."""
+    """Per-stage DMMA launches (flag bit 13), the per-stage FMA kernels
+    (bit 11) and k2_flow with four real DMMAs per complex product instead of
+    Gauss's three on its 64-wide tiles (bit 26) give the same result as the
+    dataflow default."""
     name, K, Fo, Fm, plan = pair
     X = cvec(Fo.ncols, 18, cols=67)
     want = Fo.apply(X)
@@ -87,6 +89,8 @@ def test_multi_rhs_fallback_paths(pair, path):
         if path == "k2_stage":
             plan.set_flags(dmma_flow=False)
             assert plan.launches(67) == Fo.nfactors  # one DMMA launch per stage
+        elif path == "k2_mul4":
+            plan.set_flags(k2_mul4=True)
         else:
             plan.set_flags(dmma=False)
         got = plan.apply(X)
