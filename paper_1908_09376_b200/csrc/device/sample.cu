@@ -1052,9 +1052,8 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
   };
   try {
     // Pipelined in parts: part p's V/W values download on a second stream
-    // (and are copied out on the host, on_part) while part p+1 is sampled
-    // (K3) and decomposed (K5) -- the values are contiguous per part (task
-    // order).  At least 256 tasks per part (about one K5 wave): smaller parts
+    // (and are copied out on the host, on_part) while part p+1 is
+    // decomposed (K5) -- the values are contiguous per part (task order).  At least 256 tasks per part (about one K5 wave): smaller parts
     // leave the tall 3D blocks' K5 in partial waves (cfg3 4 parts of 128:
     // K5 68 -> 109 ms).  Measured (tools/fact_timing.py): cfg1 1024-task
     // batches 7 -> 3.6 ms, factorize 55 -> 44-46 ms with 4 parts (2: 48,
@@ -1078,18 +1077,19 @@ void EntrySampler::sample_ids(int64_t ntasks, const int64_t* tasks, const int64_
     };
     tmark(I.stream);
     try {
+      // K3 samples every block of the batch in one launch (a CTA per task:
+      // a part's 256 CTAs would leave the SMs half empty), then K5 runs per part
+      I.begin(3, ws);
+      if (rowid)
+        launch_k3_ws<true>(I.k, static_cast<unsigned>(ntasks), I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+      else
+        launch_k3_ws<false>(I.k, static_cast<unsigned>(ntasks), I.stream, d_rc, d_tk, d_rid, d_cid, P.d_ws);
+      cuda_check(cudaGetLastError(), "k3_sample_ws launch");
+      I.end();
       for (int part = 0; part < parts; ++part) {
         const int64_t t0 = ntasks * part / parts, t1 = ntasks * (part + 1) / parts;
         if (t1 <= t0) continue;
         const unsigned nt = static_cast<unsigned>(t1 - t0);
-        const int64_t w0 = tk[static_cast<size_t>(t0)].off, w1 = t1 < ntasks ? tk[static_cast<size_t>(t1)].off : ws;
-        I.begin(3, w1 - w0);
-        if (rowid)
-          launch_k3_ws<true>(I.k, nt, I.stream, d_rc + t0, d_tk + t0, d_rid, d_cid, P.d_ws);
-        else
-          launch_k3_ws<false>(I.k, nt, I.stream, d_rc + t0, d_tk + t0, d_rid, d_cid, P.d_ws);
-        cuda_check(cudaGetLastError(), "k3_sample_ws launch");
-        I.end();
         I.begin(5, 0);
         launch_k5(max_m, nt, I.stream, P.d_ws, d_tk + t0, static_cast<int>(nt),
                   static_cast<int>(std::max<int64_t>(k_max, 0)), eps, rowid ? 1 : 0, P.d_vals, P.d_rank + t0,
