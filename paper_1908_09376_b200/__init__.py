@@ -219,6 +219,8 @@ class DevicePlan:
     """Device arena of one factorization (K1).  apply() takes host numpy
     arrays or device tensors (anything with data_ptr(); complex128)."""
 
+    _apply_fn = None  # bound midbf_apply (apply_ptr)
+
     def __init__(self, handle, owner=None, owned=True):
         self._h = handle
         self._owner = owner
@@ -334,8 +336,15 @@ class DevicePlan:
         return out.value
 
     def apply_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
-        """Raw-pointer apply (device or host pointers, cudaStream_t as int)."""
-        _check(lib().midbf_apply(self._h, vp(f_ptr), vp(g_ptr), nrhs, 1 if transpose else 0, vp(stream)))
+        """Raw-pointer apply (device or host pointers, cudaStream_t as int).
+        The hot loop of a Python caller: the bound C function is cached and
+        the ints go straight through its argtypes."""
+        fn = self._apply_fn
+        if fn is None:
+            fn = self._apply_fn = lib().midbf_apply
+        rc = fn(self._h, f_ptr, g_ptr, nrhs, 1 if transpose else 0, stream)
+        if rc:
+            _check(rc)
 
     def apply_async_ptr(self, f_ptr, g_ptr, nrhs=1, transpose=False, stream=0):
         """Pipelined host-operand apply (midbf_apply_async): returns after

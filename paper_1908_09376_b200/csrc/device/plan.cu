@@ -190,13 +190,20 @@ void flow_launch(FlowParams& P, int grid, cudaStream_t stream, bool lite) {
   cfg.blockDim = dim3(flow_threads<FW>(), 1, 1);
   cfg.dynamicSmemBytes = FlowCfg<FW, FS, SLOT>::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (they wait on each other)
-  attr[0].val.cooperative = P.pdl ? 0 : 1;  // chained: 1 CTA per SM fits only once the previous grid left
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // chained applies (flow.cuh P.pdl)
-  attr[1].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
+  // chained applies (flow.cuh P.pdl): programmatic dependent launch and no
+  // cooperative guarantee (1 CTA per SM fits only once the previous grid
+  // left); else a cooperative launch (all CTAs co-resident: they wait on each
+  // other).  One attribute each way (fewer attributes, cheaper launch).
+  cudaLaunchAttribute attr[1];
+  if (P.pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   if (P.prof)
     cuda_check(cudaLaunchKernelEx(&cfg, k1_flow<FW, FS, SLOT, true>, P), "k1_flow launch");
   else if (lite)
@@ -1204,13 +1211,16 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
     cfg.blockDim = dim3(kCoopWarps * 32, 1, 1);
     cfg.dynamicSmemBytes = kCoopSmem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = P.pdl ? 0 : 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = P.pdl ? 1 : 0;
+    cudaLaunchAttribute attr[1];  // as flow_launch
+    if (P.pdl) {
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+    } else {
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 1;
     cuda_check(cudaLaunchKernelEx(&cfg, k1_coop<kCoopWarps>, P), "k1_coop launch");
     return;
   }
