@@ -16,13 +16,30 @@ namespace {
 
 constexpr int kLevels = 21;
 
+// Bit b of a 21-bit value moved to bit 2b (spread2) or 3b (spread3).
+std::uint64_t spread2(std::uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+std::uint64_t spread3(std::uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
 // Interleave `dim` 21-bit coordinates; axis a lands at bit offset dim-1-a of
 // every digit (axis 0 most significant).
 std::uint64_t interleave(const std::uint32_t* q, int dim) {
-  std::uint64_t key = 0;
-  for (int b = kLevels - 1; b >= 0; --b)
-    for (int a = 0; a < dim; ++a) key = (key << 1) | ((q[a] >> b) & 1u);
-  return key;
+  if (dim == 2) return (spread2(q[0]) << 1) | spread2(q[1]);
+  return (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
 }
 
 }  // namespace
@@ -52,7 +69,8 @@ ClusterTree build_tree(const MatXd& X, Index n0, int min_depth) {
   for (Index i = 0; i < n; ++i) {
     std::uint32_t q[3] = {0, 0, 0};
     for (int a = 0; a < dim; ++a) {
-      const double s = std::floor(std::ldexp((X(i, a) - lo[a]) / ext, kLevels));
+      // (x - lo) / ext * 2^21: scaling by a power of two is exact, as ldexp
+      const double s = std::floor((X(i, a) - lo[a]) / ext * scale);
       q[a] = static_cast<std::uint32_t>(std::min(std::max(s, 0.0), top));
     }
     key[static_cast<size_t>(i)] = interleave(q, dim);
@@ -62,11 +80,20 @@ ClusterTree build_tree(const MatXd& X, Index n0, int min_depth) {
   T.dim = dim;
   T.n0 = n0;
   T.perm.resize(static_cast<size_t>(n));
-  {  // stable order by key = order by (key, index); sorting the pairs avoids the indirect compares
-    std::vector<std::pair<std::uint64_t, Index>> kv(static_cast<size_t>(n));
-    for (Index i = 0; i < n; ++i) kv[static_cast<size_t>(i)] = {key[static_cast<size_t>(i)], i};
-    std::sort(kv.begin(), kv.end());
-    for (Index p = 0; p < n; ++p) T.perm[static_cast<size_t>(p)] = kv[static_cast<size_t>(p)].second;
+  {  // stable order by key: LSD radix sort, 8 bits per pass over the key's 21*dim bits
+    std::vector<Index> tmp(static_cast<size_t>(n));
+    std::iota(T.perm.begin(), T.perm.end(), Index{0});
+    const int bits = kLevels * dim;
+    for (int sh = 0; sh < bits; sh += 8) {
+      size_t cnt[257] = {0};
+      for (Index i = 0; i < n; ++i) ++cnt[((key[static_cast<size_t>(i)] >> sh) & 0xffu) + 1];
+      for (int b = 0; b < 256; ++b) cnt[b + 1] += cnt[b];
+      for (Index p = 0; p < n; ++p) {
+        const Index i = T.perm[static_cast<size_t>(p)];
+        tmp[cnt[(key[static_cast<size_t>(i)] >> sh) & 0xffu]++] = i;
+      }
+      T.perm.swap(tmp);
+    }
   }
   T.pos_of.resize(static_cast<size_t>(n));
   for (Index p = 0; p < n; ++p) T.pos_of[static_cast<size_t>(T.perm[p])] = p;
