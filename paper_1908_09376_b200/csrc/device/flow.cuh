@@ -448,8 +448,8 @@ struct FlowCfg {
   static constexpr size_t kXArea = size_t(FW) * 2 * kXWin * 16;
   static constexpr size_t kAddArea = size_t(FW) * 2 * 32 * 16;  // per-row identity sums (stager -> consumer)
   static constexpr size_t kCtxArea = size_t(FW) * kQN * sizeof(StripCtx);
-  // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2]
-  static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 4) * 8;
+  // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2], a_full[2]
+  static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 6) * 8;
   static constexpr size_t kSmem = kSlotArea + kXArea + kAddArea + kCtxArea + kBarArea;
   static_assert(kSmem <= 232448, "k1_flow exceeds the 227 KB dynamic shared memory of a CTA");
 };
@@ -482,19 +482,20 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   StripCtx* ctx = reinterpret_cast<StripCtx*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kAddArea) + c * kQN;
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kAddArea + Cfg::kCtxArea) +
-      c * (2 * FS + 2 * kQN + 4);
+      c * (2 * FS + 2 * kQN + 6);
   uint64_t* full = bars;
   uint64_t* empty = bars + FS;
   uint64_t* cfull = bars + 2 * FS;
   uint64_t* cempty = bars + 2 * FS + kQN;
   uint64_t* xfull = bars + 2 * FS + 2 * kQN;      // x window of strip k staged (buffer k & 1)
   uint64_t* xempty = bars + 2 * FS + 2 * kQN + 2;  // buffer k & 1 released by the consumer
+  uint64_t* afull = bars + 2 * FS + 2 * kQN + 4;   // identity sums of strip k in asum[k & 1] (separate stagers)
   if (producer && lane == 0) {
     // xfull: one arrival from a separate stager warp (after its warp
     // barrier), or one per lane of the producer warp's in-warp stager, which
     // must not use warp barriers while lane 0 runs the TMA loop (FW > 4 hung
     // at cfg3 with them)
-    for (int s = 0; s < 2 * FS + 2 * kQN + 4; ++s)
+    for (int s = 0; s < 2 * FS + 2 * kQN + 6; ++s)
       mbar_init(&bars[s], (!kSep && s >= 2 * FS + 2 * kQN && s < 2 * FS + 2 * kQN + 2) ? 31 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -586,10 +587,20 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         FLOW_T(13, stage_x<NS, CMP>(C, d0 ? P.in : io.x + (io.x_par ? par_off : 0), d0 ? P.in_perm : io.xperm,
                                     xb + b * kXWin, sl, d0 ? P.in : P.stagebuf,
                                     d0 ? P.in + P.in_len : P.stagebuf + 2 * P.par_elems));
-        if (CMP && kSep && C.mapped == 1) {  // per-row sums of the identity entries, off the consumer's critical path
-          // (separate stager warps only; with the in-warp stager of FW > 4
-          // the consumers sum in place)
-          __syncwarp(mask);
+      }
+      if (kSep) {
+        __syncwarp(mask);
+        if (arriver) mbar_arrive(&xfull[b]);
+      } else {
+        mbar_arrive(&xfull[b]);  // each lane's own entries (release)
+      }
+      if (CMP && kSep) {
+        // Per-row sums of the identity entries, off the consumer's critical
+        // path: formed after x_full is signalled (the consumer needs them
+        // only after its panel sums) and signalled on a_full (separate
+        // stager warps only; with the in-warp stager of FW > 4 the
+        // consumers sum in place).
+        if (C.mapped == 1 && C.s.xcols <= kXWin && P.nodeps != 2) {
           const double2* xs = xb + b * kXWin;
           for (int r = sl; r < C.s.h; r += NS) {
             const unsigned below = (1u << r) - 1u;
@@ -605,12 +616,8 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             asum[b * 32 + r] = make_double2(ar, ai);
           }
         }
-      }
-      if (kSep) {
         __syncwarp(mask);
-        if (arriver) mbar_arrive(&xfull[b]);
-      } else {
-        mbar_arrive(&xfull[b]);  // each lane's own entries (release)
+        if (arriver) mbar_arrive(&afull[b]);
       }
     }
     if (!waited) dep_wait();
@@ -814,6 +821,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
         yi += __shfl_down_sync(0xffffffffu, yi, 16);
       }
+      if (CMP && kSep) mbar_wait(&afull[k & 1], (k >> 1) & 1);  // (signalled for every strip)
       if (CMP && kSep && C.mapped == 1 && row < h) {  // identity parts: the row's sum, formed by the x stager
         const double2 t = asum[(k & 1) * 32 + row];
         yr += t.x;
