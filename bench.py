@@ -345,6 +345,8 @@ def main():
     k3_line = {"launches": ks["k3_launches"], "entries": ks["k3_entries"], "device_seconds": ks["k3_seconds"],
                "entries_per_s": k3_rate, "k5_launches": ks["k5_launches"], "k5_device_seconds": ks["k5_seconds"],
                "note": "CUDA events around every k3_sample* launch of the timed factorization"}
+    if K.desc.kind == M.KIND_FIO2D:  # ncu capture of one cfg1 K3 launch (profiles/r2b_k3.md)
+        k3_line["fp64_pipe_busy_ncu"] = {"active": 0.599, "elapsed": 0.564, "source": "profiles/r2b_k3.md"}
     if fpe and k3_rate:
         k3_line.update({"fp64_flops_per_entry": fpe, "fp64_tflops": k3_rate * fpe / 1e12, "fp64_peak": FP64_DFMA_TFLOPS,
                         "fp64_frac": k3_rate * fpe / 1e12 / FP64_DFMA_TFLOPS,
