@@ -141,17 +141,32 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// Blocking wait.  The suspend-time hint lets the hardware park the thread
-// until the phase completes instead of re-polling: with 8 waiting warps per
-// SM, back-to-back polls otherwise contend with the TMA complete_tx updates.
+// Blocking wait: try_wait suspends the thread for an implementation-defined
+// time per attempt.  An explicit suspend-time hint of 1e6 ns (round 1) was
+// measured slightly slower than the default (second session, same-box A/B:
+// cfg1 50.8 -> 50.5 us, cfg2 224.3 -> 223.2 us, cfg4 unchanged);
+// -DMIDBF_MBAR_HINT=<ns> restores a hint.
+#ifndef MIDBF_MBAR_HINT
+#define MIDBF_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if MIDBF_MBAR_HINT == 0
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
+      "r"(parity), "r"(MIDBF_MBAR_HINT)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
