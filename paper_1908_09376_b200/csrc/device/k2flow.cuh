@@ -117,7 +117,7 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
 // G3: complex products with three real DMMAs (Gauss: P1 = a.re c.re,
 // P2 = a.im c.im, P3 = (a.re + a.im)(c.re + c.im); re = P1 - P2,
 // im = P3 - P1 - P2) instead of four; the kernel is DMMA-bound.
-template <int NCB, bool G3 = true>
+template <int NCB, bool G3 = true, bool RB2 = true>
 __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant__ K2FParams P) {
   using Cfg = K2FCfg<NCB>;
   constexpr int kW = Cfg::W, kXs = Cfg::XS, kXBuf = Cfg::XBUF, kSlots = Cfg::SLOTS;
@@ -286,17 +286,24 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
     }
   } else {
     // ------------------------------ consumers ------------------------------
+    // Warp tile: RBW row blocks of 8 rows x CBW column blocks of 8 RHS.
+    // RBW = 2 on the 64-wide tiles (16 rows x 16 RHS: per K step 2 A and 2 B
+    // fragment loads for 12 DMMAs), else 1 (8 rows x W/2 RHS).
+    constexpr int RBW = (NCB == 4 && RB2) ? 2 : 1;
+    constexpr int CBW = NCB / RBW;
     const int g = lane >> 2, t = lane & 3;
-    const int rb = w & 3, ch = w >> 2;  // row block, RHS half
-    const int row = 8 * rb + g;
+    const int rb0 = RBW == 2 ? 2 * (w & 1) : (w & 3);  // first row block
+    const int ch = RBW == 2 ? (w >> 1) : (w >> 2);     // RHS group of CBW * 8
     int gc = 0, nit = 0;
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
       constexpr int NA = G3 ? 3 : 2;  // accumulators per D fragment: re, im (or P1, P2, P3)
-      double acc[NCB][NA][2];
+      double acc[RBW][CBW][NA][2];
 #pragma unroll
-      for (int cb = 0; cb < NCB; ++cb)
+      for (int rr = 0; rr < RBW; ++rr)
 #pragma unroll
-        for (int r = 0; r < NA; ++r) acc[cb][r][0] = acc[cb][r][1] = 0.0;
+        for (int cb = 0; cb < CBW; ++cb)
+#pragma unroll
+          for (int r = 0; r < NA; ++r) acc[rr][cb][r][0] = acc[rr][cb][r][1] = 0.0;
       int4 m = make_int4(0, 0, 0, 0);
       int nq = 1;
       for (int q = 0; q < nq; ++q, ++gc) {
@@ -309,37 +316,42 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         const int krem = min(kK2Kc, m.w - q * kK2Kc);
         const int kfull = krem & ~3;
         const int pst = m.z >> 8;
-        const double2* Ps = Pb + slot * kK2PBuf + 8 * rb + g;
-        const double2* Xs = Xb + slot * kXBuf + t * kXs + ch * (kW / 2) + g;
+        const double2* Ps = Pb + slot * kK2PBuf + 8 * rb0 + g;
+        const double2* Xs = Xb + slot * kXBuf + t * kXs + ch * (CBW * 8) + g;
         auto step = [&](int kk, bool live) {
-          double2 a = Ps[(kk + t) * pst];
-          double2 bv[NCB];
+          double2 a[RBW], bv[CBW];
 #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb) bv[cb] = Xs[kk * kXs + cb * 8];
+          for (int rr = 0; rr < RBW; ++rr) a[rr] = Ps[(kk + t) * pst + 8 * rr];
+#pragma unroll
+          for (int cb = 0; cb < CBW; ++cb) bv[cb] = Xs[kk * kXs + cb * 8];
           if (!live) {  // K tail: stale slot contents must not reach the sums
-            a = make_double2(0, 0);
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) bv[cb] = make_double2(0, 0);
+            for (int rr = 0; rr < RBW; ++rr) a[rr] = make_double2(0, 0);
+#pragma unroll
+            for (int cb = 0; cb < CBW; ++cb) bv[cb] = make_double2(0, 0);
           }
-          if (G3) {
-            const double sa = a.x + a.y;
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) {
-              dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
-              dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].y);
-              dmma(acc[cb][NA - 1][0], acc[cb][NA - 1][1], sa, bv[cb].x + bv[cb].y);
-            }
-          } else {
-            const double naim = -a.y;
+          for (int rr = 0; rr < RBW; ++rr) {
+            if (G3) {
+              const double sa = a[rr].x + a[rr].y;
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) {
-              dmma(acc[cb][0][0], acc[cb][0][1], a.x, bv[cb].x);
-              dmma(acc[cb][1][0], acc[cb][1][1], a.x, bv[cb].y);
-            }
+              for (int cb = 0; cb < CBW; ++cb) {
+                dmma(acc[rr][cb][0][0], acc[rr][cb][0][1], a[rr].x, bv[cb].x);
+                dmma(acc[rr][cb][1][0], acc[rr][cb][1][1], a[rr].y, bv[cb].y);
+                dmma(acc[rr][cb][NA - 1][0], acc[rr][cb][NA - 1][1], sa, bv[cb].x + bv[cb].y);
+              }
+            } else {
+              const double naim = -a[rr].y;
 #pragma unroll
-            for (int cb = 0; cb < NCB; ++cb) {
-              dmma(acc[cb][0][0], acc[cb][0][1], naim, bv[cb].y);
-              dmma(acc[cb][1][0], acc[cb][1][1], a.y, bv[cb].x);
+              for (int cb = 0; cb < CBW; ++cb) {
+                dmma(acc[rr][cb][0][0], acc[rr][cb][0][1], a[rr].x, bv[cb].x);
+                dmma(acc[rr][cb][1][0], acc[rr][cb][1][1], a[rr].x, bv[cb].y);
+              }
+#pragma unroll
+              for (int cb = 0; cb < CBW; ++cb) {
+                dmma(acc[rr][cb][0][0], acc[rr][cb][0][1], naim, bv[cb].y);
+                dmma(acc[rr][cb][1][0], acc[rr][cb][1][1], a[rr].y, bv[cb].x);
+              }
             }
           }
         };
@@ -354,51 +366,57 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
-      if (G3) {  // (P1, P2, P3) -> (re, im) in acc[.][0], acc[.][1]
+      if (G3) {  // (P1, P2, P3) -> (re, im) in acc[..][0], acc[..][1]
 #pragma unroll
-        for (int cb = 0; cb < NCB; ++cb)
+        for (int rr = 0; rr < RBW; ++rr)
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const double p1 = acc[cb][0][i], p2 = acc[cb][1][i];
-            acc[cb][0][i] = p1 - p2;
-            acc[cb][1][i] = acc[cb][NA - 1][i] - p1 - p2;
-          }
+          for (int cb = 0; cb < CBW; ++cb)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const double p1 = acc[rr][cb][0][i], p2 = acc[rr][cb][1][i];
+              acc[rr][cb][0][i] = p1 - p2;
+              acc[rr][cb][1][i] = acc[rr][cb][NA - 1][i] - p1 - p2;
+            }
       }
-      // D fragment: row 8*rb + g, RHS (W/2)*ch + cb*8 + 2t + {0,1}
+      // D fragment: row 8*(rb0 + rr) + g, RHS (CBW*8)*ch + cb*8 + 2t + {0,1}
       const int stage = m.z & 255;
       const K2FStage io = P.st[stage];
       const bool last = stage + 1 == P.nstages;
       const int ab = P.strips[item].pad_[1];
-      if (ab >= 0 && row < m.y) {  // identity columns: Y(row, :) += X(input row, :)
-        const int xa = __ldg(P.addx + ab + row);
-        if (xa >= 0) {
-          const K2FStage xin = P.st[stage];
-          const double2* xr = xin.xperm ? xin.x + __ldg(xin.xperm + xa) : xin.x + static_cast<int64_t>(xa) * xin.xld;
-          const int64_t rs = xin.xperm ? xin.xld : 1;  // user operand: column-major; stage buffers: row-major
 #pragma unroll
-          for (int cb = 0; cb < NCB; ++cb)
+      for (int rr = 0; rr < RBW; ++rr) {
+        const int row = 8 * (rb0 + rr) + g;
+        if (ab >= 0 && row < m.y) {  // identity columns: Y(row, :) += X(input row, :)
+          const int xa = __ldg(P.addx + ab + row);
+          if (xa >= 0) {
+            const K2FStage xin = P.st[stage];
+            const double2* xr = xin.xperm ? xin.x + __ldg(xin.xperm + xa) : xin.x + static_cast<int64_t>(xa) * xin.xld;
+            const int64_t rs = xin.xperm ? xin.xld : 1;  // user operand: column-major; stage buffers: row-major
+#pragma unroll
+            for (int cb = 0; cb < CBW; ++cb)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int rhs = (CBW * 8) * ch + cb * 8 + 2 * t + i;
+                if (rhs < P.ncv) {
+                  const double2 v = xin.xperm ? __ldg(xr + rhs * rs) : flowdev::ld_cg(xr + rhs);
+                  acc[rr][cb][0][i] += v.x;
+                  acc[rr][cb][1][i] += v.y;
+                }
+              }
+          }
+        }
+        if (row < m.y) {
+          int idx = m.x + row;
+          if (io.yperm) idx = __ldg(io.yperm + idx);
+#pragma unroll
+          for (int cb = 0; cb < CBW; ++cb)
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-              const int rhs = (kW / 2) * ch + cb * 8 + 2 * t + i;
-              if (rhs < P.ncv) {
-                const double2 v = xin.xperm ? __ldg(xr + rhs * rs) : flowdev::ld_cg(xr + rhs);
-                acc[cb][0][i] += v.x;
-                acc[cb][1][i] += v.y;
-              }
+              const int rhs = (CBW * 8) * ch + cb * 8 + 2 * t + i;
+              if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : idx * io.yld + rhs] =
+                  make_double2(acc[rr][cb][0][i], acc[rr][cb][1][i]);
             }
         }
-      }
-      if (row < m.y) {
-        int idx = m.x + row;
-        if (io.yperm) idx = __ldg(io.yperm + idx);
-#pragma unroll
-        for (int cb = 0; cb < NCB; ++cb)
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int rhs = (kW / 2) * ch + cb * 8 + 2 * t + i;
-            if (rhs < P.ncv) io.y[last ? rhs * io.yld + idx : idx * io.yld + rhs] =
-                make_double2(acc[cb][0][i], acc[cb][1][i]);
-          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&done[nit % kK2FDone]);
