@@ -458,11 +458,11 @@ def main():
         # algorithmic flops = 8 * nrhs * total_nnz; k2_flow skips
         # the exact identity columns of V-type ID strips on 32/64-wide tiles
         flops = 8.0 * F.total_nnz * nrhs
-        # real DMMA flops per complex MAC: 64-wide tiles (slices of 33..64
-        # RHS) use Gauss's three real products (6 flops), narrower ones four
+        # real DMMA flops per complex MAC: 32- and 64-wide tiles (slices of
+        # 17..64 RHS) use Gauss's three real products (6 flops), 16-wide four
         gauss = not (args.flags & (1 << 26))
         slices = [min(64, nrhs - c) for c in range(0, nrhs, 64)]
-        per_mac = sum((6.0 if gauss and w > 32 else 8.0) * w for w in slices) / nrhs
+        per_mac = sum((6.0 if gauss and w > 16 else 8.0) * w for w in slices) / nrhs
         executed = per_mac * (plan.k2_bytes() / 16) * nrhs
         tf = flops / (ms_step * 1e-3) / 1e12
         etf = executed / (ms_step * 1e-3) / 1e12
@@ -475,7 +475,7 @@ def main():
                     "dmma_flops_per_complex_mac": per_mac,
                     "note": "achieved = 8*nrhs*total_nnz / apply time (SURVEY.md 8(d)); executed_* = the entries "
                             "k2_flow multiplies (identity columns of V-type strips skipped, midbf_plan_k2_bytes) x the "
-                            "real DMMA flops per complex MAC (6 with Gauss's three products on 64-wide tiles, else 8); "
+                            "real DMMA flops per complex MAC (6 with Gauss's three products on 32- / 64-wide tiles, else 8); "
                             f"FP64 tensor-core (DMMA) k2_flow: {launches} cooperative dataflow launch(es) per "
                             "apply (one per 64-RHS slice) in one graph; traffic = DRAM bytes per launch"}
     line = {

@@ -236,7 +236,7 @@ int midbf_plan_k2_bytes(midbf_plan_t plan, int transpose, int64_t* out);
  * non-cooperatively; process-wide, chained grids on different streams are
  * serialised), bits18 / 19 force / forbid k1_coop, bit24 k1_flow's stage -1
  * input prologue (instead of stage 0 gathering f itself), bit26 four real
- * DMMAs per complex product on k2_flow's 64-wide tiles (instead of Gauss's
+ * DMMAs per complex product on k2_flow's 32- / 64-wide tiles (instead of Gauss's
  * three).  A new plan starts at 0x3F | bit17. */
 int midbf_plan_set_flags(midbf_plan_t plan, unsigned flags);
 int midbf_plan_get_flags(midbf_plan_t plan, unsigned* out);

@@ -282,8 +282,8 @@ class DevicePlan:
         bit 18), never (False, bit 19), or by size (None: small plans).
         prologue: k1_flow's 4-pair layout gathers the permuted input in a
         stage -1 prologue instead of in stage 0's x windows (bit 24).
-        k2_mul4: k2_flow's 64-wide tiles multiply complex entries with four
-        real DMMAs instead of Gauss's three (bit 26)."""
+        k2_mul4: k2_flow's 32- / 64-wide tiles multiply complex entries with
+        four real DMMAs instead of Gauss's three (bit 26)."""
         f = (1 if pdl else 0) | (2 if prefetch else 0) | (4 if graph else 0) | (8 if flow else 0)
         f |= (0 if dmma else 2048) | (0 if dmma_flow else 8192) | ((variant & 3) << 4) | (0 if compress else 512)
         if chain:

@@ -168,7 +168,7 @@ int flow_setup(int num_sms) {
 template <int NCB>
 int k2flow_setup(int num_sms) {
   const size_t smem = K2FCfg<NCB>::kSmem;
-  constexpr bool kG3 = NCB == 4;  // (64-wide tiles: Gauss's three DMMAs by default, see launch_k2flow)
+  constexpr bool kG3 = NCB >= 2;  // (32- / 64-wide tiles: Gauss's three DMMAs by default, see launch_k2flow)
   cuda_check(cudaFuncSetAttribute(k2_flow<NCB, kG3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)),
              "k2_flow smem attribute");
@@ -1375,10 +1375,11 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         off += len;
       }
     }
-    // Gauss's three real DMMAs per complex product on 64-wide tiles (cfg4,
-    // 64 RHS: 377 -> 366 us); the 16-wide tiles measured slower with it (162
-    // -> 166 us at 16 RHS: the extra accumulators spill), so 16 / 32 keep
-    // four.  Flag bit 26 forces four everywhere (A/B).
+    // Gauss's three real DMMAs per complex product on 32- and 64-wide tiles
+    // (cfg4, 64 RHS: 377 -> 366 us; 32 RHS 209 -> 194 us, 24 RHS 204 -> 189
+    // us); the 16-wide tiles measured slower with it (162 -> 166 us at 16
+    // RHS, 158 -> 161 at 8), so they keep four.  Flag bit 26 forces four
+    // everywhere (A/B).
     const bool mul4 = (flags & kFlagK2Mul4) != 0;
     switch (wi) {
       case 0:
@@ -1387,7 +1388,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
         break;
       case 1:
         cfg.dynamicSmemBytes = K2FCfg<2>::kSmem;
-        cuda_check(cudaLaunchKernelEx(&cfg, k2_flow<2, false>, P), "k2_flow launch");
+        cuda_check(cudaLaunchKernelEx(&cfg, mul4 ? k2_flow<2, false> : k2_flow<2, true>, P), "k2_flow launch");
         break;
       default:
         cfg.dynamicSmemBytes = K2FCfg<4>::kSmem;
