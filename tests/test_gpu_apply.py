@@ -62,11 +62,12 @@ def test_few_rhs_dispatch(pair, nrhs):
     assert plan.launches(nrhs) == (nrhs if nrhs <= 2 else 1)
 
 
-@pytest.mark.parametrize("nrhs", [64, 70, 16, 33, 100])
+@pytest.mark.parametrize("nrhs", [64, 70, 16, 24, 33, 100])
 def test_dmma_multi_rhs_matches_oracle(pair, nrhs):
     """K2 (FP64 tensor cores) over full and ragged slices, each on the
     narrowest 16/32/64-wide tile that covers it (70 = 64 + a 16-wide 6,
-    100 = 64 + a 64-wide 36, 33 on a 64-wide tile), both directions; the
+    100 = 64 + a 64-wide 36, 24 on a 32-wide tile, 33 on a 64-wide tile;
+    Gauss's three products on the 32- / 64-wide ones), both directions; the
     widths alternate between launches on the same plan."""
     name, K, Fo, Fm, plan = pair
     X = cvec(Fo.ncols, 16, cols=nrhs)
