@@ -725,6 +725,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         }
         continue;
       }
+      const long long t_setup = PROF ? clock64() : 0;
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
       const StageIO io = P.st[C.s.stage];
       const bool d0 = kSep && P.direct0 && C.s.stage == 0;  // (4-pair layout only: plan.cu)
@@ -734,6 +735,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       const bool fast = C.s.xcols <= kXWin;
       double2* xcur = xb + (k & 1) * kXWin;
       const unsigned long long g_ctx = PROF ? globaltimer_ns() : 0;
+      if (PROF) tm[5] += clock64() - t_setup;
       FLOW_T(4, mbar_wait(&xfull[k & 1], (k >> 1) & 1));  // staged by the producer warp's lanes 1..31
       const unsigned long long g_x = PROF ? globaltimer_ns() : 0;
       // Lane mapping: strips of <= 16 rows use both half-warps (row = lane&15,
@@ -831,6 +833,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         }
         cb += n;
       }
+      const long long t_epi = PROF ? clock64() : 0;
       double yr = (ar0 + ar1) + (ar2 + ar3), yi = (ai0 + ai1) + (ai2 + ai3);
       if (halves) {  // odd-column half-warp adds into the even one (fixed order)
         yr += __shfl_down_sync(0xffffffffu, yr, 16);
@@ -866,6 +869,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       MIDBF_DCHECK(!(row < h && cpar == 0) || (io.y ? (yout + yidx >= P.stagebuf && yout + yidx < P.stagebuf + 2 * P.par_elems)
                                                     : (yidx >= 0 && yidx < P.out_len)),
                    "k1_flow row store outside its buffer");
+      if (PROF) tm[6] += clock64() - t_epi;
       FLOW_T(7, if (row < h && cpar == 0) st_signal(yout + yidx, make_double2(unsentinel(yr), unsentinel(yi))));
       if (PROF && lane == 0 && C.s.seg0 < kProfStrips) {  // per-strip timeline (ns): ctx ready, x staged, stored
         long long* ts = P.prof + kProfStripBase + 3 * static_cast<int64_t>(C.s.seg0);

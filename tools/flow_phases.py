@@ -15,7 +15,7 @@ import bench  # noqa: E402
 import paper_1908_09376_b200 as M  # noqa: E402
 
 NAMES = ["P: wait ctx", "P: wait empty slot", "C: wait ctx", "X: wait ctx", "C: wait x staged",
-         "-", "-", "C: y store", "C: wait full slot", "C: FMA loop", "total", "-",
+         "C: strip setup", "C: epilogue (sums, identity)", "C: y store", "C: wait full slot", "C: FMA loop", "total", "-",
          "X: wait x buffer free", "X: gather+poll"]
 
 
