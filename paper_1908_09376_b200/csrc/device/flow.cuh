@@ -91,6 +91,7 @@ struct FlowParams {
   int64_t arena_len;  // complex entries of the arena (checked builds)
   int64_t out_len;    // entries of `out` (checked builds)
   int direct0;        // stage 0 gathers the user input through in_perm itself (no stage -1 prologue)
+  int nstages;        // entries of st (copied into shared memory at launch)
 };
 
 // A panel as k1_flow streams it.
@@ -465,7 +466,8 @@ struct FlowCfg {
   static constexpr size_t kCtxArea = size_t(FW) * kQN * sizeof(StripCtx);
   // per pair: full[FS], empty[FS], ctx_full[kQN], ctx_empty[kQN], x_full[2], x_empty[2], a_full[2]
   static constexpr size_t kBarArea = size_t(FW) * (2 * FS + 2 * kQN + 6) * 8;
-  static constexpr size_t kSmem = kSlotArea + kXArea + kAddArea + kCtxArea + kBarArea;
+  static constexpr size_t kStageArea = size_t(kMaxStages) * sizeof(StageIO);  // the stage table, per CTA
+  static constexpr size_t kSmem = kSlotArea + kXArea + kAddArea + kCtxArea + kBarArea + kStageArea;
   static_assert(kSmem <= 232448, "k1_flow exceeds the 227 KB dynamic shared memory of a CTA");
 };
 
@@ -505,6 +507,10 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
   uint64_t* xfull = bars + 2 * FS + 2 * kQN;      // x window of strip k staged (buffer k & 1)
   uint64_t* xempty = bars + 2 * FS + 2 * kQN + 2;  // buffer k & 1 released by the consumer
   uint64_t* afull = bars + 2 * FS + 2 * kQN + 4;   // identity sums of strip k in asum[k & 1] (separate stagers)
+  // the stage table (plan constants) in shared memory: read at every strip
+  StageIO* stsm = reinterpret_cast<StageIO*>(smem + Cfg::kSlotArea + Cfg::kXArea + Cfg::kAddArea + Cfg::kCtxArea +
+                                             Cfg::kBarArea);
+  for (int i = threadIdx.x; i < P.nstages; i += blockDim.x) stsm[i] = P.st[i];
   if (producer && lane == 0) {
     // xfull: one arrival from a separate stager warp (after its warp
     // barrier), or one per lane of the producer warp's in-warp stager, which
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       if (k >= 2) FLOW_T(12, mbar_wait(&xempty[b], ((k >> 1) - 1) & 1));
       if (C.s.xcols <= kXWin && P.nodeps != 2) {
-        const StageIO io = P.st[C.s.stage];
+        const StageIO io = stsm[C.s.stage];
         const bool d0 = kSep && P.direct0 && C.s.stage == 0;
         FLOW_T(13, stage_x<NS, CMP>(C, d0 ? P.in : io.x + (io.x_par ? par_off : 0), d0 ? P.in_perm : io.xperm,
                                     xb + b * kXWin, sl, d0 ? P.in : P.stagebuf,
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
       }
       const long long t_setup = PROF ? clock64() : 0;
       const int h = C.s.h, nseg = C.s.nseg, y0 = C.s.y0;
-      const StageIO io = P.st[C.s.stage];
+      const StageIO io = stsm[C.s.stage];
       const bool d0 = kSep && P.direct0 && C.s.stage == 0;  // (4-pair layout only: plan.cu)
       const double2* xin = d0 ? P.in : io.x + (io.x_par ? par_off : 0);
       const int* xperm = d0 ? P.in_perm : io.xperm;

@@ -1187,6 +1187,7 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.nodeps = static_cast<int>((flags >> 6) & 7u);  // bits 6-8: timing experiments
   if ((flags & 4096u) && d_prof) P.prof = d_prof;  // bit 12: phase timers (experiments)
   P.st = D.d_stageio;
+  P.nstages = static_cast<int>(D.stages.size());
   P.out = out;
   P.in = in;
   P.in_flag = next_in_flag;
