@@ -92,6 +92,7 @@ struct FlowParams {
   int64_t out_len;    // entries of `out` (checked builds)
   int direct0;        // stage 0 gathers the user input through in_perm itself (no stage -1 prologue)
   int nstages;        // entries of st (copied into shared memory at launch)
+  int l2_first;       // panels streamed with an L2 evict_first policy (flag bit 27)
 };
 
 // A panel as k1_flow streams it.
@@ -174,6 +175,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// The same copy with an L2 eviction-priority policy (createpolicy).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -676,6 +691,7 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
         }
       };
       unsigned q = 0;
+      const uint64_t pol = P.l2_first ? l2_evict_first_policy() : 0ull;
       for (int k = 0; k < nmine; ++k) {
         prefetch(kf <= k);
         const int sc = k % kQN;
@@ -697,7 +713,10 @@ __global__ void __launch_bounds__(flow_threads<FW>(), 1) k1_flow(const __grid_co
             MIDBF_DCHECK(C.g[j].off >= 0 && C.g[j].off + static_cast<int64_t>(col + ncol) * h <= P.arena_len,
                          "k1_flow panel outside the arena");
             mbar_expect_tx(&full[slot], bytes);
-            bulk_g2s(slots + size_t(slot) * SLOT, src + static_cast<int64_t>(col) * h, bytes, &full[slot]);
+            if (P.l2_first)
+              bulk_g2s_hint(slots + size_t(slot) * SLOT, src + static_cast<int64_t>(col) * h, bytes, &full[slot], pol);
+            else
+              bulk_g2s(slots + size_t(slot) * SLOT, src + static_cast<int64_t>(col) * h, bytes, &full[slot]);
             prefetch(false);
           }
         }

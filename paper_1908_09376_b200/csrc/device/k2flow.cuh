@@ -92,6 +92,7 @@ struct K2FParams {
   // dependency waits, 2 stream only (no math), 3 math only (no loads)
   int mode;
   int64_t arena_len;  // complex entries of the arena (checked builds)
+  int l2_first;       // panels streamed with an L2 evict_first policy (plan.hpp kFlagK2L2Normal)
   K2FStage st[kMaxStages];
 };
 
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
   if (w == kK2FConsumers || w == kK2FConsumers + 1) {
     // ---------------- producers: panels (no waits) | inputs (dependencies) -------
     const bool xrole = w == kK2FConsumers + 1;
+    const uint64_t pol = P.l2_first ? flowdev::l2_evict_first_policy() : 0ull;
     int gc = 0;  // chunks issued
     int started = 0;  // this CTA's strips started
     for (int item = blockIdx.x; item < P.nstrips; item += gridDim.x) {
@@ -216,7 +218,12 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
           if (load) {
             if (!prun) {
               MIDBF_DCHECK(!(ok && lane < kK2Kc) || (psrc >= 0 && psrc + h <= P.arena_len), "k2_flow panel column");
-              if (ok && lane < kK2Kc) flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
+              if (ok && lane < kK2Kc) {
+                if (P.l2_first)
+                  flowdev::bulk_g2s_hint(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot], pol);
+                else
+                  flowdev::bulk_g2s(pd + c * kK2Ps, P.arena + psrc, h * 16u, &full[slot]);
+              }
             } else {
               unsigned r = runs;
               while (r) {
@@ -225,7 +232,12 @@ __global__ void __launch_bounds__(kK2FThreads, 2) k2_flow(const __grid_constant_
                 const int r1 = r ? __ffs(r) - 1 : kval;
                 const int64_t src = __shfl_sync(0xffffffffu, psrc, r0);
                 MIDBF_DCHECK(lane != 0 || (src >= 0 && src + int64_t(r1 - r0) * h <= P.arena_len), "k2_flow panel run");
-                if (lane == 0) flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
+                if (lane == 0) {
+                  if (P.l2_first)
+                    flowdev::bulk_g2s_hint(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot], pol);
+                  else
+                    flowdev::bulk_g2s(pd + r0 * h, P.arena + src, (r1 - r0) * h * 16u, &full[slot]);
+                }
               }
             }
           }

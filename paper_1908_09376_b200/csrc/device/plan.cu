@@ -1197,6 +1197,7 @@ void Plan::launch_flow(int d, const double2* in, double2* out, cudaStream_t stre
   P.arena_len = D.arena_elems + D.farena_elems;
   P.out_len = d == 0 ? nrows : ncols;
   P.pdl = (flags & kFlagChain) ? 1 : 0;
+  P.l2_first = (flags & kFlagL2Normal) ? 0 : 1;
   // Stage 0 gathers the user input through the permutation itself (no
   // stage -1 prologue), its permutation indices loaded before the chained
   // wait; 4-pair layout only (separate stager warps): measured cfg1 51.7 ->
@@ -1337,6 +1338,7 @@ void Plan::launch_k2flow(int d, const double2* in, double2* out, int64_t nrhs, c
   P.nstrips = static_cast<int>(D.nstrips);
   P.nstages = ns;
   P.mode = static_cast<int>((flags >> 14) & 3u);
+  P.l2_first = (flags & kFlagK2L2Normal) ? 0 : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kK2FThreads, 1, 1);
   cfg.stream = stream;

@@ -27,6 +27,14 @@ constexpr unsigned kFlagNoCoop = 1u << 19;
 constexpr unsigned kFlagPrologue = 1u << 24;
 // k2_flow: four real DMMAs per complex product instead of Gauss's three (A/B)
 constexpr unsigned kFlagK2Mul4 = 1u << 26;
+// k1_flow / k2_flow stream the factor panels with an L2 evict_first policy,
+// so the streamed payload (read once per apply) does not displace the
+// intermediate stage vectors the dependency polls read from L2; bits 27 / 28
+// restore the default policy (A/B).  Same-box A/B, chained applies: cfg1
+// 50.2 -> 47.6 us, cfg1_unitxi 33.8 -> 32.4, cfg3 127.2 -> 121.4, cfg2
+// 227.7 -> 223.1.
+constexpr unsigned kFlagL2Normal = 1u << 27;
+constexpr unsigned kFlagK2L2Normal = 1u << 28;
 constexpr int kMaxFlowCtas = 1024;  // per-CTA epoch words
 constexpr int kFlowColumns = 2;     // nrhs up to this: k1_flow per column (Plan::flow_ok)
 
