@@ -41,9 +41,11 @@ constexpr int kIdCols = 512;           // n <= 512
 // epilogue's triangular solves; r11 = k_max when 1 <= k_max <= 64, else 0
 // and the epilogue reads R from the workspace).
 constexpr int kIdR11Max = 64;
-template <int ROWS>
+// Plus one column slot per warp: the warp's pivot candidate for the next
+// step, kept on chip so the reflector does not re-read it through L2.
+template <int ROWS, int WARPS>
 constexpr size_t id_smem(int r11 = 0) {
-  return size_t(kIdCols) * (8 + 8 + 8 + 4) + size_t(32 * ROWS) * 16 + size_t(r11) * r11 * 16 + 64;
+  return size_t(kIdCols) * (8 + 8 + 8 + 4) + size_t(32 * ROWS) * 16 * (1 + WARPS) + size_t(r11) * r11 * 16 + 64;
 }
 __host__ __device__ inline int id_r11(int kmax) { return kmax >= 1 && kmax <= kIdR11Max ? kmax : 0; }
 
@@ -92,8 +94,11 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
   double2* R11 = vsh + kIdMaxRows;                          // r11 x r11 (epilogue)
   const int r11 = id_r11(kmax);
   int* perm = reinterpret_cast<int*>(R11 + r11 * r11);
+  double2* cbuf = reinterpret_cast<double2*>(perm + kIdCols);  // [kIdWarps][kIdMaxRows] candidate columns
   __shared__ int sh_stop, sh_rank, sh_fb;
   __shared__ double sh_beta;
+  __shared__ double cand_v[kIdWarps];  // per-warp pivot candidates of the next step (largest
+  __shared__ int cand_p[kIdWarps];     // downdated norm, lowest position), set by the trailing update
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int t = blockIdx.x;
   if (t >= ntasks) return;
@@ -127,14 +132,21 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
     if (w == 0) {  // pivot: largest remaining norm, lowest index on ties
       double bv = -1.0;
       int bp = n;
-      for (int j = k + lane; j < n; j += 32)
-        if (cur[j] > bv) bv = cur[j], bp = j;
+      if (k == 0) {
+        for (int j = lane; j < n; j += 32)
+          if (cur[j] > bv) bv = cur[j], bp = j;
+      } else if (lane < kIdWarps) {  // the update of step k - 1 left one candidate per warp
+        bv = cand_v[lane];
+        bp = cand_p[lane];
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
+        if (o >= kIdWarps && k > 0) continue;  // candidates sit in lanes 0 .. kIdWarps-1 (uniform branch)
         const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
         const int op = __shfl_xor_sync(0xffffffffu, bp, o);
         if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
       }
+      bp = __shfl_sync(0xffffffffu, bp, 0);
       // Positions are permuted, columns stay where K3 put them: position k
       // is column perm[k] of the workspace (no column swap through L2, and
       // the pivot and the reflector are one warp-0 phase)
@@ -152,11 +164,14 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
       __syncwarp();
       // Householder vector from position k's column (rows k..m-1)
       double2* col = B + static_cast<int64_t>(perm[k]) * m;
+      // the winning candidate's warp (position bp was dealt to warp (bp - k) mod kIdWarps
+      // by the update of step k - 1) left the updated column in its slot
+      const double2* src = k == 0 ? col : cbuf + ((bp - k) % kIdWarps) * kIdMaxRows;
       double2 x[kIdRows];
 #pragma unroll
       for (int r = 0; r < kIdRows; ++r) {
         const int i = lane + 32 * r;
-        x[r] = (i >= k && i < m) ? col[i] : make_double2(0, 0);
+        x[r] = (i >= k && i < m) ? src[i] : make_double2(0, 0);
       }
       double xs = 0.0;
 #pragma unroll
@@ -175,12 +190,14 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         const double aa = sqrt(nrm2(a0));
         const double2 ph = aa == 0.0 ? make_double2(1.0, 0.0) : make_double2(a0.x / aa, a0.y / aa);
         const double2 v0 = make_double2(a0.x + ph.x * xn, a0.y + ph.y * xn);
+        const double iv = 1.0 / nrm2(v0);
+        const double2 v0i = make_double2(v0.x * iv, -v0.y * iv);  // 1 / v0
         double vs = 0.0;
 #pragma unroll
         for (int r = 0; r < kIdRows; ++r) {
           const int i = lane + 32 * r;
           if (i > k && i < m) {
-            x[r] = cdiv(x[r], v0);
+            x[r] = cmul(x[r], v0i);
             vs += nrm2(x[r]);
             col[i] = x[r];
           }
@@ -213,6 +230,8 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
     // two columns per pass (kIdRows <= 8) so their loads and reduction
     // chains overlap
     constexpr int kPair = kIdRows <= 8 ? 2 : 1;
+    double best_v = -1.0;
+    int best_p = n;
     for (int j0 = k + 1 + w; j0 < n; j0 += kPair * kIdWarps) {
       double2 cv[kPair][kIdRows];
       double wr[kPair], wi[kPair];
@@ -248,31 +267,42 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         const int j = j0 + u * kIdWarps;
         if (j >= n) break;
         double2* c = B + static_cast<int64_t>(perm[j]) * m;
-        const double2 cw = make_double2(wr[u], -wi[u]);  // conj(w)
-        double rest = 0.0, ck = 0.0;
+        const double2 cw = make_double2(beta * wr[u], -beta * wi[u]);  // beta conj(w)
+        double ck = 0.0;
 #pragma unroll
         for (int r = 0; r < kIdRows; ++r) {
           const int i = lane + 32 * r;
           if (i >= k && i < m) {
-            const double2 d = cmul(make_double2(beta * v[r].x, beta * v[r].y), cw);
+            const double2 d = cmul(v[r], cw);
             cv[u][r].x -= d.x;
             cv[u][r].y -= d.y;
             c[i] = cv[u][r];
             if (i == k) ck = nrm2(cv[u][r]);
-            else rest += nrm2(cv[u][r]);
           }
         }
         ck = __shfl_sync(0xffffffffu, ck, k & 31);
         double cj = cur[j] - ck;
         double rj = ref[j];
-        if (cj < 0.0 || cj <= 1e-12 * rj) {  // recompute guard
+        if (cj < 0.0 || cj <= 1e-12 * rj) {  // recompute guard (warp-uniform, rare): rows below k
+          double rest = 0.0;
+#pragma unroll
+          for (int r = 0; r < kIdRows; ++r) {
+            const int i = lane + 32 * r;
+            if (i > k && i < m) rest += nrm2(cv[u][r]);
+          }
           const double s = wsum(rest);
           cj = m - k > 1 ? s : 0.0;
           rj = cj;
         }
         if (lane == 0) cur[j] = cj, ref[j] = rj;
+        if (cj > best_v) {  // warp-uniform; positions ascend within a warp: lowest on ties
+          best_v = cj, best_p = j;
+#pragma unroll
+          for (int r = 0; r < kIdRows; ++r) cbuf[w * kIdMaxRows + lane + 32 * r] = cv[u][r];
+        }
       }
     }
+    if (lane == 0) cand_v[w] = best_v, cand_p[w] = best_p;
     __syncthreads();
   }
   const int steps = k;

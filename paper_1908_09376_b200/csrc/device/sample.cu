@@ -662,13 +662,13 @@ void launch_k5(int64_t max_m, unsigned grid, cudaStream_t st, double2* ws, const
   // resident blocks): 2D k = 30 blocks are 150 x {64, 120} (t k = 150
   // samples), 3D k = 64 blocks 320 x {64, 512}
   if (max_m <= 160)
-    go(k5_id<5, 8>, id_smem<5>(id_r11(kmax)), 256);
+    go(k5_id<5, 8>, id_smem<5, 8>(id_r11(kmax)), 256);
   else if (max_m <= 256)
-    go(k5_id<8, 8>, id_smem<8>(id_r11(kmax)), 256);
+    go(k5_id<8, 8>, id_smem<8, 8>(id_r11(kmax)), 256);
   else if (max_m <= 320)
-    go(k5_id<10, 4>, id_smem<10>(id_r11(kmax)), 128);
+    go(k5_id<10, 4>, id_smem<10, 4>(id_r11(kmax)), 128);
   else
-    go(k5_id<16, 4>, id_smem<16>(id_r11(kmax)), 128);
+    go(k5_id<16, 4>, id_smem<16, 4>(id_r11(kmax)), 128);
 }
 
 template <class T>
