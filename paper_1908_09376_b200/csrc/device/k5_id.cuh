@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
   for (int j = tid; j < n; j += kIdWarps * 32) perm[j] = j;
   __syncthreads();
 
+  int ridx[kIdRows];  // this lane's row per slot, clamped into the column
+#pragma unroll
+  for (int r = 0; r < kIdRows; ++r) ridx[r] = min(lane + 32 * r, m - 1);
+
   int k = 0;
   for (; k < cap; ++k) {
     if (w == 0) {  // pivot: largest remaining norm, lowest index on ties
@@ -228,8 +232,17 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
     }
     // trailing columns (warp w: k+1+w, k+1+w+kIdWarps, ...): c -= beta v (v^H c),
     // two columns per pass (kIdRows <= 8) so their loads and reduction
-    // chains overlap
+    // chains overlap.  Branch-free: every row below m is loaded (rows above k
+    // hold finished R entries and meet v = 0, rows past m re-read row m - 1
+    // and meet v = 0), only rows k..m-1 are stored back; explicit fma chains.
     constexpr int kPair = kIdRows <= 8 ? 2 : 1;
+    unsigned smask = 0;  // slots this lane stores: k <= row < m
+#pragma unroll
+    for (int r = 0; r < kIdRows; ++r) {
+      const int i = lane + 32 * r;
+      smask |= (i >= k && i < m) ? 1u << r : 0u;
+    }
+    const int kslot = k >> 5;
     double best_v = -1.0;
     int best_p = n;
     for (int j0 = k + 1 + w; j0 < n; j0 += kPair * kIdWarps) {
@@ -242,44 +255,60 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         wr[u] = 0.0;
         wi[u] = 0.0;
 #pragma unroll
-        for (int r = 0; r < kIdRows; ++r) {
-          const int i = lane + 32 * r;
-          cv[u][r] = (j < n && i >= k && i < m) ? c[i] : make_double2(0, 0);
-        }
+        for (int r = 0; r < kIdRows; ++r) cv[u][r] = c[ridx[r]];
       }
 #pragma unroll
       for (int u = 0; u < kPair; ++u)
 #pragma unroll
-        for (int r = 0; r < kIdRows; ++r) {
-          const double2 q = cmulc(cv[u][r], v[r]);
-          wr[u] += q.x;
-          wi[u] += q.y;
+        for (int r = 0; r < kIdRows; ++r) {  // w += conj(c) v
+          wr[u] = fma(cv[u][r].x, v[r].x, wr[u]);
+          wr[u] = fma(cv[u][r].y, v[r].y, wr[u]);
+          wi[u] = fma(cv[u][r].x, v[r].y, wi[u]);
+          wi[u] = fma(-cv[u][r].y, v[r].x, wi[u]);
         }
+      if constexpr (kPair == 2) {
+        // The four sums reduce together: the first two rounds halve what
+        // each lane carries (6 shuffled doubles instead of 20), then
+        // lanes 0 / 8 / 16 / 24 hold wr0 / wi0 / wr1 / wi1 and broadcast them.
+        const bool hi = lane & 16, b3 = lane & 8;
+        double k0 = hi ? wr[1] : wr[0], k1 = hi ? wi[1] : wi[0];
+        k0 += __shfl_xor_sync(0xffffffffu, hi ? wr[0] : wr[1], 16);
+        k1 += __shfl_xor_sync(0xffffffffu, hi ? wi[0] : wi[1], 16);
+        double t = b3 ? k1 : k0;
+        t += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        wr[0] = __shfl_sync(0xffffffffu, t, 0);
+        wi[0] = __shfl_sync(0xffffffffu, t, 8);
+        wr[1] = __shfl_sync(0xffffffffu, t, 16);
+        wi[1] = __shfl_sync(0xffffffffu, t, 24);
+      } else {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int u = 0; u < kPair; ++u) {
-          wr[u] += __shfl_xor_sync(0xffffffffu, wr[u], o);
-          wi[u] += __shfl_xor_sync(0xffffffffu, wi[u], o);
-        }
+          for (int u = 0; u < kPair; ++u) {
+            wr[u] += __shfl_xor_sync(0xffffffffu, wr[u], o);
+            wi[u] += __shfl_xor_sync(0xffffffffu, wi[u], o);
+          }
+      }
 #pragma unroll
       for (int u = 0; u < kPair; ++u) {
         const int j = j0 + u * kIdWarps;
         if (j >= n) break;
         double2* c = B + static_cast<int64_t>(perm[j]) * m;
         const double2 cw = make_double2(beta * wr[u], -beta * wi[u]);  // beta conj(w)
-        double ck = 0.0;
+        double2 ek = make_double2(0, 0);                                 // row k's slot
 #pragma unroll
-        for (int r = 0; r < kIdRows; ++r) {
-          const int i = lane + 32 * r;
-          if (i >= k && i < m) {
-            const double2 d = cmul(v[r], cw);
-            cv[u][r].x -= d.x;
-            cv[u][r].y -= d.y;
-            c[i] = cv[u][r];
-            if (i == k) ck = nrm2(cv[u][r]);
-          }
+        for (int r = 0; r < kIdRows; ++r) {  // c -= v cw
+          cv[u][r].x = fma(-v[r].x, cw.x, cv[u][r].x);
+          cv[u][r].x = fma(v[r].y, cw.y, cv[u][r].x);
+          cv[u][r].y = fma(-v[r].x, cw.y, cv[u][r].y);
+          cv[u][r].y = fma(-v[r].y, cw.x, cv[u][r].y);
+          if (smask >> r & 1u) c[lane + 32 * r] = cv[u][r];
+          if (r == kslot) ek = cv[u][r];
         }
+        double ck = nrm2(ek);
         ck = __shfl_sync(0xffffffffu, ck, k & 31);
         double cj = cur[j] - ck;
         double rj = ref[j];
