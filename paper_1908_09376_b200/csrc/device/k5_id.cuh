@@ -127,9 +127,9 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
   for (int j = tid; j < n; j += kIdWarps * 32) perm[j] = j;
   __syncthreads();
 
-  int ridx[kIdRows];  // this lane's row per slot, clamped into the column
+  unsigned lmask = 0;  // slots of this lane that are rows of the block (row < m)
 #pragma unroll
-  for (int r = 0; r < kIdRows; ++r) ridx[r] = min(lane + 32 * r, m - 1);
+  for (int r = 0; r < kIdRows; ++r) lmask |= (lane + 32 * r < m) ? 1u << r : 0u;
 
   int k = 0;
   for (; k < cap; ++k) {
@@ -232,9 +232,10 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
     }
     // trailing columns (warp w: k+1+w, k+1+w+kIdWarps, ...): c -= beta v (v^H c),
     // two columns per pass (kIdRows <= 8) so their loads and reduction
-    // chains overlap.  Branch-free: every row below m is loaded (rows above k
-    // hold finished R entries and meet v = 0, rows past m re-read row m - 1
-    // and meet v = 0), only rows k..m-1 are stored back; explicit fma chains.
+    // chains overlap.  Every row below m is loaded (rows above k hold finished
+    // R entries and meet v = 0) through a per-lane column pointer with
+    // immediate slot offsets, only rows k..m-1 are stored back; explicit fma
+    // chains.
     constexpr int kPair = kIdRows <= 8 ? 2 : 1;
     unsigned smask = 0;  // slots this lane stores: k <= row < m
 #pragma unroll
@@ -251,11 +252,11 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
 #pragma unroll
       for (int u = 0; u < kPair; ++u) {
         const int j = j0 + u * kIdWarps;
-        const double2* c = B + static_cast<int64_t>(j < n ? perm[j] : 0) * m;
+        const double2* c = B + static_cast<int64_t>(j < n ? perm[j] : 0) * m + lane;
         wr[u] = 0.0;
         wi[u] = 0.0;
 #pragma unroll
-        for (int r = 0; r < kIdRows; ++r) cv[u][r] = c[ridx[r]];
+        for (int r = 0; r < kIdRows; ++r) cv[u][r] = (lmask >> r & 1u) ? c[32 * r] : make_double2(0, 0);
       }
 #pragma unroll
       for (int u = 0; u < kPair; ++u)
@@ -296,17 +297,21 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
       for (int u = 0; u < kPair; ++u) {
         const int j = j0 + u * kIdWarps;
         if (j >= n) break;
-        double2* c = B + static_cast<int64_t>(perm[j]) * m;
+        double2* c = B + static_cast<int64_t>(perm[j]) * m + lane;
         const double2 cw = make_double2(beta * wr[u], -beta * wi[u]);  // beta conj(w)
-        double2 ek = make_double2(0, 0);                                 // row k's slot
 #pragma unroll
         for (int r = 0; r < kIdRows; ++r) {  // c -= v cw
           cv[u][r].x = fma(-v[r].x, cw.x, cv[u][r].x);
           cv[u][r].x = fma(v[r].y, cw.y, cv[u][r].x);
           cv[u][r].y = fma(-v[r].x, cw.y, cv[u][r].y);
           cv[u][r].y = fma(-v[r].y, cw.x, cv[u][r].y);
-          if (smask >> r & 1u) c[lane + 32 * r] = cv[u][r];
-          if (r == kslot) ek = cv[u][r];
+          if (smask >> r & 1u) c[32 * r] = cv[u][r];
+        }
+        double2 ek = cv[u][0];  // row k's slot (uniform: slot 0 while k < 32)
+        if (kslot != 0) {
+#pragma unroll
+          for (int r = 1; r < kIdRows; ++r)
+            if (r == kslot) ek = cv[u][r];
         }
         double ck = nrm2(ek);
         ck = __shfl_sync(0xffffffffu, ck, k & 31);
