@@ -246,8 +246,12 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
     const int kslot = k >> 5;
     double best_v = -1.0;
     int best_p = n;
+    double2 cv[kPair][kIdRows];  // slots past row m stay zero (never loaded, v = 0 there)
+#pragma unroll
+    for (int u = 0; u < kPair; ++u)
+#pragma unroll
+      for (int r = 0; r < kIdRows; ++r) cv[u][r] = make_double2(0, 0);
     for (int j0 = k + 1 + w; j0 < n; j0 += kPair * kIdWarps) {
-      double2 cv[kPair][kIdRows];
       double wr[kPair], wi[kPair];
 #pragma unroll
       for (int u = 0; u < kPair; ++u) {
@@ -256,7 +260,8 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         wr[u] = 0.0;
         wi[u] = 0.0;
 #pragma unroll
-        for (int r = 0; r < kIdRows; ++r) cv[u][r] = (lmask >> r & 1u) ? c[32 * r] : make_double2(0, 0);
+        for (int r = 0; r < kIdRows; ++r)
+          if (lmask >> r & 1u) cv[u][r] = c[32 * r];
       }
 #pragma unroll
       for (int u = 0; u < kPair; ++u)
@@ -285,13 +290,16 @@ __global__ void __launch_bounds__(kIdWarps * 32, kIdRows <= 5 ? 2 : 1) k5_id(dou
         wr[1] = __shfl_sync(0xffffffffu, t, 16);
         wi[1] = __shfl_sync(0xffffffffu, t, 24);
       } else {
+        static_assert(kPair == 1, "one or two columns per pass");
+        // the real and the imaginary sum share the rounds after the first:
+        // lanes 0 / 16 end with wr / wi (5 shuffled doubles instead of 10)
+        const bool hi = lane & 16;
+        double t = hi ? wi[0] : wr[0];
+        t += __shfl_xor_sync(0xffffffffu, hi ? wr[0] : wi[0], 16);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int u = 0; u < kPair; ++u) {
-            wr[u] += __shfl_xor_sync(0xffffffffu, wr[u], o);
-            wi[u] += __shfl_xor_sync(0xffffffffu, wi[u], o);
-          }
+        for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        wr[0] = __shfl_sync(0xffffffffu, t, 0);
+        wi[0] = __shfl_sync(0xffffffffu, t, 16);
       }
 #pragma unroll
       for (int u = 0; u < kPair; ++u) {
